@@ -1,0 +1,65 @@
+"""Full oracle training runs for the accuracy gates (calls only oracle/ + synthdata/).
+
+Writes tests/golden/oracle_runs/<name>.json with per-epoch test loss / errors of
+the oracle's sequential SGD (or sync-batch SGD) on BASELINE.json workloads:
+
+  python scripts/oracle_reference_runs.py config1_seq        # tiny, 15 epochs (minutes)
+  python scripts/oracle_reference_runs.py config3_seq        # large, 15 epochs (~1 h)
+
+The lr schedule is lr0 * 0.9**e (BASELINE.json configs[1]; reading R6).
+"""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import synthdata as sd  # noqa: E402
+from oracle import Oracle  # noqa: E402
+
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden", "oracle_runs")
+
+RUNS = {
+    # name: (workload, mode, batch, epochs)
+    "config0_sync1": ("config0", "sync", 1, 1),
+    "config1_seq": ("config1", "seq", 1, 15),
+    "config1_sync64": ("config1", "sync", 64, 15),
+    "config2_seq": ("config2", "seq", 1, 15),
+    "config3_seq": ("config3", "seq", 1, 15),
+    "config3_sync64_e1": ("config3", "sync", 64, 1),
+    "config2_sync64_e1": ("config2", "sync", 64, 1),
+}
+
+
+def run(name):
+    wname, mode, batch, epochs = RUNS[name]
+    w = sd.WORKLOADS[wname]
+    d = sd.make_dataset(w)
+    o = Oracle(sd.ARCHS[w.arch])
+    p = sd.init_params(w.seed, o.blocks()).astype(np.float64)
+    rec = {"run": name, "workload": wname, "arch": w.arch, "mode": mode, "batch": batch, "epochs": epochs,
+           "data_sha256": d.sha256(), "lr0": w.lr0, "per_epoch": []}
+    t0 = time.time()
+    for e in range(epochs):
+        lr = w.lr0 * 0.9 ** e
+        if mode == "seq":
+            p, sl = o.train_sgd(p, d.x_train, d.y_train, lr)
+        else:
+            p, sl = o.train_sync(p, d.x_train, d.y_train, lr, batch)
+        tl, te = o.evaluate(p, d.x_test, d.y_test)
+        rec["per_epoch"].append({"epoch": e + 1, "lr": lr, "train_mean_loss": sl / len(d.y_train),
+                                 "test_mean_loss": tl, "test_errors": te, "n_test": len(d.y_test),
+                                 "elapsed_s": time.time() - t0})
+        print(name, rec["per_epoch"][-1], flush=True)
+        os.makedirs(OUT, exist_ok=True)
+        with open(os.path.join(OUT, name + ".json"), "w") as f:
+            json.dump(rec, f, indent=1)
+    if epochs == 1 or name.startswith("config0"):
+        np.save(os.path.join(OUT, name + "_params.npy"), p)
+
+
+if __name__ == "__main__":
+    for n in sys.argv[1:]:
+        run(n)

@@ -1,0 +1,373 @@
+"""Pins of the CPU oracle against things other than itself (CPU only, -m "not gpu").
+
+Each test names what pins it: a value printed in the paper (Table I), a
+hand-worked example, a library routine (torch float64
+autograd: conv2d / max_pool2d / linear / cross_entropy), finite differences,
+closed forms, invariants, or brute force on tiny inputs.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import synthdata as sd
+from oracle import Oracle, OracleError
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+C_, P_, F_ = sd.CONV, sd.POOL, sd.FULL
+T_, I_ = sd.TANH, sd.IDENT
+
+
+# --------------------------------------------------------------------------------------
+# Table I: weight counts and neuron counts, printed values
+# --------------------------------------------------------------------------------------
+TABLE_I = {
+    # per weighted layer weights (Weights column) and per layer neurons (Neurons column)
+    "paper_small": ([85, 1260, 4550, 510], [3380, 845, 810, 90, 50, 10]),
+    "paper_medium": ([340, 20040, 54150, 1510], [13520, 3380, 3240, 360, 150, 10]),
+    "paper_large": ([340, 30060, 216100, 135150, 1510],
+                    [13520, 13520, 29040, 7260, 3600, 900, 150, 10]),
+}
+
+
+@pytest.mark.parametrize("name", sorted(TABLE_I))
+def test_table1_weights_and_neurons(name):
+    arch = sd.ARCHS["medium" if name == "paper_medium" else name]
+    o = Oracle(arch)
+    weights, neurons = TABLE_I[name]
+    assert [nw + nb for (_, nw, nb) in o.blocks()] == weights
+    assert o.n_params == sum(weights)
+    # the forward trace holds every layer's output: its length is the Neurons column sum,
+    # and per-layer lengths come out of the trace split
+    assert len(o.forward(np.zeros(o.n_params), np.zeros(841, np.float32))[1]) == sum(neurons)
+
+
+def test_bj_param_counts():
+    # BASELINE.json configs[0..3] nets with the Table I "+1" formula
+    assert Oracle(sd.ARCHS["tiny"]).n_params == 8545
+    assert Oracle(sd.ARCHS["medium"]).n_params == 76040
+    assert Oracle(sd.ARCHS["large"]).n_params == 96960
+
+
+def test_arch_rejected():
+    with pytest.raises(OracleError, match="kernel"):
+        Oracle([(C_, 4, 30, T_), (F_, 10, 0, I_)])
+    with pytest.raises(OracleError):
+        Oracle([(C_, 4, 3, T_), (F_, 10, 0, T_)])  # logits must be identity
+
+
+# --------------------------------------------------------------------------------------
+# Appendix A hand-worked examples (tests/golden/appendix_a.json)
+# --------------------------------------------------------------------------------------
+HAND_ARCH = [(C_, 1, 2, T_), (P_, 0, 2, T_), (F_, 2, 0, I_)]
+
+
+@pytest.mark.parametrize("ex", ["A", "B"])
+def test_appendix_a(ex):
+    g = json.load(open(os.path.join(GOLD, "appendix_a.json")))
+    e = g[ex]
+    o = Oracle(HAND_ARCH, in_h=4, in_w=4, n_classes=2)
+    p0 = np.array(g["params0"])
+    x = np.array(e["x"], np.float32).reshape(-1)
+    logits, trace, am = o.forward(p0, x)
+    np.testing.assert_allclose(logits, e["logits"], atol=1e-9)
+    # trace = conv 3x3 (9) + pooled 1x1 (1) + logits (2)
+    assert trace[9] == pytest.approx(e["pool_value"], abs=1e-9)
+    assert int(am[0]) == e["argmax"]
+    loss, grad = o.sample_grad(p0, x, g["label"])
+    assert loss == pytest.approx(e["loss"], abs=1e-9)
+    np.testing.assert_allclose(grad, e["grad"], atol=1e-9)
+    p1, _ = o.train_sgd(p0, x[None], np.array([g["label"]]), g["lr"])
+    np.testing.assert_allclose(p1, e["params1"], atol=1e-9)
+
+
+def test_appendix_a_closed_form_values():
+    # the hand values themselves, from closed forms: tanh(0.5), softmax of (+t, -t)
+    t = math.tanh(0.5)
+    assert t == pytest.approx(0.4621171573, abs=1e-10)
+    p0 = 1.0 / (1.0 + math.exp(-2 * t))
+    assert p0 == pytest.approx(0.7159040903, abs=1e-10)
+    assert -math.log(1.0 - p0) == pytest.approx(1.2584433876, abs=1e-9)
+
+
+# --------------------------------------------------------------------------------------
+# Closed forms: zero-weight net
+# --------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["tiny", "medium", "large"])
+def test_zero_weights(name):
+    o = Oracle(sd.ARCHS[name])
+    x = sd.uniform_dataset(5, 1, 0).x_train[0]
+    loss, g = o.sample_grad(np.zeros(o.n_params), x, 3)
+    assert loss == pytest.approx(math.log(10.0), abs=1e-12)
+    gb = g[-10:]
+    expect = np.full(10, 0.1)
+    expect[3] -= 1.0
+    np.testing.assert_allclose(gb, expect, atol=1e-15)
+    assert np.count_nonzero(g[:-10]) == 0  # every other gradient is exactly 0
+
+
+def test_identity_conv_passes_input():
+    # 1x1 kernel, weight 1, bias 0, identity activation => output = input
+    o = Oracle([(C_, 1, 1, I_), (F_, 2, 0, I_)], in_h=3, in_w=3, n_classes=2)
+    p = np.zeros(o.n_params)
+    p[0] = 1.0
+    x = np.arange(9, dtype=np.float32) - 4
+    _, trace, _ = o.forward(p, x)
+    np.testing.assert_array_equal(trace[:9], x)
+
+
+# --------------------------------------------------------------------------------------
+# torch float64 autograd (library routine) on the BASELINE.json nets
+# --------------------------------------------------------------------------------------
+def torch_grad(arch, params, X, Y):
+    """Sum-reduction CE gradient with torch's own conv2d/max_pool2d/linear/cross_entropy."""
+    import torch
+    import torch.nn.functional as F
+    P = torch.tensor(params, dtype=torch.float64, requires_grad=True)
+    x = torch.tensor(np.asarray(X, np.float64)).reshape(len(Y), 1, 29, 29)
+    off = 0
+    h = x
+    c = 1
+    for kind, units, k, act in arch:
+        if kind == C_:
+            nw = units * c * k * k
+            W = P[off:off + nw].reshape(units, c, k, k)
+            b = P[off + nw:off + nw + units]
+            off += nw + units
+            h = F.conv2d(h, W, b)
+            h = torch.tanh(h) if act == T_ else h
+            c = units
+        elif kind == P_:
+            h = F.max_pool2d(h, k, stride=k, ceil_mode=False)
+        else:
+            h = h.reshape(h.shape[0], -1)
+            nin = h.shape[1]
+            W = P[off:off + units * nin].reshape(units, nin)
+            b = P[off + units * nin:off + units * nin + units]
+            off += units * nin + units
+            h = F.linear(h, W, b)
+            h = torch.tanh(h) if act == T_ else h
+    loss = F.cross_entropy(h, torch.tensor(np.asarray(Y, np.int64)), reduction="sum")
+    loss.backward()
+    return loss.item(), P.grad.numpy().copy(), h.detach().numpy()
+
+
+@pytest.mark.parametrize("name", ["tiny", "medium", "large", "paper_small"])
+def test_against_torch_f64(name):
+    arch = sd.ARCHS[name]
+    o = Oracle(arch)
+    d = sd.prototype_dataset(11, 3, 0)
+    p = sd.init_params(11, o.blocks()).astype(np.float64)
+    tl, tg, tlogits = torch_grad(arch, p, d.x_train, d.y_train)
+    tot_l = 0.0
+    tot_g = np.zeros(o.n_params)
+    for i in range(3):
+        logits, _, _ = o.forward(p, d.x_train[i])
+        np.testing.assert_allclose(logits, tlogits[i], rtol=1e-12, atol=1e-13)
+        li, gi = o.sample_grad(p, d.x_train[i], d.y_train[i])
+        tot_l += li
+        tot_g += gi
+    assert tot_l == pytest.approx(tl, rel=1e-12)
+    np.testing.assert_allclose(tot_g, tg, rtol=1e-10, atol=1e-12 * np.abs(tg).max())
+    # one sync step of batch 3 = W - lr * sum g
+    p1, _ = o.train_sync(p, d.x_train, d.y_train, 0.05, 3)
+    np.testing.assert_allclose(p1, p - 0.05 * tg, rtol=1e-12, atol=1e-14)
+
+
+# --------------------------------------------------------------------------------------
+# Central finite differences on random tie-free tiny nets with every layer kind
+# --------------------------------------------------------------------------------------
+FD_ARCH = [(C_, 3, 3, T_), (P_, 0, 2, T_), (C_, 4, 2, T_), (P_, 0, 2, T_), (F_, 5, 0, T_), (F_, 3, 0, I_)]
+
+
+def _min_pool_gap(o, p, x, arch, in_hw):
+    """Smallest top-2 gap over every pool window (ties make FD invalid, Appendix A)."""
+    _, trace, _ = o.forward(p, x)
+    off = 0
+    c, h, w = 1, in_hw, in_hw
+    gap = np.inf
+    prev = None
+    for kind, units, k, act in arch:
+        if kind == C_:
+            h, w, c = h - k + 1, w - k + 1, units
+            n = c * h * w
+            prev = trace[off:off + n].reshape(c, h, w)
+            off += n
+        elif kind == P_:
+            ph, pw = h // k, w // k
+            for m in range(c):
+                for pr in range(ph):
+                    for pc in range(pw):
+                        v = np.sort(prev[m, pr * k:pr * k + k, pc * k:pc * k + k].reshape(-1))
+                        gap = min(gap, v[-1] - v[-2])
+            h, w = ph, pw
+            off += c * h * w
+        else:
+            off += units
+            c, h, w = units, 1, 1
+    return gap
+
+
+def test_finite_differences():
+    in_hw = 11
+    o = Oracle(FD_ARCH, in_h=in_hw, in_w=in_hw, n_classes=3)
+    rng = np.random.default_rng(3)
+    done = 0
+    for trial in range(50):
+        p = rng.uniform(-0.6, 0.6, o.n_params)
+        x = rng.uniform(-1, 1, in_hw * in_hw).astype(np.float32)
+        if _min_pool_gap(o, p, x, FD_ARCH, in_hw) < 1e-3:
+            continue
+        label = int(rng.integers(0, 3))
+        _, g = o.sample_grad(p, x, label)
+        eps = 1e-5
+        fd = np.zeros_like(g)
+        for j in range(o.n_params):
+            pp = p.copy()
+            pp[j] += eps
+            lp, _ = o.sample_grad(pp, x, label)
+            pp[j] -= 2 * eps
+            lm, _ = o.sample_grad(pp, x, label)
+            fd[j] = (lp - lm) / (2 * eps)
+        scale = np.maximum(np.abs(fd), 1e-3 * np.abs(fd).max())
+        assert np.max(np.abs(fd - g) / scale) < 1e-4
+        done += 1
+        if done == 3:
+            break
+    assert done == 3
+
+
+def test_fd_invalid_at_tie():
+    # Appendix A: at the Example-A tie, FD gives half the analytic dK00
+    g = json.load(open(os.path.join(GOLD, "appendix_a.json")))
+    o = Oracle(HAND_ARCH, in_h=4, in_w=4, n_classes=2)
+    p = np.array(g["params0"])
+    x = np.array(g["A"]["x"], np.float32).reshape(-1)
+    eps = 1e-5
+    pp = p.copy()
+    pp[0] += eps
+    lp, _ = o.sample_grad(pp, x, 1)
+    pp[0] -= 2 * eps
+    lm, _ = o.sample_grad(pp, x, 1)
+    assert (lp - lm) / (2 * eps) == pytest.approx(0.5630198049, abs=1e-6)
+
+
+# --------------------------------------------------------------------------------------
+# Invariants
+# --------------------------------------------------------------------------------------
+def test_softmax_delta_invariants():
+    o = Oracle(sd.ARCHS["tiny"])
+    d = sd.prototype_dataset(4, 4, 0)
+    p = sd.init_params(4, o.blocks())
+    for i in range(4):
+        _, g = o.sample_grad(p, d.x_train[i], d.y_train[i])
+        gb = g[-10:]  # output-layer bias gradient = softmax - onehot
+        prob = gb.copy()
+        prob[d.y_train[i]] += 1.0
+        assert prob.sum() == pytest.approx(1.0, abs=1e-12)
+        assert np.all(prob > 0) and np.all(prob < 1)
+
+
+def test_floor_dropped_inputs_do_not_matter():
+    # conv 1x1 identity on 5x5, pool 2 -> 2x2 drops row 4 / col 4: changing those pixels
+    # (kept below the window maxima) changes neither loss nor gradient
+    arch = [(C_, 1, 1, I_), (P_, 0, 2, T_), (F_, 2, 0, I_)]
+    o = Oracle(arch, in_h=5, in_w=5, n_classes=2)
+    p = np.array([1.0, 0.0, 0.3, -0.2, 0.1, -0.4, 0.0, 0.0, 0.0, 0.0])[:o.n_params]
+    x = np.random.default_rng(0).uniform(0, 1, 25).astype(np.float32)
+    l0, g0 = o.sample_grad(p, x, 0)
+    x2 = x.reshape(5, 5).copy()
+    x2[4, :] = -7.0
+    x2[:, 4] = -3.0
+    l1, g1 = o.sample_grad(p, x2.reshape(-1), 0)
+    assert l0 == l1
+    np.testing.assert_array_equal(g0, g1)
+
+
+def test_pool_gradient_routes_to_argmax_only():
+    # identity 1x1 conv, so conv gW = sum over windows of delta_pool * x[argmax]:
+    # compare with brute force over the windows
+    arch = [(C_, 1, 1, I_), (P_, 0, 2, T_), (F_, 1, 0, T_), (F_, 2, 0, I_)]
+    o = Oracle(arch, in_h=4, in_w=4, n_classes=2)
+    rng = np.random.default_rng(1)
+    p = rng.uniform(-1, 1, o.n_params)
+    p[0], p[1] = 1.0, 0.0
+    x = rng.uniform(-1, 1, 16).astype(np.float32)
+    logits, trace, am = o.forward(p, x)
+    _, g = o.sample_grad(p, x, 1)
+    # delta at the pooled outputs by the chain rule written out for this tiny net
+    V1, c1 = p[2:6], p[6]
+    V2, c2 = p[7:9], p[9:11]
+    pooled = trace[16:20]
+    h = np.tanh(V1 @ pooled + c1)
+    z = V2 * h + c2
+    prob = np.exp(z - z.max()) / np.exp(z - z.max()).sum()
+    dz = prob - np.array([0.0, 1.0])
+    dh = (V2 @ dz) * (1 - h * h)
+    dpool = V1 * dh * 1.0  # pool sits on an identity conv: no tanh derivative
+    xs = x.reshape(4, 4).astype(np.float64)
+    expect_gw = sum(dpool[w] * xs[(w // 2) * 2 + am[w] // 2, (w % 2) * 2 + am[w] % 2] for w in range(4))
+    assert g[0] == pytest.approx(expect_gw, rel=1e-12)
+    assert g[1] == pytest.approx(dpool.sum(), rel=1e-12)
+
+
+def test_sync_batch1_equals_sequential_bitwise():
+    o = Oracle(sd.ARCHS["tiny"])
+    d = sd.prototype_dataset(7, 20, 0)
+    p = sd.init_params(7, o.blocks())
+    a, la = o.train_sgd(p, d.x_train, d.y_train, 0.01)
+    b, lb = o.train_sync(p, d.x_train, d.y_train, 0.01, 1)
+    np.testing.assert_array_equal(a, b)
+    assert la == lb
+
+
+def test_sync_permutation_within_batch():
+    o = Oracle(sd.ARCHS["tiny"])
+    d = sd.prototype_dataset(8, 8, 0)
+    p = sd.init_params(8, o.blocks())
+    a, _ = o.train_sync(p, d.x_train, d.y_train, 0.01, 8)
+    perm = np.random.default_rng(0).permutation(8)
+    b, _ = o.train_sync(p, d.x_train[perm], d.y_train[perm], 0.01, 8)
+    np.testing.assert_allclose(a, b, rtol=1e-12, atol=1e-15)
+
+
+def test_sync_full_batch_is_all_concurrent_replay():
+    # brute force, 3 samples: B = n equals every sample read at W0, one summed update
+    o = Oracle(sd.ARCHS["tiny"])
+    d = sd.prototype_dataset(9, 3, 0)
+    p = sd.init_params(9, o.blocks()).astype(np.float64)
+    gs = [o.sample_grad(p, d.x_train[i], d.y_train[i])[1] for i in range(3)]
+    a, _ = o.train_sync(p, d.x_train, d.y_train, 0.02, 3)
+    np.testing.assert_allclose(a, p - 0.02 * ((gs[0] + gs[1]) + gs[2]), rtol=0, atol=1e-15)
+
+
+def test_evaluate_brute_force():
+    o = Oracle(sd.ARCHS["tiny"])
+    d = sd.prototype_dataset(10, 0, 30)
+    p = sd.init_params(10, o.blocks())
+    ml, ne, losses, preds = o.evaluate(p, d.x_test, d.y_test, per_sample=True)
+    errs = 0
+    for i in range(30):
+        logits, _, _ = o.forward(p, d.x_test[i])
+        errs += int(np.argmax(logits)) != d.y_test[i]  # numpy argmax: first maximum
+        assert preds[i] == int(np.argmax(logits))
+    assert ne == errs
+    _, tg, tlog = torch_grad(sd.ARCHS["tiny"], p.astype(np.float64), d.x_test, d.y_test)
+    import torch
+    tce = torch.nn.functional.cross_entropy(torch.tensor(tlog), torch.tensor(d.y_test.astype(np.int64)))
+    assert ml == pytest.approx(tce.item(), rel=1e-12)
+
+
+def test_label_out_of_range():
+    o = Oracle(sd.ARCHS["tiny"])
+    with pytest.raises(OracleError):
+        o.sample_grad(np.zeros(o.n_params), np.zeros(841, np.float32), 10)
+
+
+def test_empty_training_is_noop():
+    o = Oracle(sd.ARCHS["tiny"])
+    p = sd.init_params(1, o.blocks())
+    q, _ = o.train_sgd(p, np.zeros((0, 841), np.float32), np.zeros(0, np.int32), 0.1)
+    np.testing.assert_array_equal(q, p.astype(np.float64))
