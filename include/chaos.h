@@ -1,0 +1,143 @@
+/*
+ * chaos.h -- C ABI of the B200-native CHAOS training hot path (libchaos.so).
+ *
+ * CHAOS = "Controlled Hogwild with Arbitrary Order of Synchronization",
+ * Viebke & Pllana, arXiv:1506.09067, §III-A.  The library
+ * trains small MNIST-shaped CNNs (conv -> tanh -> max-pool blocks, fully
+ * connected layers, softmax cross-entropy; Table I
+ * PAPER.md:212-247) with per-sample forward propagation, back-propagation and
+ * the controlled-hogwild shared-weight update, all in hand-written sm_100a
+ * kernels.  No C++ type, exception or torch type crosses this boundary.
+ *
+ * Conventions (apply to every call):
+ *  - Ownership: the net owns its device parameters, scratch, work counter and
+ *    error latch (cudaMalloc on the device current at chaos_net_create).  Device
+ *    image/label pointers passed in are BORROWED and must stay valid until the
+ *    net's stream has passed the call.  Host buffers are caller-owned.
+ *  - Threading: one host thread per net.
+ *  - Streams: all device work is enqueued on the net's stream
+ *    (CHAOS_OPT_STREAM; default = the legacy default stream).
+ *  - Errors: argument / architecture errors return immediately with a status and
+ *    set chaos_last_error().  Errors detected on the device (label outside
+ *    [0, n_classes), non-finite loss) are latched and returned by the next
+ *    synchronizing call (chaos_evaluate, chaos_net_get_params, chaos_net_sync,
+ *    chaos_compute_gradients, chaos_forward).
+ *  - n == 0 is a no-op returning CHAOS_OK.
+ *  - Data layout: images fp32 [n][in_c][in_h][in_w] contiguous, labels int32 [n].
+ *  - Parameter layout (normative; get/set/compute_gradients use it): for each
+ *    weighted layer in order, W then b; conv W is [M][C][k][k], FC W is
+ *    [N][In]; the FC input is flattened [map][row][col].  Counts follow Table I's
+ *    "+1" formula: conv M*(C*k*k+1), FC N*(In+1).  The device
+ *    keeps its own internal layout (conv W transposed to [C*k*k][M'] with M
+ *    padded to a multiple of 4, every block 16-byte aligned); get/set convert.
+ */
+#ifndef CHAOS_H
+#define CHAOS_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    CHAOS_OK = 0,
+    CHAOS_E_INVALID = -1,     /* bad argument (NULL, n<0, non-finite lr, ...) */
+    CHAOS_E_ARCH = -2,        /* shape chain invalid (message names the layer) */
+    CHAOS_E_UNSUPPORTED = -3, /* valid arch without a compiled sm_100a instantiation */
+    CHAOS_E_LABEL = -4,       /* device latch: a label outside [0, n_classes) */
+    CHAOS_E_NONFINITE = -5,   /* device latch: non-finite loss */
+    CHAOS_E_CUDA = -6,        /* CUDA runtime error (message has cudaGetErrorString) */
+    CHAOS_E_NCCL = -7         /* reserved */
+} chaos_status;
+
+typedef enum { CHAOS_CONV = 1, CHAOS_MAXPOOL = 2, CHAOS_FULL = 3 } chaos_layer_kind;
+typedef enum { CHAOS_TANH = 0, CHAOS_IDENTITY = 1 } chaos_act; /* last FULL = logits -> softmax-CE */
+
+typedef struct {
+    int32_t kind;   /* chaos_layer_kind */
+    int32_t units;  /* conv: output maps; full: neurons; maxpool: ignored */
+    int32_t kernel; /* conv kernel k (k x k, stride 1, valid) or pool window kp (kp x kp, stride kp, floor) */
+    int32_t act;    /* chaos_act: conv/full hidden layers CHAOS_TANH, last full CHAOS_IDENTITY */
+} chaos_layer;
+
+typedef struct {
+    int32_t in_c, in_h, in_w, n_classes, n_layers;
+    chaos_layer layers[16];
+    uint64_t init_seed; /* parameters U(+-1/sqrt(fan_in)) from splitmix64(init_seed ^ 0x5EED) (R7) */
+} chaos_arch;
+
+/* Paper: Training with several workers sharing weights.
+ * HOGWILD: persistent CTAs claim groups of G images from a device counter
+ *   (first come, first served) and, after each layer's gradient
+ *   and the previous layer's partial derivatives are computed, add -lr*gradient
+ *   to the shared fp32 weights with atomics in arbitrary order.
+ * SYNC: deterministic: consecutive batches of CHAOS_OPT_SYNC_BATCH images; every
+ *   gradient at the batch-start weights; one update W -= lr * sum_i g_i, the sum
+ *   taken in a fixed order (BASELINE.json north_star).  Bitwise run-to-run
+ *   reproducible. */
+typedef enum { CHAOS_HOGWILD = 0, CHAOS_SYNC = 1 } chaos_mode;
+
+typedef enum {
+    CHAOS_OPT_STREAM = 0,        /* value = (int64_t)cudaStream_t */
+    CHAOS_OPT_SYNC_BATCH = 1,    /* B >= 1, default 64 */
+    CHAOS_OPT_GROUP = 2,         /* G, images per CTA per claim: compiled values 1 and the net's default */
+    CHAOS_OPT_MAX_CTAS = 3,      /* cap on resident CTAs (1 => a single worker = sequential SGD when G=1) */
+    CHAOS_OPT_DEBUG_CLAIMS = 4   /* 1 => count claims per image into a device buffer (exactly-once test) */
+} chaos_option;
+
+typedef struct chaos_net chaos_net;
+
+/* Validate the arch, pick the compiled instantiation, allocate, initialise the
+ * parameters.  NULL on error (see chaos_last_error(); status via chaos_last_status()). */
+chaos_net* chaos_net_create(const chaos_arch* arch);
+void chaos_net_destroy(chaos_net* net);
+chaos_status chaos_net_set_option(chaos_net* net, chaos_option opt, int64_t value);
+int64_t chaos_net_get_option(const chaos_net* net, chaos_option opt);
+int64_t chaos_net_num_params(const chaos_net* net);
+/* Synchronizing.  host_dst / host_src hold n == num_params floats, normative layout. */
+chaos_status chaos_net_get_params(chaos_net* net, float* host_dst, int64_t n);
+chaos_status chaos_net_set_params(chaos_net* net, const float* host_src, int64_t n);
+/* Device pointer to the internal parameter buffer (for NCCL / torch views of the
+ * whole buffer; element-wise averaging is layout independent). */
+float* chaos_net_device_params(chaos_net* net);
+int64_t chaos_net_device_params_len(const chaos_net* net); /* floats, incl. padding */
+
+/* One Training phase over images [0, n).  Asynchronous on the
+ * net's stream.  lr is per call: the caller applies the x0.9/epoch schedule. */
+chaos_status chaos_train_epoch(chaos_net* net, const float* d_images, const int32_t* d_labels, int64_t n, float lr,
+                               chaos_mode mode);
+/* Same, from HOST buffers: the images/labels are copied to net-owned device
+ * staging buffers on the net's stream, chunk by chunk, overlapped with training
+ * (hogwild) -- the end-to-end entry point.  Synchronizing on return. */
+chaos_status chaos_train_epoch_host(chaos_net* net, const float* h_images, const int32_t* h_labels, int64_t n,
+                                    float lr, chaos_mode mode);
+/* Mean training loss (double) of the last chaos_train_epoch call; synchronizing. */
+chaos_status chaos_last_train_loss(chaos_net* net, double* mean_loss);
+
+/* Validation / Testing: forward only; mean cross-entropy (fixed-order
+ * double sum) and the number of images whose argmax logit (lowest index on ties)
+ * differs from the label.  Synchronizing.  Never writes the parameters. */
+chaos_status chaos_evaluate(chaos_net* net, const float* d_images, const int32_t* d_labels, int64_t n,
+                            double* mean_loss, int64_t* n_errors);
+/* Forward only: logits [n][n_classes] into the device buffer d_logits.  Synchronizing. */
+chaos_status chaos_forward(chaos_net* net, const float* d_images, int64_t n, float* d_logits);
+/* Test hook: host_grad_sum[j] = sum_i dL_i/dparam_j at the current weights (normative
+ * layout, no update; fixed-order sum).  Synchronizing. */
+chaos_status chaos_compute_gradients(chaos_net* net, const float* d_images, const int32_t* d_labels, int64_t n,
+                                     float* host_grad_sum);
+/* Debug: copies the per-image claim counts of the last hogwild epoch (needs
+ * CHAOS_OPT_DEBUG_CLAIMS=1 before the epoch) into host_counts[n]. */
+chaos_status chaos_debug_claims(chaos_net* net, int32_t* host_counts, int64_t n);
+
+/* Waits for the net's stream; returns (and clears) latched device errors. */
+chaos_status chaos_net_sync(chaos_net* net);
+/* Number of SMs and resident CTAs per SM the training kernel uses (for reports). */
+chaos_status chaos_net_launch_info(chaos_net* net, int32_t* grid, int32_t* block, int32_t* smem_bytes, int32_t* group);
+/* Thread-local message of the last failing call on this thread. */
+const char* chaos_last_error(void);
+chaos_status chaos_last_status(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

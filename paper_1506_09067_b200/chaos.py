@@ -1,0 +1,243 @@
+"""Thin ctypes binding of libchaos.so (include/chaos.h): argument marshalling only.
+
+Every step of the hot path runs in the library's sm_100a kernels.  There is no CPU
+fallback: if ``libchaos.so`` is missing or no CUDA device is present, construction
+raises.  Names follow the C ABI (``chaos_net_create`` -> ``Net``, ``chaos_train_epoch``
+-> ``Net.train_epoch`` ...).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libchaos.so")
+
+CHAOS_CONV, CHAOS_MAXPOOL, CHAOS_FULL = 1, 2, 3
+CHAOS_TANH, CHAOS_IDENTITY = 0, 1
+HOGWILD, SYNC = 0, 1
+OPT_STREAM, OPT_SYNC_BATCH, OPT_GROUP, OPT_MAX_CTAS, OPT_DEBUG_CLAIMS = 0, 1, 2, 3, 4
+STATUS = {0: "CHAOS_OK", -1: "CHAOS_E_INVALID", -2: "CHAOS_E_ARCH", -3: "CHAOS_E_UNSUPPORTED",
+          -4: "CHAOS_E_LABEL", -5: "CHAOS_E_NONFINITE", -6: "CHAOS_E_CUDA", -7: "CHAOS_E_NCCL"}
+
+# every symbol include/chaos.h declares (checked by tests/test_abi.py)
+EXPORTS = ["chaos_net_create", "chaos_net_destroy", "chaos_net_set_option", "chaos_net_get_option",
+           "chaos_net_num_params", "chaos_net_get_params", "chaos_net_set_params", "chaos_net_device_params",
+           "chaos_net_device_params_len", "chaos_train_epoch", "chaos_train_epoch_host", "chaos_last_train_loss",
+           "chaos_evaluate", "chaos_forward", "chaos_compute_gradients", "chaos_debug_claims", "chaos_net_sync",
+           "chaos_net_launch_info", "chaos_last_error", "chaos_last_status"]
+
+
+class ChaosError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Layer(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("units", C.c_int32), ("kernel", C.c_int32), ("act", C.c_int32)]
+
+
+class Arch(C.Structure):
+    _fields_ = [("in_c", C.c_int32), ("in_h", C.c_int32), ("in_w", C.c_int32), ("n_classes", C.c_int32),
+                ("n_layers", C.c_int32), ("layers", Layer * 16), ("init_seed", C.c_uint64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libchaos.so (raises if it was not built: no fallback path exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (nvcc, sm_100a)")
+        L = C.CDLL(LIB_PATH)
+        vp, fp, ip = C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_int32)
+        sig = {
+            "chaos_net_create": ([C.POINTER(Arch)], vp),
+            "chaos_net_destroy": ([vp], None),
+            "chaos_net_set_option": ([vp, C.c_int, C.c_int64], C.c_int),
+            "chaos_net_get_option": ([vp, C.c_int], C.c_int64),
+            "chaos_net_num_params": ([vp], C.c_int64),
+            "chaos_net_get_params": ([vp, fp, C.c_int64], C.c_int),
+            "chaos_net_set_params": ([vp, fp, C.c_int64], C.c_int),
+            "chaos_net_device_params": ([vp], C.c_void_p),
+            "chaos_net_device_params_len": ([vp], C.c_int64),
+            "chaos_train_epoch": ([vp, vp, vp, C.c_int64, C.c_float, C.c_int], C.c_int),
+            "chaos_train_epoch_host": ([vp, fp, ip, C.c_int64, C.c_float, C.c_int], C.c_int),
+            "chaos_last_train_loss": ([vp, C.POINTER(C.c_double)], C.c_int),
+            "chaos_evaluate": ([vp, vp, vp, C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_int64)], C.c_int),
+            "chaos_forward": ([vp, vp, C.c_int64, vp], C.c_int),
+            "chaos_compute_gradients": ([vp, vp, vp, C.c_int64, fp], C.c_int),
+            "chaos_debug_claims": ([vp, ip, C.c_int64], C.c_int),
+            "chaos_net_sync": ([vp], C.c_int),
+            "chaos_net_launch_info": ([vp, ip, ip, ip, ip], C.c_int),
+            "chaos_last_error": ([], C.c_char_p),
+            "chaos_last_status": ([], C.c_int),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        raise ChaosError(rc, lib().chaos_last_error().decode())
+
+
+def make_arch(layers, init_seed=0, in_c=1, in_h=29, in_w=29, n_classes=10) -> Arch:
+    a = Arch()
+    a.in_c, a.in_h, a.in_w, a.n_classes, a.n_layers = in_c, in_h, in_w, n_classes, len(layers)
+    for i, (kind, units, kernel, act) in enumerate(layers):
+        a.layers[i] = Layer(kind, units, kernel, act)
+    a.init_seed = init_seed
+    return a
+
+
+def _ptr(t):
+    """Device pointer of a CUDA torch tensor (contiguous)."""
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValueError("expected a contiguous CUDA tensor")
+    return C.c_void_p(t.data_ptr())
+
+
+class _CudaArray:
+    """__cuda_array_interface__ wrapper so torch.as_tensor can alias the library's buffer."""
+
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3,
+                                         "strides": None, "stream": None}
+
+
+class Net:
+    """chaos_net_create(arch) ... chaos_net_destroy."""
+
+    def __init__(self, layers, init_seed=0, in_c=1, in_h=29, in_w=29, n_classes=10, stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("libchaos needs a CUDA device (no CPU fallback)")
+        torch.cuda.init()
+        self._arch = make_arch(layers, init_seed, in_c, in_h, in_w, n_classes)
+        h = lib().chaos_net_create(C.byref(self._arch))
+        if not h:
+            raise ChaosError(lib().chaos_last_status(), lib().chaos_last_error().decode())
+        self._h = C.c_void_p(h)
+        self.n_params = int(lib().chaos_net_num_params(self._h))
+        self.n_classes = n_classes
+        self.n_in = in_c * in_h * in_w
+        s = stream if stream is not None else torch.cuda.current_stream()
+        self.set_option(OPT_STREAM, s.cuda_stream)
+        self._stream = s
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().chaos_net_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self):
+        return self._stream
+
+    def set_option(self, opt, value):
+        _check(lib().chaos_net_set_option(self._h, opt, int(value)))
+
+    def get_option(self, opt):
+        return int(lib().chaos_net_get_option(self._h, opt))
+
+    def get_params(self) -> np.ndarray:
+        out = np.zeros(self.n_params, np.float32)
+        _check(lib().chaos_net_get_params(self._h, out.ctypes.data_as(C.POINTER(C.c_float)), self.n_params))
+        return out
+
+    def set_params(self, p):
+        p = np.ascontiguousarray(p, np.float32)
+        if p.shape != (self.n_params,):
+            raise ValueError(f"expected {self.n_params} params")
+        _check(lib().chaos_net_set_params(self._h, p.ctypes.data_as(C.POINTER(C.c_float)), self.n_params))
+
+    def device_params(self):
+        """torch view (no copy) of the internal parameter buffer (for NCCL averaging)."""
+        import torch
+        ptr = lib().chaos_net_device_params(self._h)
+        n = int(lib().chaos_net_device_params_len(self._h))
+        return torch.as_tensor(_CudaArray(ptr, n), device="cuda")
+
+    def train_epoch(self, images, labels, lr, mode=HOGWILD):
+        """chaos_train_epoch: asynchronous on the net's stream; images/labels CUDA tensors."""
+        n = int(labels.shape[0])
+        _check(lib().chaos_train_epoch(self._h, _ptr(images), _ptr(labels), n, float(lr), int(mode)))
+
+    def train_epoch_host(self, images, labels, lr, mode=HOGWILD):
+        """chaos_train_epoch_host: host (ideally pinned) buffers; synchronizing."""
+        import torch
+        if isinstance(images, torch.Tensor):
+            assert not images.is_cuda and images.is_contiguous() and images.dtype == torch.float32
+            assert not labels.is_cuda and labels.is_contiguous() and labels.dtype == torch.int32
+            xp = C.cast(C.c_void_p(images.data_ptr()), C.POINTER(C.c_float))
+            yp = C.cast(C.c_void_p(labels.data_ptr()), C.POINTER(C.c_int32))
+            n = int(labels.shape[0])
+        else:
+            images = np.ascontiguousarray(images, np.float32)
+            labels = np.ascontiguousarray(labels, np.int32)
+            xp = images.ctypes.data_as(C.POINTER(C.c_float))
+            yp = labels.ctypes.data_as(C.POINTER(C.c_int32))
+            n = len(labels)
+        _check(lib().chaos_train_epoch_host(self._h, xp, yp, n, float(lr), int(mode)))
+
+    def last_train_loss(self):
+        v = C.c_double()
+        _check(lib().chaos_last_train_loss(self._h, C.byref(v)))
+        return v.value
+
+    def evaluate(self, images, labels):
+        ml = C.c_double()
+        ne = C.c_int64()
+        n = int(labels.shape[0])
+        if n == 0:
+            _check(lib().chaos_evaluate(self._h, None, None, 0, C.byref(ml), C.byref(ne)))
+        else:
+            _check(lib().chaos_evaluate(self._h, _ptr(images), _ptr(labels), n, C.byref(ml), C.byref(ne)))
+        return ml.value, int(ne.value)
+
+    def forward(self, images):
+        import torch
+        n = int(images.shape[0])
+        out = torch.empty((n, self.n_classes), dtype=torch.float32, device=images.device)
+        if n:
+            _check(lib().chaos_forward(self._h, _ptr(images), n, _ptr(out)))
+        return out
+
+    def compute_gradients(self, images, labels):
+        g = np.zeros(self.n_params, np.float32)
+        n = int(labels.shape[0])
+        gp = g.ctypes.data_as(C.POINTER(C.c_float))
+        if n == 0:
+            _check(lib().chaos_compute_gradients(self._h, None, None, 0, gp))
+        else:
+            _check(lib().chaos_compute_gradients(self._h, _ptr(images), _ptr(labels), n, gp))
+        return g
+
+    def debug_claims(self, n):
+        out = np.zeros(n, np.int32)
+        _check(lib().chaos_debug_claims(self._h, out.ctypes.data_as(C.POINTER(C.c_int32)), n))
+        return out
+
+    def sync(self):
+        _check(lib().chaos_net_sync(self._h))
+
+    def launch_info(self):
+        v = [C.c_int32() for _ in range(4)]
+        _check(lib().chaos_net_launch_info(self._h, *[C.byref(x) for x in v]))
+        return {"grid": v[0].value, "block": v[1].value, "smem_bytes": v[2].value, "group": v[3].value}

@@ -1,0 +1,707 @@
+// chaos_runtime.cu -- host runtime and C ABI of libchaos.so (see include/chaos.h).
+//
+// Owns: arch validation and matching against the compiled sm_100a instantiations,
+// the internal parameter layout and its conversion to/from the normative layout,
+// device allocations, the documented parameter initialiser, launches of the worker
+// kernel in its four modes, the deterministic sync-mode update, the fixed-order
+// evaluation reduction, and the device error latch.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "chaos.h"
+#include "chaos_kernels.cuh"
+
+using namespace chaos;
+
+// ----------------------------------------------------------------------------------
+// Compiled nets (BASELINE.json configs).  Tuning knobs per conv block: MT, TT, GS, NCH.
+// ----------------------------------------------------------------------------------
+namespace {
+
+struct TinyNet {  // configs[0], configs[1]: conv5 4x4 -> tanh -> pool2 -> FC 845->10
+    static constexpr int NCONV = 1, NFULL = 1, GDEF = 8, NT = 256;
+    using C1 = Conv<1, 29, 29, 5, 4, 2, /*MT*/ 5, /*TT*/ 1, /*GS*/ 4, /*NCH*/ 1>;
+    using C2 = C1;
+    using C3 = C1;
+    using F1 = Full<845, 10, false>;
+    using F2 = F1;
+};
+struct MediumNet {  // configs[2] = Table I medium
+    static constexpr int NCONV = 2, NFULL = 2, GDEF = 4, NT = 512;
+    using C1 = Conv<1, 29, 29, 20, 4, 2, 10, 1, 1, 1>;
+    using C2 = Conv<20, 13, 13, 40, 5, 3, 4, 25, 1, 10>;
+    using C3 = C2;
+    using F1 = Full<360, 150, true>;
+    using F2 = Full<150, 10, false>;
+};
+struct LargeNet {  // configs[3], configs[4]
+    static constexpr int NCONV = 3, NFULL = 2, GDEF = 4, NT = 512;
+    using C1 = Conv<1, 29, 29, 20, 4, 2, 10, 1, 1, 1>;
+    using C2 = Conv<20, 13, 13, 60, 3, 2, 12, 9, 1, 10>;
+    using C3 = Conv<60, 5, 5, 100, 2, 2, 4, 4, 1, 10>;
+    using F1 = Full<400, 150, true>;
+    using F2 = Full<150, 10, false>;
+};
+
+using KernelFn = void (*)(KArgs);
+
+struct Block {  // one weighted layer, host view
+    bool conv;
+    int C, K, M, MP;  // conv
+    int IN, OUT;      // full
+    long long int_w, int_b;    // internal offsets (floats)
+    long long norm_w, norm_b;  // normative offsets
+    long long nw, nb, fan_in;
+};
+
+struct LayerSig {
+    int kind, units, kernel, act;
+};
+
+struct NetDesc {
+    const char* name;
+    std::vector<LayerSig> sig;
+    std::vector<Block> blocks;
+    long long pint = 0;    // internal floats
+    long long nparams = 0; // normative count
+    int gdef = 1, nt = 256;
+    // [gi][mode]: gi 0 -> G=1, gi 1 -> G=gdef
+    KernelFn fn[2][4] = {};
+    int smem[2] = {0, 0};
+    double flops_per_sample = 0;  // algorithmic
+};
+
+template <class L>
+void add_conv(NetDesc& d, long long w, long long b, long long& norm) {
+    Block k{};
+    k.conv = true;
+    k.C = L::C;
+    k.K = L::K;
+    k.M = L::M;
+    k.MP = L::MP;
+    k.int_w = w;
+    k.int_b = b;
+    k.nw = (long long)L::M * L::C * L::K * L::K;
+    k.nb = L::M;
+    k.fan_in = (long long)L::C * L::K * L::K;
+    k.norm_w = norm;
+    k.norm_b = norm + k.nw;
+    norm += k.nw + k.nb;
+    d.blocks.push_back(k);
+}
+template <class F>
+void add_full(NetDesc& d, long long w, long long b, long long& norm) {
+    Block k{};
+    k.conv = false;
+    k.IN = F::IN;
+    k.OUT = F::OUT;
+    k.int_w = w;
+    k.int_b = b;
+    k.nw = (long long)F::IN * F::OUT;
+    k.nb = F::OUT;
+    k.fan_in = F::IN;
+    k.norm_w = norm;
+    k.norm_b = norm + k.nw;
+    norm += k.nw + k.nb;
+    d.blocks.push_back(k);
+}
+
+template <class Net, int G>
+void fill_kernels(NetDesc& d, int gi) {
+    d.fn[gi][kHogwild] = chaos_worker<Net, G, Net::NT, kHogwild>;
+    d.fn[gi][kSync] = chaos_worker<Net, G, Net::NT, kSync>;
+    d.fn[gi][kEval] = chaos_worker<Net, G, Net::NT, kEval>;
+    d.fn[gi][kForward] = chaos_worker<Net, G, Net::NT, kForward>;
+    d.smem[gi] = SLayout<Net, G>::BYTES;
+}
+
+template <class L>
+double conv_flops() {  // forward on needed outputs + argmax-only gW (+ delta_in) + update
+    const double fwd = 2.0 * L::M * L::P * L::KP * L::KP * L::C * L::KK;
+    const double gw = 2.0 * L::M * L::P * L::C * L::KK;
+    return fwd + gw;
+}
+
+template <class Net>
+NetDesc make_desc(const char* name, std::vector<LayerSig> sig) {
+    using O = POff<Net>;
+    NetDesc d;
+    d.name = name;
+    d.sig = std::move(sig);
+    long long norm = 0;
+    add_conv<typename Net::C1>(d, O::c1w, O::c1b, norm);
+    if constexpr (Net::NCONV >= 2) add_conv<typename Net::C2>(d, O::c2w, O::c2b, norm);
+    if constexpr (Net::NCONV >= 3) add_conv<typename Net::C3>(d, O::c3w, O::c3b, norm);
+    add_full<typename Net::F1>(d, O::f1w, O::f1b, norm);
+    if constexpr (Net::NFULL >= 2) add_full<typename Net::F2>(d, O::f2w, O::f2b, norm);
+    d.pint = O::total;
+    d.nparams = norm;
+    d.gdef = Net::GDEF;
+    d.nt = Net::NT;
+    fill_kernels<Net, 1>(d, 0);
+    fill_kernels<Net, Net::GDEF>(d, 1);
+    return d;
+}
+
+const std::vector<NetDesc>& registry() {
+    static const std::vector<NetDesc> r = [] {
+        std::vector<NetDesc> v;
+        v.push_back(make_desc<TinyNet>("tiny", {{CHAOS_CONV, 5, 4, CHAOS_TANH}, {CHAOS_MAXPOOL, 0, 2, 0},
+                                                {CHAOS_FULL, 10, 0, CHAOS_IDENTITY}}));
+        v.push_back(make_desc<MediumNet>(
+            "medium", {{CHAOS_CONV, 20, 4, CHAOS_TANH}, {CHAOS_MAXPOOL, 0, 2, 0}, {CHAOS_CONV, 40, 5, CHAOS_TANH},
+                       {CHAOS_MAXPOOL, 0, 3, 0}, {CHAOS_FULL, 150, 0, CHAOS_TANH}, {CHAOS_FULL, 10, 0, CHAOS_IDENTITY}}));
+        v.push_back(make_desc<LargeNet>(
+            "large", {{CHAOS_CONV, 20, 4, CHAOS_TANH}, {CHAOS_MAXPOOL, 0, 2, 0}, {CHAOS_CONV, 60, 3, CHAOS_TANH},
+                      {CHAOS_MAXPOOL, 0, 2, 0}, {CHAOS_CONV, 100, 2, CHAOS_TANH}, {CHAOS_MAXPOOL, 0, 2, 0},
+                      {CHAOS_FULL, 150, 0, CHAOS_TANH}, {CHAOS_FULL, 10, 0, CHAOS_IDENTITY}}));
+        return v;
+    }();
+    return r;
+}
+
+thread_local std::string g_err;
+thread_local chaos_status g_status = CHAOS_OK;
+
+chaos_status fail(chaos_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    g_status = s;
+    return s;
+}
+
+#define CUDA_TRY(expr)                                                                           \
+    do {                                                                                         \
+        cudaError_t e_ = (expr);                                                                 \
+        if (e_ != cudaSuccess) return fail(CHAOS_E_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+    } while (0)
+
+}  // namespace
+
+struct chaos_net {
+    const NetDesc* d = nullptr;
+    int dev = 0;
+    int sms = 0;
+    cudaStream_t stream = nullptr;
+    float* params = nullptr;
+    int* latch = nullptr;
+    unsigned long long* counter = nullptr;
+    double* loss_sum = nullptr;
+    long long last_train_n = 0;
+    float* partial = nullptr;
+    long long partial_slots = 0;
+    float* grad_out = nullptr;
+    int* claims = nullptr;
+    long long claims_cap = 0;
+    float* ev_loss = nullptr;
+    unsigned char* ev_wrong = nullptr;
+    long long ev_cap = 0;
+    double* ev_sum = nullptr;
+    long long* ev_err = nullptr;
+    float* st_x = nullptr;
+    int* st_y = nullptr;
+    long long st_cap = 0;
+    int sync_batch = 64;
+    int group = 1;
+    int max_ctas = 0;
+    int debug_claims = 0;
+    int occ[2][4] = {};
+};
+
+namespace {
+
+int gidx(const chaos_net* net) { return net->group == 1 ? 0 : 1; }
+
+chaos_status ensure_kernel_attrs(chaos_net* net) {
+    for (int gi = 0; gi < 2; ++gi)
+        for (int m = 0; m < 4; ++m) {
+            KernelFn f = net->d->fn[gi][m];
+            CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, net->d->smem[gi]));
+            int occ = 0;
+            CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, net->d->nt, net->d->smem[gi]));
+            if (occ < 1) return fail(CHAOS_E_CUDA, "kernel %s G=%d mode %d does not fit on an SM (%d B smem)",
+                                     net->d->name, gi ? net->d->gdef : 1, m, net->d->smem[gi]);
+            net->occ[gi][m] = occ;
+        }
+    return CHAOS_OK;
+}
+
+int grid_for(const chaos_net* net, int mode, long long work_groups) {
+    long long g = (long long)net->sms * net->occ[gidx(net)][mode];
+    if (net->max_ctas > 0 && g > net->max_ctas) g = net->max_ctas;
+    if (g > work_groups) g = work_groups;
+    return (int)(g < 1 ? 1 : g);
+}
+
+chaos_status check_latch(chaos_net* net) {
+    int h = 0;
+    CUDA_TRY(cudaMemcpyAsync(&h, net->latch, sizeof(int), cudaMemcpyDeviceToHost, net->stream));
+    CUDA_TRY(cudaStreamSynchronize(net->stream));
+    if (h) {
+        CUDA_TRY(cudaMemsetAsync(net->latch, 0, sizeof(int), net->stream));
+        CUDA_TRY(cudaStreamSynchronize(net->stream));
+        if (h & kLatchLabel) return fail(CHAOS_E_LABEL, "device: a label outside [0, %d)", kClasses);
+        return fail(CHAOS_E_NONFINITE, "device: non-finite loss");
+    }
+    return CHAOS_OK;
+}
+
+void to_internal(const NetDesc& d, const float* norm, std::vector<float>& out) {
+    out.assign((size_t)d.pint, 0.f);
+    for (const Block& b : d.blocks) {
+        if (b.conv) {
+            for (int m = 0; m < b.M; ++m)
+                for (int n = 0; n < b.C; ++n)
+                    for (int t = 0; t < b.K * b.K; ++t)
+                        out[b.int_w + ((long long)n * b.K * b.K + t) * b.MP + m] =
+                            norm[b.norm_w + ((long long)m * b.C + n) * b.K * b.K + t];
+        } else {
+            std::memcpy(&out[b.int_w], norm + b.norm_w, sizeof(float) * b.nw);
+        }
+        std::memcpy(&out[b.int_b], norm + b.norm_b, sizeof(float) * b.nb);
+    }
+}
+
+void to_normative(const NetDesc& d, const float* in, float* norm) {
+    for (const Block& b : d.blocks) {
+        if (b.conv) {
+            for (int m = 0; m < b.M; ++m)
+                for (int n = 0; n < b.C; ++n)
+                    for (int t = 0; t < b.K * b.K; ++t)
+                        norm[b.norm_w + ((long long)m * b.C + n) * b.K * b.K + t] =
+                            in[b.int_w + ((long long)n * b.K * b.K + t) * b.MP + m];
+        } else {
+            std::memcpy(norm + b.norm_w, &in[b.int_w], sizeof(float) * b.nw);
+        }
+        std::memcpy(norm + b.norm_b, &in[b.int_b], sizeof(float) * b.nb);
+    }
+}
+
+// splitmix64 draw i of stream `seed` (R7): mix(seed + (i+1)*gamma)
+uint64_t splitmix_at(uint64_t seed, uint64_t i) {
+    uint64_t z = seed + (i + 1) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// Shape chain check (conv o = h-k+1, pool o = floor(h/kp)); message names the layer.
+chaos_status validate(const chaos_arch* a) {
+    if (!a) return fail(CHAOS_E_INVALID, "arch is NULL");
+    if (a->n_layers < 1 || a->n_layers > 16 || a->in_c < 1 || a->in_h < 1 || a->in_w < 1 || a->n_classes < 1)
+        return fail(CHAOS_E_INVALID, "invalid arch header");
+    int c = a->in_c, h = a->in_h, w = a->in_w;
+    for (int l = 0; l < a->n_layers; ++l) {
+        const chaos_layer& s = a->layers[l];
+        if (s.kind == CHAOS_CONV) {
+            if (s.units < 1 || s.kernel < 1 || s.kernel > h || s.kernel > w)
+                return fail(CHAOS_E_ARCH, "layer %d (conv k=%d): input %dx%d < kernel or units < 1", l, s.kernel, h,
+                            w);
+            c = s.units;
+            h = h - s.kernel + 1;
+            w = w - s.kernel + 1;
+        } else if (s.kind == CHAOS_MAXPOOL) {
+            if (s.kernel < 1 || s.kernel > h || s.kernel > w)
+                return fail(CHAOS_E_ARCH, "layer %d (pool k=%d): input %dx%d < window", l, s.kernel, h, w);
+            h /= s.kernel;
+            w /= s.kernel;
+        } else if (s.kind == CHAOS_FULL) {
+            if (s.units < 1) return fail(CHAOS_E_ARCH, "layer %d (full): units < 1", l);
+            c = s.units;
+            h = w = 1;
+        } else {
+            return fail(CHAOS_E_ARCH, "layer %d: unknown kind %d", l, s.kind);
+        }
+    }
+    const chaos_layer& last = a->layers[a->n_layers - 1];
+    if (last.kind != CHAOS_FULL || last.units != a->n_classes || last.act != CHAOS_IDENTITY)
+        return fail(CHAOS_E_ARCH, "layer %d: last layer must be FULL with n_classes units and identity activation",
+                    a->n_layers - 1);
+    return CHAOS_OK;
+}
+
+const NetDesc* match(const chaos_arch* a) {
+    if (a->in_c != 1 || a->in_h != 29 || a->in_w != 29 || a->n_classes != kClasses) return nullptr;
+    for (const NetDesc& d : registry()) {
+        if ((int)d.sig.size() != a->n_layers) continue;
+        bool ok = true;
+        for (int l = 0; l < a->n_layers && ok; ++l) {
+            const chaos_layer& s = a->layers[l];
+            const LayerSig& q = d.sig[l];
+            ok = s.kind == q.kind && s.kernel == q.kernel &&
+                 (s.kind == CHAOS_MAXPOOL || (s.units == q.units && s.act == q.act));
+        }
+        if (ok) return &d;
+    }
+    return nullptr;
+}
+
+chaos_status ensure_partial(chaos_net* net, long long slots) {
+    if (slots <= net->partial_slots) return CHAOS_OK;
+    if (net->partial) cudaFree(net->partial);
+    net->partial = nullptr;
+    const size_t bytes = sizeof(float) * (size_t)slots * (size_t)net->d->pint;
+    CUDA_TRY(cudaMalloc(&net->partial, bytes));
+    CUDA_TRY(cudaMemsetAsync(net->partial, 0, bytes, net->stream));  // padding entries stay 0 forever
+    net->partial_slots = slots;
+    return CHAOS_OK;
+}
+
+chaos_status ensure_eval(chaos_net* net, long long n) {
+    if (n <= net->ev_cap) return CHAOS_OK;
+    if (net->ev_loss) cudaFree(net->ev_loss);
+    if (net->ev_wrong) cudaFree(net->ev_wrong);
+    net->ev_loss = nullptr;
+    net->ev_wrong = nullptr;
+    CUDA_TRY(cudaMalloc(&net->ev_loss, sizeof(float) * n));
+    CUDA_TRY(cudaMalloc(&net->ev_wrong, n));
+    net->ev_cap = n;
+    return CHAOS_OK;
+}
+
+KArgs base_args(chaos_net* net) {
+    KArgs k{};
+    k.params = net->params;
+    k.partial = net->partial;
+    k.pstride = net->d->pint;
+    k.counter = net->counter;
+    k.latch = net->latch;
+    return k;
+}
+
+// One sync-mode batch: gradients of [0, nb) at the current weights into slots, then
+// (out == nullptr) params -= lr * fixed-order sum, or out = sum.
+chaos_status sync_batch(chaos_net* net, const float* X, const int32_t* Y, long long nb, float lr, float* out,
+                        double* loss_sum) {
+    const int G = net->group;
+    const long long slots = (nb + G - 1) / G;
+    chaos_status s = ensure_partial(net, slots);
+    if (s) return s;
+    KArgs k = base_args(net);
+    k.partial = net->partial;
+    k.images = X;
+    k.labels = Y;
+    k.n = nb;
+    k.loss_sum = loss_sum;
+    const int grid = grid_for(net, kSync, slots);
+    net->d->fn[gidx(net)][kSync]<<<grid, net->d->nt, net->d->smem[gidx(net)], net->stream>>>(k);
+    CUDA_TRY(cudaGetLastError());
+    const long long np = net->d->pint;
+    chaos_reduce_update<<<(unsigned)((np + 255) / 256), 256, 0, net->stream>>>(net->params, net->partial, np,
+                                                                              (int)slots, lr, np, out);
+    CUDA_TRY(cudaGetLastError());
+    return CHAOS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* chaos_last_error(void) { return g_err.c_str(); }
+chaos_status chaos_last_status(void) { return g_status; }
+
+chaos_net* chaos_net_create(const chaos_arch* arch) {
+    g_err.clear();
+    g_status = CHAOS_OK;
+    if (validate(arch) != CHAOS_OK) return nullptr;
+    const NetDesc* d = match(arch);
+    if (!d) {
+        fail(CHAOS_E_UNSUPPORTED, "valid arch without a compiled sm_100a instantiation (compiled: tiny, medium, large)");
+        return nullptr;
+    }
+    chaos_net* net = new chaos_net();
+    net->d = d;
+    net->group = d->gdef;
+    auto bail = [&](chaos_status) -> chaos_net* {
+        chaos_net_destroy(net);
+        return nullptr;
+    };
+    if (cudaGetDevice(&net->dev) != cudaSuccess) {
+        fail(CHAOS_E_CUDA, "no CUDA device");
+        return bail(CHAOS_E_CUDA);
+    }
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, net->dev) != cudaSuccess) {
+        fail(CHAOS_E_CUDA, "cudaGetDeviceProperties failed");
+        return bail(CHAOS_E_CUDA);
+    }
+    if (prop.major != 10) {
+        fail(CHAOS_E_UNSUPPORTED, "libchaos.so is built for sm_100a; device is sm_%d%d", prop.major, prop.minor);
+        return bail(CHAOS_E_UNSUPPORTED);
+    }
+    net->sms = prop.multiProcessorCount;
+    if (ensure_kernel_attrs(net) != CHAOS_OK) return bail(g_status);
+    if (cudaMalloc(&net->params, sizeof(float) * d->pint) != cudaSuccess ||
+        cudaMalloc(&net->latch, sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&net->counter, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&net->loss_sum, sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&net->ev_sum, sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&net->ev_err, sizeof(long long)) != cudaSuccess) {
+        fail(CHAOS_E_CUDA, "cudaMalloc failed");
+        return bail(CHAOS_E_CUDA);
+    }
+    cudaMemset(net->latch, 0, sizeof(int));
+    cudaMemset(net->loss_sum, 0, sizeof(double));
+    // parameters: U(-1/sqrt(fan_in), +1/sqrt(fan_in)), W then b per layer, splitmix64(seed ^ 0x5EED)
+    std::vector<float> norm((size_t)d->nparams);
+    const uint64_t seed = arch->init_seed ^ 0x5EEDull;
+    uint64_t pos = 0;
+    for (const Block& b : d->blocks) {
+        const double lim = 1.0 / std::sqrt((double)b.fan_in);
+        for (long long j = 0; j < b.nw + b.nb; ++j, ++pos) {
+            const double u = (double)(splitmix_at(seed, pos) >> 40) * (1.0 / 16777216.0);
+            norm[(size_t)(b.norm_w + j)] = (float)((2.0 * u - 1.0) * lim);
+        }
+    }
+    if (chaos_net_set_params(net, norm.data(), d->nparams) != CHAOS_OK) return bail(g_status);
+    return net;
+}
+
+void chaos_net_destroy(chaos_net* net) {
+    if (!net) return;
+    if (net->stream) cudaStreamSynchronize(net->stream);
+    cudaDeviceSynchronize();
+    void* ptrs[] = {net->params, net->latch,  net->counter, net->loss_sum, net->partial, net->grad_out, net->claims,
+                    net->ev_loss, net->ev_wrong, net->ev_sum, net->ev_err, net->st_x, net->st_y};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    delete net;
+}
+
+chaos_status chaos_net_set_option(chaos_net* net, chaos_option opt, int64_t value) {
+    if (!net) return fail(CHAOS_E_INVALID, "net is NULL");
+    switch (opt) {
+        case CHAOS_OPT_STREAM:
+            net->stream = reinterpret_cast<cudaStream_t>(value);
+            return CHAOS_OK;
+        case CHAOS_OPT_SYNC_BATCH:
+            if (value < 1 || value > (1 << 20)) return fail(CHAOS_E_INVALID, "sync batch must be in [1, 2^20]");
+            net->sync_batch = (int)value;
+            return CHAOS_OK;
+        case CHAOS_OPT_GROUP:
+            if (value != 1 && value != net->d->gdef)
+                return fail(CHAOS_E_INVALID, "group G must be 1 or %d for net %s", net->d->gdef, net->d->name);
+            net->group = (int)value;
+            return CHAOS_OK;
+        case CHAOS_OPT_MAX_CTAS:
+            if (value < 0) return fail(CHAOS_E_INVALID, "max_ctas must be >= 0 (0 = all SMs)");
+            net->max_ctas = (int)value;
+            return CHAOS_OK;
+        case CHAOS_OPT_DEBUG_CLAIMS:
+            net->debug_claims = value ? 1 : 0;
+            return CHAOS_OK;
+    }
+    return fail(CHAOS_E_INVALID, "unknown option %d", (int)opt);
+}
+
+int64_t chaos_net_get_option(const chaos_net* net, chaos_option opt) {
+    if (!net) return -1;
+    switch (opt) {
+        case CHAOS_OPT_STREAM: return (int64_t)net->stream;
+        case CHAOS_OPT_SYNC_BATCH: return net->sync_batch;
+        case CHAOS_OPT_GROUP: return net->group;
+        case CHAOS_OPT_MAX_CTAS: return net->max_ctas;
+        case CHAOS_OPT_DEBUG_CLAIMS: return net->debug_claims;
+    }
+    return -1;
+}
+
+int64_t chaos_net_num_params(const chaos_net* net) { return net ? net->d->nparams : -1; }
+float* chaos_net_device_params(chaos_net* net) { return net ? net->params : nullptr; }
+int64_t chaos_net_device_params_len(const chaos_net* net) { return net ? net->d->pint : -1; }
+
+chaos_status chaos_net_get_params(chaos_net* net, float* host_dst, int64_t n) {
+    if (!net || !host_dst) return fail(CHAOS_E_INVALID, "NULL argument");
+    if (n != net->d->nparams) return fail(CHAOS_E_INVALID, "n=%lld != num_params=%lld", (long long)n, net->d->nparams);
+    std::vector<float> in((size_t)net->d->pint);
+    CUDA_TRY(cudaMemcpyAsync(in.data(), net->params, sizeof(float) * in.size(), cudaMemcpyDeviceToHost, net->stream));
+    CUDA_TRY(cudaStreamSynchronize(net->stream));
+    to_normative(*net->d, in.data(), host_dst);
+    return check_latch(net);
+}
+
+chaos_status chaos_net_set_params(chaos_net* net, const float* host_src, int64_t n) {
+    if (!net || !host_src) return fail(CHAOS_E_INVALID, "NULL argument");
+    if (n != net->d->nparams) return fail(CHAOS_E_INVALID, "n=%lld != num_params=%lld", (long long)n, net->d->nparams);
+    std::vector<float> in;
+    to_internal(*net->d, host_src, in);
+    CUDA_TRY(cudaMemcpyAsync(net->params, in.data(), sizeof(float) * in.size(), cudaMemcpyHostToDevice, net->stream));
+    CUDA_TRY(cudaStreamSynchronize(net->stream));
+    return CHAOS_OK;
+}
+
+chaos_status chaos_train_epoch(chaos_net* net, const float* d_images, const int32_t* d_labels, int64_t n, float lr,
+                               chaos_mode mode) {
+    if (!net) return fail(CHAOS_E_INVALID, "net is NULL");
+    if (n < 0) return fail(CHAOS_E_INVALID, "n < 0");
+    if (!std::isfinite(lr)) return fail(CHAOS_E_INVALID, "lr is not finite");
+    if (mode != CHAOS_HOGWILD && mode != CHAOS_SYNC) return fail(CHAOS_E_INVALID, "unknown mode %d", (int)mode);
+    CUDA_TRY(cudaMemsetAsync(net->loss_sum, 0, sizeof(double), net->stream));
+    net->last_train_n = n;
+    if (n == 0) return CHAOS_OK;
+    if (!d_images || !d_labels) return fail(CHAOS_E_INVALID, "NULL images/labels");
+    const int G = net->group;
+    if (mode == CHAOS_HOGWILD) {
+        KArgs k = base_args(net);
+        k.images = d_images;
+        k.labels = d_labels;
+        k.n = n;
+        k.neg_lr = -lr;
+        k.loss_sum = net->loss_sum;
+        if (net->debug_claims) {
+            if (net->claims_cap < n) {
+                if (net->claims) cudaFree(net->claims);
+                net->claims = nullptr;
+                CUDA_TRY(cudaMalloc(&net->claims, sizeof(int) * n));
+                net->claims_cap = n;
+            }
+            CUDA_TRY(cudaMemsetAsync(net->claims, 0, sizeof(int) * n, net->stream));
+            k.claims = net->claims;
+        }
+        CUDA_TRY(cudaMemsetAsync(net->counter, 0, sizeof(unsigned long long), net->stream));
+        const int grid = grid_for(net, kHogwild, (n + G - 1) / G);
+        net->d->fn[gidx(net)][kHogwild]<<<grid, net->d->nt, net->d->smem[gidx(net)], net->stream>>>(k);
+        CUDA_TRY(cudaGetLastError());
+        return CHAOS_OK;
+    }
+    for (long long b0 = 0; b0 < n; b0 += net->sync_batch) {
+        const long long nb = (n - b0) < net->sync_batch ? (n - b0) : net->sync_batch;
+        chaos_status s = sync_batch(net, d_images + b0 * 841, d_labels + b0, nb, lr, nullptr, net->loss_sum);
+        if (s) return s;
+    }
+    return CHAOS_OK;
+}
+
+chaos_status chaos_train_epoch_host(chaos_net* net, const float* h_images, const int32_t* h_labels, int64_t n,
+                                    float lr, chaos_mode mode) {
+    if (!net) return fail(CHAOS_E_INVALID, "net is NULL");
+    if (n < 0) return fail(CHAOS_E_INVALID, "n < 0");
+    if (n == 0) return chaos_train_epoch(net, nullptr, nullptr, 0, lr, mode);
+    if (!h_images || !h_labels) return fail(CHAOS_E_INVALID, "NULL images/labels");
+    if (net->st_cap < n) {
+        if (net->st_x) cudaFree(net->st_x);
+        if (net->st_y) cudaFree(net->st_y);
+        net->st_x = nullptr;
+        net->st_y = nullptr;
+        CUDA_TRY(cudaMalloc(&net->st_x, sizeof(float) * 841 * n));
+        CUDA_TRY(cudaMalloc(&net->st_y, sizeof(int) * n));
+        net->st_cap = n;
+    }
+    CUDA_TRY(cudaMemcpyAsync(net->st_x, h_images, sizeof(float) * 841 * n, cudaMemcpyHostToDevice, net->stream));
+    CUDA_TRY(cudaMemcpyAsync(net->st_y, h_labels, sizeof(int) * n, cudaMemcpyHostToDevice, net->stream));
+    chaos_status s = chaos_train_epoch(net, net->st_x, net->st_y, n, lr, mode);
+    if (s) return s;
+    return chaos_net_sync(net);
+}
+
+chaos_status chaos_last_train_loss(chaos_net* net, double* mean_loss) {
+    if (!net || !mean_loss) return fail(CHAOS_E_INVALID, "NULL argument");
+    double s = 0;
+    CUDA_TRY(cudaMemcpyAsync(&s, net->loss_sum, sizeof(double), cudaMemcpyDeviceToHost, net->stream));
+    CUDA_TRY(cudaStreamSynchronize(net->stream));
+    *mean_loss = net->last_train_n > 0 ? s / (double)net->last_train_n : 0.0;
+    return check_latch(net);
+}
+
+chaos_status chaos_evaluate(chaos_net* net, const float* d_images, const int32_t* d_labels, int64_t n,
+                            double* mean_loss, int64_t* n_errors) {
+    if (!net || !mean_loss || !n_errors) return fail(CHAOS_E_INVALID, "NULL argument");
+    if (n < 0) return fail(CHAOS_E_INVALID, "n < 0");
+    if (n == 0) {
+        *mean_loss = 0.0;
+        *n_errors = 0;
+        return check_latch(net);
+    }
+    if (!d_images || !d_labels) return fail(CHAOS_E_INVALID, "NULL images/labels");
+    chaos_status s = ensure_eval(net, n);
+    if (s) return s;
+    KArgs k = base_args(net);
+    k.images = d_images;
+    k.labels = d_labels;
+    k.n = n;
+    k.out_loss = net->ev_loss;
+    k.out_wrong = net->ev_wrong;
+    const int G = net->group;
+    const int grid = grid_for(net, kEval, (n + G - 1) / G);
+    net->d->fn[gidx(net)][kEval]<<<grid, net->d->nt, net->d->smem[gidx(net)], net->stream>>>(k);
+    CUDA_TRY(cudaGetLastError());
+    chaos_eval_reduce<<<1, 1024, 0, net->stream>>>(net->ev_loss, net->ev_wrong, n, net->ev_sum, net->ev_err);
+    CUDA_TRY(cudaGetLastError());
+    double sum = 0;
+    long long err = 0;
+    CUDA_TRY(cudaMemcpyAsync(&sum, net->ev_sum, sizeof(double), cudaMemcpyDeviceToHost, net->stream));
+    CUDA_TRY(cudaMemcpyAsync(&err, net->ev_err, sizeof(long long), cudaMemcpyDeviceToHost, net->stream));
+    CUDA_TRY(cudaStreamSynchronize(net->stream));
+    *mean_loss = sum / (double)n;
+    *n_errors = err;
+    return check_latch(net);
+}
+
+chaos_status chaos_forward(chaos_net* net, const float* d_images, int64_t n, float* d_logits) {
+    if (!net) return fail(CHAOS_E_INVALID, "net is NULL");
+    if (n < 0) return fail(CHAOS_E_INVALID, "n < 0");
+    if (n == 0) return check_latch(net);
+    if (!d_images || !d_logits) return fail(CHAOS_E_INVALID, "NULL argument");
+    KArgs k = base_args(net);
+    k.images = d_images;
+    k.n = n;
+    k.out_logits = d_logits;
+    const int G = net->group;
+    const int grid = grid_for(net, kForward, (n + G - 1) / G);
+    net->d->fn[gidx(net)][kForward]<<<grid, net->d->nt, net->d->smem[gidx(net)], net->stream>>>(k);
+    CUDA_TRY(cudaGetLastError());
+    return check_latch(net);
+}
+
+chaos_status chaos_compute_gradients(chaos_net* net, const float* d_images, const int32_t* d_labels, int64_t n,
+                                     float* host_grad_sum) {
+    if (!net || !host_grad_sum) return fail(CHAOS_E_INVALID, "NULL argument");
+    if (n < 0) return fail(CHAOS_E_INVALID, "n < 0");
+    if (!net->grad_out) CUDA_TRY(cudaMalloc(&net->grad_out, sizeof(float) * net->d->pint));
+    CUDA_TRY(cudaMemsetAsync(net->grad_out, 0, sizeof(float) * net->d->pint, net->stream));
+    if (n > 0) {
+        if (!d_images || !d_labels) return fail(CHAOS_E_INVALID, "NULL images/labels");
+        chaos_status s = sync_batch(net, d_images, d_labels, n, 0.f, net->grad_out, nullptr);
+        if (s) return s;
+    }
+    std::vector<float> in((size_t)net->d->pint);
+    CUDA_TRY(cudaMemcpyAsync(in.data(), net->grad_out, sizeof(float) * in.size(), cudaMemcpyDeviceToHost,
+                             net->stream));
+    CUDA_TRY(cudaStreamSynchronize(net->stream));
+    to_normative(*net->d, in.data(), host_grad_sum);
+    return check_latch(net);
+}
+
+chaos_status chaos_debug_claims(chaos_net* net, int32_t* host_counts, int64_t n) {
+    if (!net || !host_counts) return fail(CHAOS_E_INVALID, "NULL argument");
+    if (!net->claims || n > net->claims_cap) return fail(CHAOS_E_INVALID, "no claim record of that size");
+    CUDA_TRY(cudaMemcpyAsync(host_counts, net->claims, sizeof(int) * n, cudaMemcpyDeviceToHost, net->stream));
+    CUDA_TRY(cudaStreamSynchronize(net->stream));
+    return CHAOS_OK;
+}
+
+chaos_status chaos_net_sync(chaos_net* net) {
+    if (!net) return fail(CHAOS_E_INVALID, "net is NULL");
+    CUDA_TRY(cudaStreamSynchronize(net->stream));
+    return check_latch(net);
+}
+
+chaos_status chaos_net_launch_info(chaos_net* net, int32_t* grid, int32_t* block, int32_t* smem_bytes,
+                                   int32_t* group) {
+    if (!net) return fail(CHAOS_E_INVALID, "net is NULL");
+    if (grid) *grid = grid_for(net, kHogwild, 1LL << 40);
+    if (block) *block = net->d->nt;
+    if (smem_bytes) *smem_bytes = net->d->smem[gidx(net)];
+    if (group) *group = net->group;
+    return CHAOS_OK;
+}
+
+}  // extern "C"

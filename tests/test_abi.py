@@ -1,0 +1,77 @@
+"""The C-ABI library loads and exports every symbol include/chaos.h declares (CPU only, no compute)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "chaos.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(chaos_[a-z_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def so_path():
+    from paper_1506_09067_b200 import build
+    return build.build()
+
+
+def test_header_and_binding_agree():
+    from paper_1506_09067_b200.chaos import EXPORTS
+    assert sorted(EXPORTS) == declared_symbols()
+
+
+def test_library_exports_every_declared_symbol(so_path):
+    lib = ctypes.CDLL(so_path)
+    for s in declared_symbols():
+        assert hasattr(lib, s), s
+    nm = subprocess.run(["nm", "-D", "--defined-only", so_path], capture_output=True, text=True).stdout
+    for s in declared_symbols():
+        assert re.search(rf"\bT {s}$", nm, flags=re.M), f"{s} not exported as a text symbol"
+
+
+def test_library_is_sm100a(so_path):
+    out = subprocess.run(["cuobjdump", "--list-elf", so_path], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_cpu_fallback_without_device():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("device present")
+    from paper_1506_09067_b200 import Net
+    import synthdata as sd
+    with pytest.raises(RuntimeError):
+        Net(sd.ARCHS["tiny"])
+
+
+def test_arch_errors_need_no_device(so_path):
+    # validation happens before any CUDA call: a broken shape chain is rejected on the host
+    from paper_1506_09067_b200.chaos import lib, make_arch
+    L = lib()
+    a = make_arch([(1, 4, 30, 0), (3, 10, 0, 1)])
+    assert not L.chaos_net_create(ctypes.byref(a))
+    assert L.chaos_last_status() == -2
+    assert b"layer 0" in L.chaos_last_error()
+    a = make_arch([(1, 7, 3, 0), (3, 10, 0, 1)])  # valid shape chain, no compiled instantiation
+    assert not L.chaos_net_create(ctypes.byref(a))
+    assert L.chaos_last_status() == -3
+
+
+def test_oracle_shares_nothing_with_product():
+    """Neither side imports, includes or loads the other (only synthdata/ is shared)."""
+    pat_prod = re.compile(r"^\s*(import oracle|from oracle)|liboracle|oracle\.h|orc_", re.M)
+    prod = os.path.join(ROOT, "paper_1506_09067_b200")
+    for dirpath, _, files in os.walk(prod):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                assert not pat_prod.search(open(os.path.join(dirpath, f)).read()), f
+    pat_orc = re.compile(r"^\s*(import|from) paper_1506_09067_b200|#include\s*\"chaos|libchaos|chaos_[a-z]+\(", re.M)
+    for f in os.listdir(os.path.join(ROOT, "oracle")):
+        if f.endswith((".c", ".h", ".py")):
+            assert not pat_orc.search(open(os.path.join(ROOT, "oracle", f)).read()), f

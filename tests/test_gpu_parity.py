@@ -1,0 +1,359 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element.
+
+Tolerance (reading R9): per tensor, |gpu-ref| <= 1e-4 * max(|ref|, 1e-2*||ref||_inf)
+element-wise and ||gpu-ref||_2 <= 1e-5 ||ref||_2 for gradients and weights after one step;
+mean test loss after one epoch within rel 1e-3 (BASELINE.json north_star).
+"""
+import json
+import os
+import itertools
+
+import numpy as np
+import pytest
+
+import synthdata as sd
+from oracle import Oracle
+from helpers import assert_parity, parity_report
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "oracle_runs")
+NETS = ["tiny", "medium", "large"]
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("gpu test selected but no CUDA device is visible")
+    return torch
+
+
+def make(name, seed, torch_cuda, group=None):
+    from paper_1506_09067_b200 import OPT_GROUP, Net
+    o = Oracle(sd.ARCHS[name])
+    net = Net(sd.ARCHS[name], init_seed=seed)
+    if group is not None:
+        net.set_option(OPT_GROUP, group)
+    p = sd.init_params(seed, o.blocks())
+    net.set_params(p)
+    return o, net, p
+
+
+def dev(torch, *arrays):
+    return [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in arrays]
+
+
+@pytest.mark.parametrize("name", NETS)
+def test_create_initialises_like_the_generator(name, torch_cuda):
+    from paper_1506_09067_b200 import Net
+    o = Oracle(sd.ARCHS[name])
+    for seed in (0, 1, 2):
+        net = Net(sd.ARCHS[name], init_seed=seed)
+        np.testing.assert_array_equal(net.get_params(), sd.init_params(seed, o.blocks()))
+        net.close()
+
+
+@pytest.mark.parametrize("name", NETS)
+def test_set_get_roundtrip(name, torch_cuda):
+    o, net, p = make(name, 3, torch_cuda)
+    q = np.random.default_rng(0).standard_normal(o.n_params).astype(np.float32)
+    net.set_params(q)
+    np.testing.assert_array_equal(net.get_params(), q)
+    assert net.device_params().numel() >= o.n_params
+
+
+@pytest.mark.parametrize("name", NETS)
+@pytest.mark.parametrize("group", [None, 1])
+def test_forward_logits(name, group, torch_cuda):
+    o, net, p = make(name, 4, torch_cuda, group)
+    d = sd.prototype_dataset(4, 0, 37)  # ragged vs G
+    X, = dev(torch_cuda, d.x_test)
+    logits = net.forward(X).cpu().numpy()
+    for i in range(37):
+        ref, _, _ = o.forward(p, d.x_test[i])
+        tol = 1e-4 * np.maximum(np.abs(ref), 1e-2 * np.abs(ref).max())
+        assert np.all(np.abs(logits[i] - ref) <= tol), (i, logits[i], ref)
+
+
+@pytest.mark.parametrize("name", NETS)
+@pytest.mark.parametrize("n", [1, 13])
+def test_gradients(name, n, torch_cuda):
+    o, net, p = make(name, 5, torch_cuda)
+    d = sd.prototype_dataset(5, n, 0)
+    X, Y = dev(torch_cuda, d.x_train, d.y_train)
+    g = net.compute_gradients(X, Y)
+    ref = np.zeros(o.n_params)
+    for i in range(n):
+        ref += o.sample_grad(p, d.x_train[i], d.y_train[i])[1]
+    assert_parity(g, ref, o.blocks())
+
+
+@pytest.mark.parametrize("name", NETS)
+def test_gradients_group1_equal_default_group(name, torch_cuda):
+    # G only changes the summation grouping: within tolerance of each other and the oracle
+    o, net, p = make(name, 6, torch_cuda, 1)
+    d = sd.prototype_dataset(6, 9, 0)
+    X, Y = dev(torch_cuda, d.x_train, d.y_train)
+    g1 = net.compute_gradients(X, Y)
+    _, net2, _ = make(name, 6, torch_cuda)
+    g4 = net2.compute_gradients(X, Y)
+    assert_parity(g1, g4.astype(np.float64), o.blocks())
+
+
+@pytest.mark.parametrize("name", NETS)
+def test_sync_steps(name, torch_cuda):
+    # 3 sync batches (B=64, last one partial: 150 = 64+64+22), weights after the steps
+    from paper_1506_09067_b200 import OPT_SYNC_BATCH, SYNC
+    o, net, p = make(name, 7, torch_cuda)
+    net.set_option(OPT_SYNC_BATCH, 64)
+    d = sd.prototype_dataset(7, 150, 0)
+    X, Y = dev(torch_cuda, d.x_train, d.y_train)
+    lr = 0.05
+    net.train_epoch(X, Y, lr, SYNC)
+    got = net.get_params()
+    ref, _ = o.train_sync(p, d.x_train, d.y_train, lr, 64)
+    # the weights move by lr*g: compare the step (ref - p) as well as the weights
+    assert_parity(got, ref, o.blocks())
+    step_ok, w, wn, _ = parity_report(got.astype(np.float64) - p, ref - p, o.blocks(), rel=1e-3, floor=1e-2,
+                                      norm_rel=1e-4)
+    assert step_ok, (w, wn)
+
+
+def test_sync_is_bitwise_deterministic(torch_cuda):
+    from paper_1506_09067_b200 import OPT_SYNC_BATCH, SYNC
+    d = sd.prototype_dataset(8, 500, 0)
+    outs = []
+    for _ in range(2):
+        o, net, p = make("large", 8, torch_cuda)
+        net.set_option(OPT_SYNC_BATCH, 64)
+        X, Y = dev(torch_cuda, d.x_train, d.y_train)
+        net.train_epoch(X, Y, 0.01, SYNC)
+        outs.append(net.get_params())
+    np.testing.assert_array_equal(outs[0], outs[1])
+
+
+def test_sync_epoch_config0(torch_cuda):
+    # BASELINE.json configs[0]: tiny net, 1,000 / 200 images, sync batch 1, lr 0.01, 1 epoch
+    from paper_1506_09067_b200 import OPT_SYNC_BATCH, SYNC
+    w = sd.WORKLOADS["config0"]
+    d = sd.make_dataset(w)
+    o, net, p = make("tiny", w.seed, torch_cuda)
+    net.set_option(OPT_SYNC_BATCH, 1)
+    X, Y, Xt, Yt = dev(torch_cuda, d.x_train, d.y_train, d.x_test, d.y_test)
+    net.train_epoch(X, Y, w.lr0, SYNC)
+    ml, ne = net.evaluate(Xt, Yt)
+    refp, _ = o.train_sync(p, d.x_train, d.y_train, w.lr0, 1)
+    rml, rne = o.evaluate(refp, d.x_test, d.y_test)
+    assert abs(ml - rml) <= 1e-3 * abs(rml)
+    assert abs(ne - rne) <= 2  # argmax near-ties may flip (reading R9)
+
+
+@pytest.mark.parametrize("run", ["config1_sync64", "config2_sync64_e1", "config3_sync64_e1"])
+def test_sync_epoch_loss_vs_oracle_run(run, torch_cuda):
+    # one full epoch of sync B=64 on the 60k set; mean test CE within rel 1e-3 of the oracle's
+    from paper_1506_09067_b200 import OPT_SYNC_BATCH, SYNC
+    path = os.path.join(GOLD, run + ".json")
+    if not os.path.exists(path):
+        pytest.skip(f"oracle reference run {run} not recorded yet")
+    rec = json.load(open(path))
+    w = sd.WORKLOADS[rec["workload"]]
+    d = sd.make_dataset(w)
+    assert d.sha256() == rec["data_sha256"]
+    o, net, p = make(w.arch, w.seed, torch_cuda)
+    net.set_option(OPT_SYNC_BATCH, 64)
+    X, Y, Xt, Yt = dev(torch_cuda, d.x_train, d.y_train, d.x_test, d.y_test)
+    net.train_epoch(X, Y, w.lr0, SYNC)
+    ml, ne = net.evaluate(Xt, Yt)
+    e1 = rec["per_epoch"][0]
+    assert abs(ml - e1["test_mean_loss"]) <= 1e-3 * e1["test_mean_loss"], (ml, e1)
+    assert abs(ne - e1["test_errors"]) <= 5
+
+
+@pytest.mark.parametrize("name", NETS)
+def test_hogwild_single_worker_is_sequential_sgd(name, torch_cuda):
+    # one CTA, G = 1: CHAOS with one worker = sequential SGD (SURVEY C-9)
+    from paper_1506_09067_b200 import OPT_MAX_CTAS
+    o, net, p = make(name, 9, torch_cuda, 1)
+    net.set_option(OPT_MAX_CTAS, 1)
+    d = sd.prototype_dataset(9, 24, 0)
+    X, Y = dev(torch_cuda, d.x_train, d.y_train)
+    net.train_epoch(X, Y, 0.05)
+    got = net.get_params()
+    ref, _ = o.train_sgd(p, d.x_train, d.y_train, 0.05)
+    assert_parity(got, ref, o.blocks())
+
+
+@pytest.mark.parametrize("name", NETS)
+def test_hogwild_claims_each_image_exactly_once(name, torch_cuda):
+    from paper_1506_09067_b200 import OPT_DEBUG_CLAIMS
+    o, net, p = make(name, 10, torch_cuda)
+    net.set_option(OPT_DEBUG_CLAIMS, 1)
+    n = 10003
+    d = sd.prototype_dataset(10, n, 0)
+    X, Y = dev(torch_cuda, d.x_train, d.y_train)
+    net.train_epoch(X, Y, 0.001)
+    net.sync()
+    np.testing.assert_array_equal(net.debug_claims(n), np.ones(n, np.int32))
+
+
+def interval_orders(n):
+    """All strict interval orders on n samples, as the set of predecessors of each sample.
+
+    Enumerated as the distinct read-before-publish patterns of n workers: each sample i
+    reads at time r_i and publishes at time w_i > r_i; j precedes i iff w_j < r_i."""
+    pats = set()
+    for perm in itertools.permutations(range(2 * n)):
+        r = perm[:n]
+        w = perm[n:]
+        if any(w[i] < r[i] for i in range(n)):
+            continue
+        pats.add(tuple(frozenset(j for j in range(n) if w[j] < r[i]) for i in range(n)))
+    return sorted(pats, key=str)
+
+
+def replay(o, p, X, Y, lr, preds):
+    """Hogwild replay: sample i computed at W0 - lr*sum_{j<i} g_j."""
+    n = len(Y)
+    order = sorted(range(n), key=lambda i: len(preds[i]))
+    g = {}
+    for i in order:
+        w = p.astype(np.float64).copy()
+        for j in preds[i]:
+            w -= lr * g[j]
+        g[i] = o.sample_grad(w, X[i], Y[i])[1]
+    return p - lr * sum(g.values())
+
+
+def test_interval_order_counts():
+    assert len(interval_orders(2)) == 3
+    assert len(interval_orders(3)) == 19
+
+
+@pytest.mark.parametrize("name", ["tiny", "large"])
+def test_hogwild_three_samples_brute_force(name, torch_cuda):
+    # 3 workers x G=1 on 3 samples: the result is one of the 19 replay outcomes
+    # (or a mixed-layer read, which per-layer publishing allows: reported)
+    o, net, p = make(name, 11, torch_cuda, 1)
+    d = sd.prototype_dataset(11, 3, 0)
+    X, Y = dev(torch_cuda, d.x_train, d.y_train)
+    lr = 0.5
+    net.train_epoch(X, Y, lr)
+    got = net.get_params().astype(np.float64)
+    best = np.inf
+    for preds in interval_orders(3):
+        ref = replay(o, p, d.x_train, d.y_train, lr, preds)
+        ok, w, wn, _ = parity_report(got, ref, o.blocks())
+        best = min(best, max(w, wn))
+        if ok:
+            return
+    pytest.xfail(f"mixed-layer read (closest replay at {best:.3g} x tol)")
+
+
+def test_evaluate_matches_oracle_and_is_pure(torch_cuda):
+    o, net, p = make("large", 12, torch_cuda)
+    d = sd.prototype_dataset(12, 0, 301)
+    Xt, Yt = dev(torch_cuda, d.x_test, d.y_test)
+    before = net.get_params()
+    ml, ne = net.evaluate(Xt, Yt)
+    np.testing.assert_array_equal(net.get_params(), before)
+    rml, rne, _, rpred = o.evaluate(p, d.x_test, d.y_test, per_sample=True)
+    assert abs(ml - rml) <= 1e-4 * rml
+    logits = net.forward(Xt).cpu().numpy()
+    assert ne == int(np.sum(np.argmax(logits, 1) != d.y_test))  # brute force over the GPU logits
+    assert abs(ne - rne) <= 2
+
+
+def test_evaluate_group_independent(torch_cuda):
+    from paper_1506_09067_b200 import OPT_GROUP
+    o, net, p = make("medium", 13, torch_cuda)
+    d = sd.prototype_dataset(13, 0, 97)
+    Xt, Yt = dev(torch_cuda, d.x_test, d.y_test)
+    a = net.evaluate(Xt, Yt)
+    net.set_option(OPT_GROUP, 1)
+    b = net.evaluate(Xt, Yt)
+    assert a[1] == b[1] and abs(a[0] - b[0]) <= 1e-6 * a[0]
+
+
+def test_label_out_of_range_is_latched(torch_cuda):
+    from paper_1506_09067_b200 import ChaosError
+    o, net, p = make("tiny", 14, torch_cuda)
+    d = sd.prototype_dataset(14, 8, 0)
+    y = d.y_train.copy()
+    y[3] = 10
+    X, Y = dev(torch_cuda, d.x_train, y)
+    net.train_epoch(X, Y, 0.01)
+    with pytest.raises(ChaosError, match="LABEL"):
+        net.sync()
+    net.sync()  # latch cleared
+
+
+def test_empty_and_invalid(torch_cuda):
+    from paper_1506_09067_b200 import ChaosError, SYNC
+    o, net, p = make("tiny", 15, torch_cuda)
+    X, Y = dev(torch_cuda, np.zeros((0, 841), np.float32), np.zeros(0, np.int32))
+    net.train_epoch(X, Y, 0.01)
+    net.train_epoch(X, Y, 0.01, SYNC)
+    assert net.evaluate(X, Y) == (0.0, 0)
+    np.testing.assert_array_equal(net.get_params(), p)
+    with pytest.raises(ChaosError, match="INVALID"):
+        net.train_epoch(X, Y, float("nan"))
+
+
+def test_host_entry_point(torch_cuda):
+    # chaos_train_epoch_host (e2e path) equals device-buffer training in sync mode
+    from paper_1506_09067_b200 import OPT_SYNC_BATCH, SYNC
+    d = sd.prototype_dataset(16, 200, 0)
+    o, a, p = make("large", 16, torch_cuda)
+    a.set_option(OPT_SYNC_BATCH, 64)
+    a.train_epoch_host(d.x_train, d.y_train, 0.01, SYNC)
+    _, b, _ = make("large", 16, torch_cuda)
+    b.set_option(OPT_SYNC_BATCH, 64)
+    X, Y = dev(torch_cuda, d.x_train, d.y_train)
+    b.train_epoch(X, Y, 0.01, SYNC)
+    np.testing.assert_array_equal(a.get_params(), b.get_params())
+
+
+def test_full_size_sampled_parity(torch_cuda):
+    # the bench launch configuration (large net, default G, all SMs) on the 60k set:
+    # sampled logits and gradients of single images checked one by one against the oracle
+    w = sd.WORKLOADS["config3"]
+    d = sd.make_dataset(w, 60000, 64)
+    o, net, p = make("large", w.seed, torch_cuda)
+    X, = dev(torch_cuda, d.x_train)
+    logits = net.forward(X).cpu().numpy()
+    rng = np.random.default_rng(0)
+    for i in rng.choice(60000, 12, replace=False):
+        ref, _, _ = o.forward(p, d.x_train[i])
+        tol = 1e-4 * np.maximum(np.abs(ref), 1e-2 * np.abs(ref).max())
+        assert np.all(np.abs(logits[i] - ref) <= tol), i
+    # sum of gradients over a 4096-image slice equals the sum of the oracle's per-image gradients
+    Xs, Ys = dev(torch_cuda, d.x_train[:256], d.y_train[:256])
+    g = net.compute_gradients(Xs, Ys)
+    ref = np.zeros(o.n_params)
+    for i in range(256):
+        ref += o.sample_grad(p, d.x_train[i], d.y_train[i])[1]
+    assert_parity(g, ref, o.blocks())
+
+
+@pytest.mark.parametrize("run", ["config1_seq", "config3_seq", "config2_seq"])
+def test_hogwild_accuracy_gate(run, torch_cuda):
+    # BASELINE.json north_star: hogwild test error within 0.5 pp of the oracle's sequential SGD
+    import torch
+    path = os.path.join(GOLD, run + ".json")
+    if not os.path.exists(path):
+        pytest.skip(f"oracle reference run {run} not recorded yet")
+    rec = json.load(open(path))
+    if len(rec["per_epoch"]) < rec["epochs"]:
+        pytest.skip(f"oracle reference run {run} incomplete")
+    w = sd.WORKLOADS[rec["workload"]]
+    d = sd.make_dataset(w)
+    assert d.sha256() == rec["data_sha256"]
+    o, net, p = make(w.arch, w.seed, torch_cuda)
+    X, Y, Xt, Yt = dev(torch, d.x_train, d.y_train, d.x_test, d.y_test)
+    curve = []
+    for e in range(w.epochs):
+        net.train_epoch(X, Y, w.lr0 * 0.9 ** e)
+        curve.append(net.evaluate(Xt, Yt))
+    ref = rec["per_epoch"][-1]
+    n = len(d.y_test)
+    assert abs(curve[-1][1] - ref["test_errors"]) / n * 100 <= 0.5, (curve, ref)
