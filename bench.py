@@ -1,0 +1,299 @@
+"""Benchmark of the CHAOS hot path on B200 (contract: one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload config3]
+
+Workload (BASELINE.json configs[3]): the large net (conv20 4x4 -> pool2 -> conv60 3x3 -> pool2
+floor -> conv100 2x2 -> pool2 -> FC 400->150 -> FC 150->10), hogwild (CHAOS) mode, synthetic
+prototype+noise 29x29 fp32 data.  One *step* = one Training phase (epoch) over 60,000 images per
+GPU: claim, forward, softmax-CE, back-propagation and the controlled-hogwild update of every
+image, plus the NCCL weight average every K=1024 images per GPU when
+N > 1 (row a9).  Weak scaling: 60,000 images per GPU per step (N=1: configs[3]; N>1: the
+configs[4] generator, seed 2, rank r gets images [60000 r, 60000 (r+1))).  Evaluation (row a8)
+is timed separately and reported under "eval".  Inputs (202 MB per GPU) exceed the 126 MB L2.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synthdata as sd  # noqa: E402
+
+PER_GPU = 60000
+K_AVG = 1024
+METRIC = "training samples/sec (fwd+bwd+update) at 1/2/4/8 B200; % of FP32 roofline"
+# FP32 FFMA peak from unit counts and clock: 148 SMs x 128 FFMA/clk x 2 FLOP x 1.965 GHz
+N_SM = 148
+FP32_PEAK_TFLOPS = N_SM * 128 * 2 * 1.965e9 / 1e12
+# algorithmic FLOP per training image: forward of the conv outputs
+# the pools use, argmax-only backward (gW and delta_in), 2 FLOP per parameter for the update
+ALGO_FLOP = {"tiny": 202_990, "medium": 4_985_880, "large": 5_495_720}
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.index), "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def make_data(world, rank):
+    if world == 1:
+        w = sd.WORKLOADS["config3"]
+        d = sd.make_dataset(w, PER_GPU, 10000)
+        return w, d.x_train, d.y_train, d.x_test, d.y_test
+    w = sd.WORKLOADS["config4"]
+    xs, ys = sd.prototype_samples(w.seed, rank * PER_GPU, PER_GPU)
+    xt, yt = sd.prototype_samples(w.seed, w.n_train, 10000)
+    return w, xs, ys, xt, yt
+
+
+def cpu_baseline(arch, seconds=12.0):
+    """The oracle as it stands (double, 1 thread) on a bounded sample of the same workload."""
+    from oracle import Oracle
+    w = sd.WORKLOADS["config3"]
+    o = Oracle(sd.ARCHS[arch])
+    p = sd.init_params(w.seed, o.blocks())
+    xs, ys = sd.prototype_samples(w.seed, 0, 4000)
+    # calibrate on 64 images, then run a sample sized to ~`seconds`
+    t = time.perf_counter()
+    o.train_sgd(p, xs[:64], ys[:64], w.lr0)
+    per = (time.perf_counter() - t) / 64
+    n = int(max(64, min(4000, seconds / per)))
+    t = time.perf_counter()
+    o.train_sgd(p, xs[:n], ys[:n], w.lr0)
+    dt = time.perf_counter() - t
+    return {"value": n / dt, "unit": "samples/s", "cores": 1, "kind": "oracle",
+            "sample": f"sequential SGD (oracle, float64, 1 thread) over the first {n} images of configs[3]"}
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    from oracle import Oracle
+    w = sd.WORKLOADS["config3"]
+    o = Oracle(sd.ARCHS["large"])
+    p = sd.init_params(w.seed, o.blocks())
+    per_step = args.ref_images
+    xs, ys = sd.prototype_samples(w.seed, 0, per_step * (args.warmup + args.steps))
+    for s in range(args.warmup):
+        p, _ = o.train_sgd(p, xs[s * per_step:(s + 1) * per_step], ys[s * per_step:(s + 1) * per_step], w.lr0)
+    t = time.perf_counter()
+    for s in range(args.warmup, args.warmup + args.steps):
+        p, _ = o.train_sgd(p, xs[s * per_step:(s + 1) * per_step], ys[s * per_step:(s + 1) * per_step], w.lr0)
+    dt = time.perf_counter() - t
+    v = per_step * args.steps / dt
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "configs[3] large net, sequential SGD (the oracle) on a bounded sample",
+                       "images_per_step": per_step, "arch": "large"},
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{per_step} images of configs[3] per step, oracle float64, 1 thread"},
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--arch", default="large", choices=["tiny", "medium", "large"])
+    ap.add_argument("--k", type=int, default=K_AVG)
+    ap.add_argument("--ref-images", type=int, default=400)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1506_09067_b200 import HOGWILD, Net
+    from paper_1506_09067_b200.dist import DistTrainer
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w, xs, ys, xt, yt = make_data(world, rank)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    net = Net(sd.ARCHS[args.arch], init_seed=w.seed, stream=stream)
+    info = net.launch_info()
+    X = torch.from_numpy(xs).cuda()
+    Y = torch.from_numpy(ys).cuda()
+    Xt = torch.from_numpy(xt).cuda()
+    Yt = torch.from_numpy(yt).cuda()
+    trainer = DistTrainer(net, rank, world, args.k)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    lr = w.lr0
+    for s in range(args.warmup):
+        trainer.epoch(X, Y, lr * 0.9 ** s)
+    net.sync()
+    barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = trainer.n_launches
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    t0.record(stream)
+    for s in range(args.steps):
+        ev[s][0].record(stream)
+        trainer.epoch(X, Y, lr * 0.9 ** (args.warmup + s))
+        ev[s][1].record(stream)
+    t1.record(stream)
+    barrier()
+    clocks = clk.stop()
+    elapsed = t0.elapsed_time(t1) / 1e3
+    per_step_ms = [a.elapsed_time(b) for a, b in ev]
+    launches = trainer.n_launches - launches0
+    tmax = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    elapsed = float(tmax.item())
+    total = PER_GPU * world * args.steps
+    value = total / elapsed
+    train_loss = net.last_train_loss()
+
+    # a8: evaluation on the averaged model (timed separately)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    ml, ne = net.evaluate(Xt, Yt)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    eval_ms = e0.elapsed_time(e1)
+
+    # e2e: the same metric through the public C-ABI host-buffer entry (H2D of every step's
+    # images + labels from pinned memory, D2H of the step's mean training loss)
+    e2e = None
+    if not args.no_e2e and world == 1:
+        Xh = torch.from_numpy(xs).pin_memory()
+        Yh = torch.from_numpy(ys).pin_memory()
+        net.train_epoch_host(Xh, Yh, lr * 0.5)  # warm the staging buffers
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for s in range(args.steps):
+            net.train_epoch_host(Xh, Yh, lr * 0.5)
+            net.last_train_loss()
+        dt = time.perf_counter() - t
+        e2e = {"value": PER_GPU * args.steps / dt, "unit": "samples/s",
+               "h2d_bytes_per_step": int(Xh.numel() * 4 + Yh.numel() * 4), "d2h_bytes_per_step": 8}
+
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+    # roofline of the dominant kernel: the persistent worker (one launch per step at N=1)
+    kern_s = statistics.median(per_step_ms) / 1e3 if world == 1 else elapsed / args.steps
+    achieved = ALGO_FLOP[args.arch] * PER_GPU / kern_s / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "latest_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(args.arch)
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "configs[3] large net, hogwild (CHAOS), 60,000 images per GPU per step"
+                               + ("" if world == 1 else f"; configs[4] generator, NCCL average every {args.k}"),
+                   "arch": args.arch, "mode": "hogwild", "images_per_gpu_per_step": PER_GPU,
+                   "group_G": info["group"], "ctas": info["grid"], "threads_per_cta": info["block"],
+                   "smem_bytes_per_cta": info["smem_bytes"], "sync_interval_K": args.k if world > 1 else None,
+                   "l2": "inputs (202 MB/GPU) larger than the 126 MB L2", "parallelism": f"dp{world}"},
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic,
+                     "kernel": "chaos_worker<LargeNet,G,512,kHogwild>",
+                     "flop_per_image": ALGO_FLOP[args.arch],
+                     "peak_source": "148 SM x 128 FFMA/clk x 2 x 1.965 GHz (unit counts x max clock)"},
+        "clocks": clocks,
+        "gpu_launches": launches,
+        "e2e": e2e,
+        "eval": {"images": int(Yt.shape[0]), "ms": eval_ms, "samples_per_s": Yt.shape[0] / (eval_ms / 1e3),
+                 "test_mean_loss": ml, "test_errors": ne},
+        "train_mean_loss_last_step": train_loss,
+        "per_step_ms": per_step_ms,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.arch)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,65 @@
+"""Multi-GPU plumbing (BASELINE.json north_star): one process per GPU,
+contiguous data shards, and an allreduce-average of all parameters every K local images.
+
+Each rank trains its replica in hogwild mode on its shard; after every interval of K
+images (and at the end of the shard) the replicas are averaged, w <- (1/P) sum_r w_r
+(reading R11: average weights, not summed deltas).  The collective is
+torch.distributed (NCCL on GPUs; gloo on CPU for the host-logic tests); the averaging
+runs on the training stream so the next interval's kernel sees the averaged weights.
+"""
+from __future__ import annotations
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous shard [r*n/P, (r+1)*n/P) of rank r (SURVEY C-10), rounded to multiples of 4
+    so every shard start keeps the 16-B image alignment the bulk copies use."""
+    def edge(r):
+        return (n * r // world) // 4 * 4 if r < world else n
+    return edge(rank), edge(rank + 1)
+
+
+def intervals(lo: int, hi: int, k: int) -> list[tuple[int, int]]:
+    """Sync intervals of at most k images over [lo, hi); an average follows each one."""
+    if k <= 0:
+        return [(lo, hi)] if hi > lo else []
+    return [(s, min(s + k, hi)) for s in range(lo, hi, k)]
+
+
+def n_averages(n_local: int, k: int) -> int:
+    return len(intervals(0, n_local, k))
+
+
+def average_(tensor, world: int, group=None):
+    """In-place all-reduce average.  NCCL has ReduceOp.AVG; gloo does not (sum, then scale)."""
+    import torch.distributed as dist
+    if world == 1:
+        return tensor
+    if dist.get_backend(group) == "nccl":
+        dist.all_reduce(tensor, op=dist.ReduceOp.AVG, group=group)
+    else:
+        dist.all_reduce(tensor, op=dist.ReduceOp.SUM, group=group)
+        tensor.div_(world)
+    return tensor
+
+
+class DistTrainer:
+    """Trains one replica per rank with periodic averaging.
+
+    ``net`` needs ``train_epoch(images, labels, lr)`` and ``device_params()`` (the
+    chaos.Net API); tests substitute a CPU stand-in with the same two methods."""
+
+    def __init__(self, net, rank: int, world: int, k: int, group=None):
+        self.net, self.rank, self.world, self.k, self.group = net, rank, world, k, group
+        self.n_collectives = 0
+        self.n_launches = 0
+
+    def epoch(self, images, labels, lr: float, lo: int = 0, hi: int | None = None):
+        """One Training phase over this rank's images[lo:hi) (already sharded by the caller)."""
+        hi = int(labels.shape[0]) if hi is None else hi
+        params = self.net.device_params()
+        for s, e in intervals(lo, hi, self.k if self.world > 1 else 0):
+            self.net.train_epoch(images[s:e], labels[s:e], lr)
+            self.n_launches += 1
+            if self.world > 1:
+                average_(params, self.world, self.group)
+                self.n_collectives += 1
