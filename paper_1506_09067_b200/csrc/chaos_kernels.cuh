@@ -7,12 +7,17 @@
 // faster workers can process more images"), runs the whole forward pass, the
 // softmax cross-entropy error and the back-propagation for its G images with every
 // activation, argmax and partial derivative in shared memory, and publishes each
-// layer's gradient sum with fp32 REDs into the one shared weight copy in HBM/L2
-// right after that layer's gradients are computed (controlled hogwild:
-// "updates of shared weights are delayed to the end of each layer's computations";
-// PAPER.md:140, arbitrary order of synchronization: no locks, first come first
-// served writes, on-demand reads).  Conv-layer weights are read on demand from L2
-// into shared memory with one cp.async.bulk (TMA bulk copy) per layer and group.
+// layer's gradient sum into the one shared fp32 weight store right after that layer's
+// gradients are computed (controlled hogwild: "updates of shared weights
+// are delayed to the end of each layer's computations", arbitrary order
+// of synchronization: no locks, first come first served writes, on-demand reads).
+//
+// Blackwell mapping: conv weights are read on demand from L2 into shared memory with
+// TMA bulk copies (cp.async.bulk, SASS UBLKCP) issued ahead of use; a layer's gradient
+// (-lr * sum over the G images) is assembled in shared memory in the weight store's
+// layout and published with ONE TMA bulk reduction (cp.reduce.async.bulk .add.f32,
+// SASS UBLKRED) -- the TMA engine performs the fp32 adds in L2, no per-element atomics
+// from the SM.  Sync mode publishes the same buffer with a bulk copy into its slot.
 //
 // Layer arithmetic (readings R1-R5):
 //   conv   z[m][r][c] = b[m] + sum_n sum_i sum_j W[m][n][i][j] * a[n][r+i][c+j]
@@ -31,6 +36,7 @@ namespace chaos {
 constexpr int kClasses = 10;
 constexpr int kZStride = 16;  // logits / output-delta row stride in shared memory
 constexpr int kHdrBytes = 256;
+constexpr int kBiasScratch = 256;  // floats: FC bias-gradient scratch
 
 enum Mode : int { kHogwild = 0, kSync = 1, kEval = 2, kForward = 3 };
 enum Latch : int { kLatchLabel = 1, kLatchNonfinite = 2 };
@@ -40,23 +46,24 @@ __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 
 // Convolution block: conv (valid, stride 1, C->M maps, KxK) -> tanh -> KPxKP max-pool (floor).
 // Tuning knobs: MT maps per thread in the forward; TT taps per thread and GS split of the
-// (image, window) sum in the weight gradient; NCH input maps per thread in delta_in.
-template <int C_, int H_, int W_, int M_, int K_, int KP_, int MT_, int TT_, int GS_, int NCH_>
+// (image, window) sum in the weight gradient; RB input rows per band in delta_in.
+template <int C_, int H_, int W_, int M_, int K_, int KP_, int MT_, int TT_, int GS_, int RB_>
 struct Conv {
     static constexpr int C = C_, H = H_, W = W_, M = M_, K = K_, KP = KP_;
     static constexpr int OH = H - K + 1, OW = W - K + 1;
     static constexpr int PH = OH / KP, PW = OW / KP, P = PH * PW;
-    static constexpr int MP = round4(M);     // internal row pitch (maps padded to 16 B)
+    static constexpr int MP = round4(M);  // internal row pitch (maps padded to 16 B)
     static constexpr int KK = K * K;
-    static constexpr int ROWS = C * KK;      // internal W is [C*K*K][MP], bias [MP]
-    static constexpr int WFL = ROWS * MP, BFL = MP;
+    static constexpr int ROWS = C * KK;   // internal W is [C*K*K][MP], bias [MP]
+    static constexpr int WFL = ROWS * MP, BFL = MP, BLK = WFL + BFL;
     static constexpr int IN_SZ = C * H * W, OUT_SZ = M * P;
-    static constexpr int MT = MT_, TT = TT_, GS = GS_, NCH = NCH_;
+    static constexpr int MT = MT_, TT = TT_, GS = GS_, RB = RB_;
+    static constexpr int NB = (H + RB - 1) / RB;
     static_assert(M % MT == 0, "MT must divide M");
     static_assert(KK % TT == 0, "TT must divide K*K");
-    static_assert(C % NCH == 0, "NCH must divide C");
+    static_assert(RB % KP == 0 || NB == 1, "bands must start on a window row");
     static_assert(PH >= 1 && PW >= 1, "pool larger than the conv output");
-    static constexpr int SCRATCH = GS > 1 ? GS * WFL : 0;
+    static constexpr int GW_SCRATCH = (GS > 1 ? GS * WFL : 0) + BLK;  // floats to assemble gW (+ splits)
 };
 
 // Fully connected layer IN -> OUT, tanh or identity (logits).
@@ -88,28 +95,34 @@ struct POff {
     static constexpr int total = f2b + (Net::NFULL >= 2 ? F2::BFL : 0);
 };
 
-// Shared-memory carve-up for G images per worker.
+// Shared-memory carve-up for G images per worker (floats unless noted).
+//   S     : images during the forward pass; FC gradient scratch (two halves); the last conv
+//           layer's delta_in output (3 conv layers); the images again for conv1's gradient
+//   A1..3 : pooled activations, overwritten in place by their partial derivatives
+//   HH, Z : hidden FC activations / deltas, logits / output deltas
+//   WB    : staged conv weights (prefetched ahead) and conv gradient scratch
 template <class Net, int G>
 struct SLayout {
     using C1 = typename Net::C1;
     using C2 = typename Net::C2;
     using C3 = typename Net::C3;
     using F1 = typename Net::F1;
-    static constexpr int conv_blk(int w, int b) { return w + b; }
     static constexpr int WBUF = round4(cmax(
-        cmax(cmax(C1::WFL + C1::BFL, C1::SCRATCH),
-             Net::NCONV >= 2 ? cmax(C2::WFL + C2::BFL, C2::SCRATCH) : 0),
-        Net::NCONV >= 3 ? cmax(C3::WFL + C3::BFL, C3::SCRATCH) : 0));
-    static constexpr int X = 0;  // float offsets, relative to the float arena
-    static constexpr int A1 = X + round4(G * C1::IN_SZ);
+        cmax(cmax(C1::BLK + (Net::NCONV >= 2 ? C2::BLK : 0), C1::GW_SCRATCH),
+             Net::NCONV >= 3 ? 2 * C2::BLK : 0),
+        Net::NCONV >= 3 ? C3::BLK : 0));
+    static constexpr int SFL = round4(cmax(cmax(G * C1::IN_SZ, Net::SFL),
+                                           Net::NCONV >= 3 ? G * C2::OUT_SZ : 0));
+    static constexpr int S = 0;
+    static constexpr int A1 = S + SFL;
     static constexpr int A2 = A1 + round4(G * C1::OUT_SZ);
     static constexpr int A3 = A2 + (Net::NCONV >= 2 ? round4(G * C2::OUT_SZ) : 0);
     static constexpr int HH = A3 + (Net::NCONV >= 3 ? round4(G * C3::OUT_SZ) : 0);
     static constexpr int Z = HH + (Net::NFULL >= 2 ? round4(G * F1::OUT) : 0);
-    static constexpr int WB = Z + G * kZStride;
+    static constexpr int BS = Z + G * kZStride;
+    static constexpr int WB = BS + kBiasScratch;
     static constexpr int FLOATS = WB + WBUF;
-    // argmax bytes
-    static constexpr int AM1 = 0;
+    static constexpr int AM1 = 0;  // argmax bytes
     static constexpr int AM2 = AM1 + (G * C1::OUT_SZ + 15) / 16 * 16;
     static constexpr int AM3 = AM2 + (Net::NCONV >= 2 ? (G * C2::OUT_SZ + 15) / 16 * 16 : 0);
     static constexpr int AMB = AM3 + (Net::NCONV >= 3 ? (G * C3::OUT_SZ + 15) / 16 * 16 : 0);
@@ -117,25 +130,24 @@ struct SLayout {
 };
 
 struct KArgs {
-    float* params;              // internal layout, shared by all workers (the CHAOS weight store)
-    float* partial;             // sync: [slot][pstride] gradient sums
+    float* params;               // internal layout, shared by all workers (the CHAOS weight store)
+    float* partial;              // sync: [slot][pstride] gradient sums
     long long pstride;
-    const float* images;        // [n][in]
-    const int* labels;          // [n]
-    long long n;                // images in this launch
-    long long first_slot_sample;// sync: sample index of slot 0 (relative to images)
-    unsigned long long* counter;// hogwild work counter (claims in units of images)
-    int* latch;                 // device error latch
-    double* loss_sum;           // training loss accumulator
+    const float* images;         // [n][in]
+    const int* labels;           // [n]
+    long long n;                 // images in this launch
+    unsigned long long* counter; // hogwild work counter (claims in units of images)
+    int* latch;                  // device error latch
+    double* loss_sum;            // training loss accumulator
     float neg_lr;
-    int* claims;                // optional per-image claim counts
-    float* out_loss;            // eval: per-image loss
-    unsigned char* out_wrong;   // eval: per-image error flag
-    float* out_logits;          // forward: [n][kClasses]
+    int* claims;                 // optional per-image claim counts
+    float* out_loss;             // eval: per-image loss
+    unsigned char* out_wrong;    // eval: per-image error flag
+    float* out_logits;           // forward: [n][kClasses]
 };
 
 // ------------------------------------------------------------------------------------
-// small PTX helpers: mbarrier + cp.async.bulk (TMA bulk copy global -> shared)
+// PTX helpers: mbarrier, TMA bulk copies global->shared, bulk reduce/copy shared->global
 // ------------------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -168,24 +180,41 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     } while (!done);
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_reduce_add(float* gdst, const float* ssrc, uint32_t bytes) {
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(gdst),
+                 "r"(smem_u32(ssrc)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(float* gdst, const float* ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_all() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void red_add(float* p, float v) {
+    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
 
-// Issue (tid 0) a bulk copy of `floats` floats; everyone waits.  Caller guarantees
-// 16-B alignment of both ends and floats % 4 == 0.
-struct Stager {
+// Async loads into shared memory tracked by one mbarrier each (tid 0 issues).
+struct Loader {
     uint64_t* bar;
     uint32_t phase;
-    __device__ __forceinline__ void begin() {
-        fence_proxy_async();  // order earlier generic accesses (smem reuse, our REDs) before the async proxy
-        __syncthreads();
-    }
-    __device__ __forceinline__ void issue(float* dst, const float* src, int floats, uint32_t extra_bytes = 0) {
+    // caller: all threads passed a barrier after their last generic access of dst
+    __device__ __forceinline__ void issue(float* dst, const float* src, int floats) const {
         if (threadIdx.x == 0) {
-            mbar_expect_tx(bar, static_cast<uint32_t>(floats) * 4u + extra_bytes);
-            int off = 0;
-            while (off < floats) {
-                const int chunk = (floats - off) > 16384 ? 16384 : (floats - off);  // 64 KiB pieces
+            mbar_expect_tx(bar, static_cast<uint32_t>(floats) * 4u);
+            for (int off = 0; off < floats; off += 16384) {
+                const int chunk = (floats - off) > 16384 ? 16384 : (floats - off);
                 bulk_g2s(dst + off, src + off, static_cast<uint32_t>(chunk) * 4u, bar);
-                off += chunk;
             }
         }
     }
@@ -193,12 +222,45 @@ struct Stager {
         mbar_wait(bar, phase);
         phase ^= 1u;
     }
-    __device__ __forceinline__ void stage(float* dst, const float* src, int floats) {
-        begin();
-        issue(dst, src, floats);
-        wait();
-    }
 };
+
+// Everyone: make generic smem writes visible to the async proxy, then barrier.
+__device__ __forceinline__ void sync_for_async() {
+    fence_async_smem();
+    __syncthreads();
+}
+// Before reusing a buffer a bulk publish is reading: tid 0 waits for the TMA reads, barrier.
+__device__ __forceinline__ void wait_publish_reads() {
+    if (threadIdx.x == 0) bulk_wait_read<0>();
+    __syncthreads();
+}
+
+// Publish `floats` floats of gradient (already scaled by -lr in hogwild mode) from shared
+// memory to global offset goff: hogwild = TMA bulk reduce-add into the shared weights;
+// sync = TMA bulk copy into this group's slot.  Call after sync_for_async(); tid 0 issues.
+template <int MODE>
+__device__ __forceinline__ void publish_bulk(const KArgs& a, int slot, int goff, const float* src, int floats) {
+    if (threadIdx.x == 0) {
+        float* dst = (MODE == kHogwild) ? a.params + goff
+                                        : a.partial + static_cast<long long>(slot) * a.pstride + goff;
+        for (int off = 0; off < floats; off += 16384) {
+            const int chunk = (floats - off) > 16384 ? 16384 : (floats - off);
+            if constexpr (MODE == kHogwild)
+                bulk_reduce_add(dst + off, src + off, static_cast<uint32_t>(chunk) * 4u);
+            else
+                bulk_s2g(dst + off, src + off, static_cast<uint32_t>(chunk) * 4u);
+        }
+        bulk_commit();
+    }
+}
+// Direct per-element publish (layers whose gradient does not fit the scratch).
+template <int MODE>
+__device__ __forceinline__ void publish_elem(const KArgs& a, int slot, int idx, float g_scaled) {
+    if constexpr (MODE == kHogwild)
+        red_add(a.params + idx, g_scaled);
+    else
+        a.partial[static_cast<long long>(slot) * a.pstride + idx] = g_scaled;
+}
 
 template <int N, bool A4>
 __device__ __forceinline__ void load_vec(float (&v)[N], const float* p) {
@@ -231,21 +293,10 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
-// Publish one gradient element: hogwild = RED.ADD of -lr*g into the shared weights
-// (no lock, arbitrary order); sync = plain store of the group sum into its slot.
-template <int MODE>
-__device__ __forceinline__ void publish(const KArgs& a, int slot, int idx, float g) {
-    if constexpr (MODE == kHogwild) {
-        atomicAdd(a.params + idx, a.neg_lr * g);
-    } else if constexpr (MODE == kSync) {
-        a.partial[static_cast<long long>(slot) * a.pstride + idx] = g;
-    }
-}
-
 // ------------------------------------------------------------------------------------
-// conv -> tanh -> max-pool forward (fused).  One thread item = MT maps x one pooled
-// window x one image; the KP*KP conv outputs of the window stay in registers, the
-// weights of the MT maps are warp-uniform vector loads from the staged block.
+// PHASE(conv_fwd) conv -> tanh -> max-pool forward (fused).  One thread item = MT maps x
+// one pooled window x one image; the KP*KP conv outputs of the window stay in registers,
+// the weights of the MT maps are warp-uniform vector loads from the staged block.
 // ------------------------------------------------------------------------------------
 template <class L, int NT>
 __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const float* __restrict__ wsm,
@@ -311,70 +362,85 @@ __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const flo
 }
 
 // ------------------------------------------------------------------------------------
-// conv backward.  dp[g][m][pp] holds dL/dz at the argmax of pooled output pp (the
-// pool routes the delta there and nowhere else).  Step 1: weight gradient
+// PHASE(conv_gw) conv weight gradient.  dp[g][m][pp] = dL/dz at the argmax of pooled
+// output pp (the pool routes the delta there and nowhere else):
 //   gW[n][i][j][m] = sum_g sum_pp dp[g][m][pp] * in[g][n][r(pp)+i][c(pp)+j],  gb[m] = sum dp
-// one thread per (m, n, tap group [, split]), published as soon as it is complete.
-// Step 2 (NEED_DIN): partial derivatives of the previous layer, gathered per input
-// element from the staged (pre-update) W snapshot and multiplied by (1 - a^2), written
-// in place over `in` (the previous pooled activations are dead after step 1).
+// One thread item = (input map n, output map m, tap group, split of the (g, pp) range),
+// n fastest so a warp's lanes gather from different maps of the same window (map stride
+// H*W is odd: conflict-free) and dp/argmax loads are broadcasts.  With SCRATCH the sums,
+// scaled by `sc` (-lr in hogwild), are assembled in shared memory in the weight store's
+// layout (splits reduced in a fixed order) and published with one bulk op; otherwise
+// each element is published directly.
 // ------------------------------------------------------------------------------------
-template <class L, int NT, int MODE, bool NEED_DIN>
-__device__ __forceinline__ void conv_bwd(const KArgs& a, int slot, float* __restrict__ in,
-                                         const float* __restrict__ dp, const uint8_t* __restrict__ am,
-                                         float* __restrict__ wsm, int woff, int boff, int cnt) {
+template <class L, int NT, int MODE, bool SCRATCH>
+__device__ __forceinline__ void conv_gw(const KArgs& a, int slot, const float* __restrict__ in,
+                                        const float* __restrict__ dp, const uint8_t* __restrict__ am,
+                                        float* __restrict__ scr, int woff, int cnt, float sc) {
     constexpr int K = L::K, KP = L::KP, KK = L::KK, PW = L::PW, P = L::P, M = L::M, C = L::C;
     constexpr int TT = L::TT, TG = KK / TT, GS = L::GS;
+    constexpr int HW = L::H * L::W;
+    static_assert(GS == 1 || SCRATCH, "split sums need the scratch");
+    float* fin = scr + (GS > 1 ? GS * L::WFL : 0);  // final [WFL][BFL] block
     const int span = cnt * P;
-    // ---- step 1: weight gradients
-    {
-        const int total = M * C * TG * GS;
-        for (int it = threadIdx.x; it < total; it += NT) {
-            const int m = it % M;
-            int r = it / M;
-            const int n = r % C;
-            r /= C;
-            const int tg = r % TG;
-            const int s = r / TG;
-            const int q0 = (GS == 1) ? 0 : (span * s) / GS;
-            const int q1 = (GS == 1) ? span : (span * (s + 1)) / GS;
-            float acc[TT];
+    const int total = C * M * TG * GS;
+    for (int it = threadIdx.x; it < total; it += NT) {
+        const int n = it % C;
+        int r = it / C;
+        const int m = r % M;
+        r /= M;
+        const int tg = r % TG;
+        const int s = r / TG;
+        const int q0 = (GS == 1) ? 0 : (span * s) / GS;
+        const int q1 = (GS == 1) ? span : (span * (s + 1)) / GS;
+        float acc[TT];
 #pragma unroll
-            for (int t = 0; t < TT; ++t) acc[t] = 0.f;
-            int g = q0 / P;
-            int pp = q0 - g * P;
-            for (int q = q0; q < q1; ++q) {
-                const int o = g * L::OUT_SZ + m * P + pp;
-                const float d = dp[o];
-                const int arg = am[o];
-                const int r0 = (pp / PW) * KP + arg / KP;
-                const int c0 = (pp % PW) * KP + arg % KP;
-                const float* base = in + g * L::IN_SZ + n * (L::H * L::W) + r0 * L::W + c0;
-#pragma unroll
-                for (int t = 0; t < TT; ++t) {
-                    const int tap = tg * TT + t;
-                    acc[t] = fmaf(d, base[(tap / K) * L::W + (tap % K)], acc[t]);
-                }
-                if (++pp == P) {
-                    pp = 0;
-                    ++g;
-                }
-            }
+        for (int t = 0; t < TT; ++t) acc[t] = 0.f;
+        float accb = 0.f;
+        int g = q0 / P;
+        int pp = q0 - g * P;
+        const float* ing = in + g * L::IN_SZ + n * HW;
+        const float* dpg = dp + g * L::OUT_SZ + m * P;
+        const uint8_t* amg = am + g * L::OUT_SZ + m * P;
+#pragma unroll 4
+        for (int q = q0; q < q1; ++q) {
+            const float d = dpg[pp];
+            const int arg = amg[pp];
+            const int pr = pp / PW, pc = pp - (pp / PW) * PW;
+            const float* base = ing + (pr * KP + arg / KP) * L::W + pc * KP + arg % KP;
 #pragma unroll
             for (int t = 0; t < TT; ++t) {
-                const int widx = (n * KK + tg * TT + t) * L::MP + m;
-                if constexpr (GS == 1)
-                    publish<MODE>(a, slot, woff + widx, acc[t]);
-                else
-                    wsm[s * L::WFL + widx] = acc[t];
+                const int tap = tg * TT + t;
+                acc[t] = fmaf(d, base[(tap / K) * L::W + (tap % K)], acc[t]);
+            }
+            accb += d;
+            if (++pp == P) {
+                pp = 0;
+                ++g;
+                ing += L::IN_SZ;
+                dpg += L::OUT_SZ;
+                amg += L::OUT_SZ;
             }
         }
-        for (int m = threadIdx.x; m < M; m += NT) {  // bias gradient
-            float gb = 0.f;
-            for (int g = 0; g < cnt; ++g)
-                for (int pp = 0; pp < P; ++pp) gb += dp[g * L::OUT_SZ + m * P + pp];
-            publish<MODE>(a, slot, boff + m, gb);
+#pragma unroll
+        for (int t = 0; t < TT; ++t) {
+            const int widx = (n * KK + tg * TT + t) * L::MP + m;
+            if constexpr (!SCRATCH)
+                publish_elem<MODE>(a, slot, woff + widx, sc * acc[t]);
+            else if constexpr (GS == 1)
+                fin[widx] = sc * acc[t];
+            else
+                scr[s * L::WFL + widx] = acc[t];
         }
+        if constexpr (GS == 1) {
+            if (n == 0 && tg == 0) {
+                if constexpr (!SCRATCH)
+                    publish_elem<MODE>(a, slot, woff + L::WFL + m, sc * accb);
+                else
+                    fin[L::WFL + m] = sc * accb;
+            }
+        }
+    }
+    if constexpr (SCRATCH) {
         if constexpr (GS > 1) {
             __syncthreads();
             for (int e = threadIdx.x; e < L::ROWS * M; e += NT) {
@@ -383,60 +449,124 @@ __device__ __forceinline__ void conv_bwd(const KArgs& a, int slot, float* __rest
                 const int widx = row * L::MP + m;
                 float s = 0.f;
 #pragma unroll
-                for (int k = 0; k < GS; ++k) s += wsm[k * L::WFL + widx];
-                publish<MODE>(a, slot, woff + widx, s);
+                for (int k = 0; k < GS; ++k) s += scr[k * L::WFL + widx];
+                fin[widx] = sc * s;
+            }
+            for (int m = threadIdx.x; m < M; m += NT) {  // bias: fixed-order sum by one thread per map
+                float s = 0.f;
+                for (int g = 0; g < cnt; ++g)
+                    for (int pp = 0; pp < P; ++pp) s += dp[g * L::OUT_SZ + m * P + pp];
+                fin[L::WFL + m] = sc * s;
             }
         }
+        if constexpr (L::MP > M) {  // padding columns of the block publish zeros
+            for (int e = threadIdx.x; e < (L::ROWS + 1) * (L::MP - M); e += NT)
+                fin[(e / (L::MP - M)) * L::MP + M + e % (L::MP - M)] = 0.f;
+        }
+        sync_for_async();
+        publish_bulk<MODE>(a, slot, woff, fin, L::BLK);
     }
-    if constexpr (NEED_DIN) {
-        static_assert(GS == 1, "delta_in needs the staged weights intact");
-        __syncthreads();
-        // ---- step 2: delta_in (gather form), in place over `in`
-        constexpr int NCG = C / L::NCH;
-        constexpr int HW = L::H * L::W;
-        const int total = cnt * HW * NCG;
-        for (int it = threadIdx.x; it < total; it += NT) {
-            const int pos = it % HW;
-            const int r = it / HW;
-            const int g = r % cnt;
-            const int ncg = r / cnt;
-            const int y = pos / L::W, x = pos - (pos / L::W) * L::W;
-            float acc[L::NCH];
+}
+
+// ------------------------------------------------------------------------------------
+// PHASE(conv_din) partial derivatives of the previous layer:
+//   dout[g][n][y][x] = (1 - in^2) * sum_m sum_pp [tap in range] W[n][y-r][x-c][m] dp[g][m][pp]
+// One warp per (image g, band of RB input rows, 32 input maps); lanes over n.  The windows
+// that reach the band are a static set relative to the band, the argmax branch is uniform
+// across the warp, and every (tap, window) pair lands in a compile-time register of the
+// band accumulator: exactly the argmax-sparse MACs, no atomics, no divergence.  W is the
+// staged (pre-update) snapshot (SURVEY C-9).  dout may alias in (in place).
+// ------------------------------------------------------------------------------------
+template <class L, int NT>
+__device__ __forceinline__ void conv_din(const float* __restrict__ wsm, const float* __restrict__ dp,
+                                         const uint8_t* __restrict__ am, const float* in, float* dout, int cnt) {
+    constexpr int K = L::K, KP = L::KP, KK = L::KK, PW = L::PW, PH = L::PH, P = L::P, M = L::M, C = L::C;
+    constexpr int HW = L::H * L::W, RB = L::RB, NB = L::NB;
+    constexpr int R2 = (NB == 1) ? 0 : RB / KP;       // window rows per band step
+    constexpr int DLO = (NB == 1) ? 0 : -((KP + K - 2) / KP);
+    constexpr int DHI = (NB == 1) ? PH - 1 : (RB - 1) / KP;
+    constexpr int NWR = DHI - DLO + 1;                // window rows that can reach a band
+    constexpr int NCW = (C + 31) / 32;
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int total = cnt * NB * NCW;
+    for (int vw = warp; vw < total; vw += NW) {
+        const int cw = vw % NCW;
+        const int t = vw / NCW;
+        const int b = t % NB;
+        const int g = t / NB;
+        const int n = cw * 32 + lane;
+        if (n >= C) continue;
+        float acc[RB][L::W];
 #pragma unroll
-            for (int c = 0; c < L::NCH; ++c) acc[c] = 0.f;
-            const int ylo = y - (K - 1) - (KP - 1), xlo = x - (K - 1) - (KP - 1);
-            const int pr0 = ylo <= 0 ? 0 : (ylo + KP - 1) / KP;
-            const int pc0 = xlo <= 0 ? 0 : (xlo + KP - 1) / KP;
-            const int pr1 = min(L::PH - 1, y / KP), pc1 = min(L::PW - 1, x / KP);
-            const float* wrow0 = wsm + (ncg * L::NCH) * KK * L::MP;
-            for (int m = 0; m < M; ++m) {
-                for (int pr = pr0; pr <= pr1; ++pr)
-                    for (int pc = pc0; pc <= pc1; ++pc) {
-                        const int o = g * L::OUT_SZ + m * P + pr * PW + pc;
-                        const int arg = am[o];
-                        const int i = y - (pr * KP + arg / KP);
-                        const int j = x - (pc * KP + arg % KP);
-                        if (i >= 0 && i < K && j >= 0 && j < K) {
-                            const float d = dp[o];
-                            const float* wr = wrow0 + (i * K + j) * L::MP + m;
+        for (int r = 0; r < RB; ++r)
 #pragma unroll
-                            for (int c = 0; c < L::NCH; ++c) acc[c] = fmaf(wr[c * KK * L::MP], d, acc[c]);
-                        }
-                    }
+            for (int c = 0; c < L::W; ++c) acc[r][c] = 0.f;
+        const float* wn = wsm + n * KK * L::MP;
+        const float* dpg = dp + g * L::OUT_SZ;
+        const uint8_t* amg = am + g * L::OUT_SZ;
+        const int pr0 = b * R2;
+#pragma unroll 1
+        for (int m = 0; m < M; ++m) {
+            float w[KK];
+#pragma unroll
+            for (int tp = 0; tp < KK; ++tp) w[tp] = wn[tp * L::MP + m];
+            float dv[NWR][PW];
+            int av[NWR][PW];
+#pragma unroll
+            for (int dr = 0; dr < NWR; ++dr) {
+                const int pr = pr0 + DLO + dr;
+                const bool ok = pr >= 0 && pr < PH;
+#pragma unroll
+                for (int pc = 0; pc < PW; ++pc) {
+                    const int o = m * P + (ok ? pr : 0) * PW + pc;
+                    dv[dr][pc] = ok ? dpg[o] : 0.f;
+                    av[dr][pc] = ok ? static_cast<int>(amg[o]) : -1;
+                }
             }
 #pragma unroll
-            for (int c = 0; c < L::NCH; ++c) {
-                float* pa = in + g * L::IN_SZ + (ncg * L::NCH + c) * HW + pos;
-                const float v = *pa;
-                *pa = acc[c] * (1.f - v * v);
+            for (int dr = 0; dr < NWR; ++dr) {
+                const int dlt = DLO + dr;
+#pragma unroll
+                for (int pc = 0; pc < PW; ++pc) {
+                    const int arg = av[dr][pc];
+                    const float d = dv[dr][pc];
+#pragma unroll
+                    for (int ph = 0; ph < KP * KP; ++ph) {
+                        if (arg == ph) {  // warp-uniform branch on the argmax phase
+#pragma unroll
+                            for (int i = 0; i < K; ++i) {
+                                const int rr = dlt * KP + ph / KP + i;
+                                if (rr < 0 || rr >= RB) continue;  // compile-time after unrolling
+#pragma unroll
+                                for (int j = 0; j < K; ++j) {
+                                    const int cc = pc * KP + ph % KP + j;
+                                    acc[rr][cc] = fmaf(w[i * K + j], d, acc[rr][cc]);
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        const float* ib = in + g * L::IN_SZ + n * HW + b * RB * L::W;
+        float* ob = dout + g * L::IN_SZ + n * HW + b * RB * L::W;
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+            if (b * RB + r < L::H) {
+#pragma unroll
+                for (int c = 0; c < L::W; ++c) {
+                    const float v = ib[r * L::W + c];
+                    ob[r * L::W + c] = acc[r][c] * (1.f - v * v);
+                }
             }
         }
     }
 }
 
 // ------------------------------------------------------------------------------------
-// fully connected forward: one warp per output row, lanes over inputs, weights
-// streamed from L2 (__ldcg: on-demand reads of the shared store, no stale L1 copy).
+// PHASE(fc_fwd) fully connected forward: one warp per output row, lanes over inputs,
+// weights streamed from L2 (__ldcg: on-demand reads of the shared store, no stale L1 copy).
 // ------------------------------------------------------------------------------------
 template <class F, int G, int NT>
 __device__ __forceinline__ void fc_fwd(const float* __restrict__ Wg, const float* __restrict__ bg,
@@ -464,50 +594,96 @@ __device__ __forceinline__ void fc_fwd(const float* __restrict__ Wg, const float
     }
 }
 
-// fully connected backward: one thread per input column i, loop over outputs o.
-// Reads W[o][i] (pre-update, on demand) for delta_in, forms gW[o][i] = sum_g dz[g][o] a[g][i]
-// and publishes it; delta_in * (1 - a^2) is written in place over the input activations.
-template <class F, int G, int NT, int MODE, bool NEED_DIN>
+// ------------------------------------------------------------------------------------
+// PHASE(fc_bwd) fully connected backward: one thread per input column i, outputs o in
+// chunks.  Reads W[o][i] (pre-update, on demand) for delta_in; gW[o][i] = sum_g dz[g][o] a[g][i]
+// goes (scaled) into a shared-memory chunk that is published with one bulk op while the
+// next chunk is computed into the other half of S; delta_in * (1 - a^2) is written in
+// place over the input activations.  Bias gradients go through `bsc`.
+// ------------------------------------------------------------------------------------
+template <class F, int G, int NT, int MODE, int SHALF>
 __device__ __forceinline__ void fc_bwd(const KArgs& a, int slot, int woff, int boff, float* __restrict__ in,
-                                       const float* __restrict__ dz, int dstride, int cnt) {
+                                       const float* __restrict__ dz, int dstride, float* __restrict__ S,
+                                       float* __restrict__ bsc, int cnt, float sc) {
+    constexpr int RPC0 = SHALF / F::IN;  // rows per chunk
+    constexpr int RPC = (RPC0 >= F::OUT) ? F::OUT : ((RPC0 * F::IN) % 4 == 0 ? RPC0 : RPC0 / 4 * 4);
+    static_assert(RPC >= 1, "S half must hold a weight row");
+    static_assert(RPC == F::OUT || (RPC * F::IN) % 4 == 0, "chunk starts must stay 16-B aligned");
+    constexpr int NCH = (F::OUT + RPC - 1) / RPC;
+    static_assert(F::WFL - (NCH - 1) * RPC * F::IN <= SHALF, "last chunk must fit");
     const float* Wg = a.params + woff;
-    for (int i = threadIdx.x; i < F::IN; i += NT) {
-        float av[G], din[G];
+    constexpr int NI = (F::IN + NT - 1) / NT;  // columns per thread
+    float av[NI][G], din[NI][G];
+#pragma unroll
+    for (int k = 0; k < NI; ++k)
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-            av[g] = (g < cnt) ? in[g * F::IN + i] : 0.f;
-            din[g] = 0.f;
+            const int col = threadIdx.x + k * NT;
+            av[k][g] = (g < cnt && col < F::IN) ? in[g * F::IN + col] : 0.f;
+            din[k][g] = 0.f;
         }
-#pragma unroll 2
-        for (int o = 0; o < F::OUT; ++o) {
-            float w = 0.f;
-            if constexpr (NEED_DIN) w = __ldcg(Wg + static_cast<long long>(o) * F::IN + i);
-            float gw = 0.f;
+    for (int c = 0; c < NCH; ++c) {
+        const int o0 = c * RPC;
+        const int o1 = (o0 + RPC < F::OUT) ? o0 + RPC : F::OUT;
+        float* buf = S + (c & 1) * SHALF;
+        if (c >= 2) {  // the bulk publish of chunk c-2 must have read this half
+            if (threadIdx.x == 0) bulk_wait_read<1>();
+            __syncthreads();
+        }
 #pragma unroll
-            for (int g = 0; g < G; ++g) {
-                if (g < cnt) {
-                    const float d = dz[g * dstride + o];
-                    din[g] = fmaf(w, d, din[g]);
-                    gw = fmaf(d, av[g], gw);
+        for (int k = 0; k < NI; ++k) {
+            const int col = threadIdx.x + k * NT;
+            if (col < F::IN) {
+                for (int o = o0; o < o1; o += 4) {
+                    float w[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        w[q] = (o + q < o1) ? __ldcg(Wg + static_cast<long long>(o + q) * F::IN + col) : 0.f;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        if (o + q < o1) {
+                            float gw = 0.f;
+#pragma unroll
+                            for (int g = 0; g < G; ++g) {
+                                if (g < cnt) {
+                                    const float d = dz[g * dstride + o + q];
+                                    din[k][g] = fmaf(w[q], d, din[k][g]);
+                                    gw = fmaf(d, av[k][g], gw);
+                                }
+                            }
+                            buf[(o + q - o0) * F::IN + col] = sc * gw;
+                        }
+                    }
                 }
             }
-            publish<MODE>(a, slot, woff + o * F::IN + i, gw);
         }
-        if constexpr (NEED_DIN) {
+        const int fl = (o1 == F::OUT) ? F::WFL - o0 * F::IN : (o1 - o0) * F::IN;
+        if (o1 == F::OUT)
+            for (int e = (o1 - o0) * F::IN + threadIdx.x; e < fl; e += NT) buf[e] = 0.f;  // block padding
+        sync_for_async();
+        publish_bulk<MODE>(a, slot, woff + o0 * F::IN, buf, fl);
+    }
+    for (int o = threadIdx.x; o < F::BFL; o += NT) {  // bias
+        float gb = 0.f;
+        if (o < F::OUT)
+            for (int g = 0; g < cnt; ++g) gb += dz[g * dstride + o];
+        bsc[o] = sc * gb;
+    }
+    sync_for_async();
+    publish_bulk<MODE>(a, slot, boff, bsc, F::BFL);
+    // delta_in, in place (each thread owns its columns)
+#pragma unroll
+    for (int k = 0; k < NI; ++k) {
+        const int col = threadIdx.x + k * NT;
+        if (col < F::IN)
 #pragma unroll
             for (int g = 0; g < G; ++g)
-                if (g < cnt) in[g * F::IN + i] = din[g] * (1.f - av[g] * av[g]);
-        }
-    }
-    for (int o = threadIdx.x; o < F::OUT; o += NT) {
-        float gb = 0.f;
-        for (int g = 0; g < cnt; ++g) gb += dz[g * dstride + o];
-        publish<MODE>(a, slot, boff + o, gb);
+                if (g < cnt) in[g * F::IN + col] = din[k][g] * (1.f - av[k][g] * av[k][g]);
     }
 }
 
 // ------------------------------------------------------------------------------------
-// The worker kernel: hogwild training, sync-batch gradients, evaluation, forward.
+// PHASE(worker) The worker kernel: hogwild training, sync-batch gradients, evaluation, forward.
 // ------------------------------------------------------------------------------------
 template <class Net, int G, int NT, int MODE>
 __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
@@ -520,32 +696,46 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
     using S = SLayout<Net, G>;
     constexpr int NCONV = Net::NCONV, NFULL = Net::NFULL;
     constexpr int IMG = C1::IN_SZ;
+    constexpr int SHALF = S::SFL / 2 / 4 * 4;
+    constexpr bool TRAIN = (MODE == kHogwild || MODE == kSync);
+    // weight-buffer placement: W1 at 0, W2 at the tail (prefetched during conv1), W3 in two
+    // halves (first half prefetched during conv2 into [0, W3A), second after conv2)
+    constexpr int W2OFF = (NCONV >= 2) ? S::WBUF - C2::BLK : 0;
+    constexpr int W3A = (NCONV >= 3) ? (C3::C / 2) * C3::KK * C3::MP : 0;
+    static_assert(NCONV < 3 || W3A <= W2OFF, "W3 first half must not overlap W2");
+    static_assert(NCONV < 2 || C1::BLK <= W2OFF, "W1 and W2 must not overlap");
 
     extern __shared__ __align__(128) unsigned char smem[];
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-    int* s_base = reinterpret_cast<int*>(smem + 8);
-    int* s_lab = reinterpret_cast<int*>(smem + 16);  // G labels
-    float* s_loss = reinterpret_cast<float*>(smem + 16 + 4 * 16);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // 4 mbarriers
+    int* s_base = reinterpret_cast<int*>(smem + 32);
+    int* s_lab = reinterpret_cast<int*>(smem + 48);                // G labels (<= 16)
+    float* s_loss = reinterpret_cast<float*>(smem + 48 + 4 * 16);  // G losses
     float* fa = reinterpret_cast<float*>(smem + kHdrBytes);
-    float* xs = fa + S::X;
+    float* sS = fa + S::S;
     float* a1 = fa + S::A1;
     float* a2 = fa + S::A2;
     float* a3 = fa + S::A3;
     float* hh = fa + S::HH;
     float* zz = fa + S::Z;
+    float* bsc = fa + S::BS;
     float* wb = fa + S::WB;
     uint8_t* amb = smem + kHdrBytes + S::FLOATS * 4;
     uint8_t* am1 = amb + S::AM1;
     uint8_t* am2 = amb + S::AM2;
     uint8_t* am3 = amb + S::AM3;
     const float* P = a.params;
+    const float sc = (MODE == kHogwild) ? a.neg_lr : 1.f;
+    (void)a2;
+    (void)a3;
+    (void)am2;
+    (void)am3;
 
     if (threadIdx.x == 0) {
-        mbar_init(bar, 1);
+        for (int k = 0; k < 4; ++k) mbar_init(bars + k, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    Stager st{bar, 0u};
+    Loader L0{bars + 0, 0u}, L1{bars + 1, 0u}, L2{bars + 2, 0u}, L3{bars + 3, 0u};
 
     long long iter = 0;
     for (;;) {
@@ -558,6 +748,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 base = (static_cast<long long>(blockIdx.x) + iter * gridDim.x) * G;
             *s_base = base < a.n ? static_cast<int>(base) : -1;
         }
+        fence_proxy_async();  // earlier generic smem / global accesses precede the async proxy
         __syncthreads();
         const int base = *s_base;
         if (base < 0) break;
@@ -577,39 +768,41 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             if constexpr (MODE == kHogwild)
                 if (a.claims) atomicAdd(a.claims + base + threadIdx.x, 1);
         }
-        // stage conv1 weights (+ the images when the group is 16-B aligned) with one bulk copy
+        // stage images (bulk when 16-B aligned) + W1 on bar0, prefetch W2 on bar1
         const float* xsrc = a.images + static_cast<long long>(base) * IMG;
         const bool x_bulk = ((reinterpret_cast<uintptr_t>(xsrc) & 15u) == 0) && ((cnt * IMG) % 4 == 0);
-        st.begin();
-        if (x_bulk) {
-            if (threadIdx.x == 0) {
-                mbar_expect_tx(bar, static_cast<uint32_t>(C1::WFL + C1::BFL + cnt * IMG) * 4u);
-                bulk_g2s(wb, P + O::c1w, static_cast<uint32_t>(C1::WFL + C1::BFL) * 4u, bar);
-                int off = 0;
-                const int tot = cnt * IMG;
-                while (off < tot) {
-                    const int chunk = (tot - off) > 16384 ? 16384 : (tot - off);
-                    bulk_g2s(xs + off, xsrc + off, static_cast<uint32_t>(chunk) * 4u, bar);
-                    off += chunk;
+        if (threadIdx.x == 0) {
+            mbar_expect_tx(bars + 0, static_cast<uint32_t>(C1::BLK + (x_bulk ? cnt * IMG : 0)) * 4u);
+            bulk_g2s(wb, P + O::c1w, static_cast<uint32_t>(C1::BLK) * 4u, bars + 0);
+            if (x_bulk)
+                for (int off = 0; off < cnt * IMG; off += 16384) {
+                    const int chunk = (cnt * IMG - off) > 16384 ? 16384 : (cnt * IMG - off);
+                    bulk_g2s(sS + off, xsrc + off, static_cast<uint32_t>(chunk) * 4u, bars + 0);
                 }
-            }
-        } else {
-            for (int i = threadIdx.x; i < cnt * IMG; i += NT) xs[i] = __ldg(xsrc + i);
-            st.issue(wb, P + O::c1w, C1::WFL + C1::BFL);
         }
-        st.wait();
-        if (!x_bulk) __syncthreads();  // the plain image stores of other threads
+        if constexpr (NCONV >= 2) L1.issue(wb + W2OFF, P + O::c2w, C2::BLK);
+        if (!x_bulk)
+            for (int i = threadIdx.x; i < cnt * IMG; i += NT) sS[i] = __ldg(xsrc + i);
+        L0.wait();
+        if (!x_bulk) __syncthreads();
 
         // ---------------- a2: conv -> tanh -> pool, layer by layer
-        conv_fwd<C1, NT>(xs, wb, a1, am1, cnt);
+        conv_fwd<C1, NT>(sS, wb, a1, am1, cnt);
         float* alast = a1;
         if constexpr (NCONV >= 2) {
-            st.stage(wb, P + O::c2w, C2::WFL + C2::BFL);
-            conv_fwd<C2, NT>(a1, wb, a2, am2, cnt);
+            fence_proxy_async();
+            __syncthreads();
+            if constexpr (NCONV >= 3) L2.issue(wb, P + O::c3w, W3A);  // W1 region is dead: W3's first half
+            L1.wait();
+            conv_fwd<C2, NT>(a1, wb + W2OFF, a2, am2, cnt);
             alast = a2;
         }
         if constexpr (NCONV >= 3) {
-            st.stage(wb, P + O::c3w, C3::WFL + C3::BFL);
+            fence_proxy_async();
+            __syncthreads();
+            L3.issue(wb + W3A, P + O::c3w + W3A, C3::BLK - W3A);
+            L2.wait();
+            L3.wait();
             conv_fwd<C3, NT>(a2, wb, a3, am3, cnt);
             alast = a3;
         }
@@ -653,36 +846,59 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 }
             }
         }
-        if constexpr (MODE == kHogwild || MODE == kSync) {
+        if constexpr (TRAIN) {
             __syncthreads();
             if (threadIdx.x == 0 && a.loss_sum) {
                 double ls = 0.0;
                 for (int g = 0; g < cnt; ++g) ls += s_loss[g];
                 atomicAdd(a.loss_sum, ls);
             }
-            // ---------------- a5: full layers backward (publish per layer)
+            // ---------------- a5: full layers backward, one bulk publish per chunk / layer
             if constexpr (NFULL == 2) {
-                fc_bwd<F2, G, NT, MODE, true>(a, slot, O::f2w, O::f2b, hh, zz, kZStride, cnt);
-                __syncthreads();
-                fc_bwd<F1, G, NT, MODE, true>(a, slot, O::f1w, O::f1b, alast, hh, F1::OUT, cnt);
+                fc_bwd<F2, G, NT, MODE, SHALF>(a, slot, O::f2w, O::f2b, hh, zz, kZStride, sS, bsc, cnt, sc);
+                wait_publish_reads();
+                fc_bwd<F1, G, NT, MODE, SHALF>(a, slot, O::f1w, O::f1b, alast, hh, F1::OUT, sS, bsc, cnt, sc);
             } else {
-                fc_bwd<F1, G, NT, MODE, true>(a, slot, O::f1w, O::f1b, alast, zz, kZStride, cnt);
+                fc_bwd<F1, G, NT, MODE, SHALF>(a, slot, O::f1w, O::f1b, alast, zz, kZStride, sS, bsc, cnt, sc);
             }
+            wait_publish_reads();
             // ---------------- a6/a7: pool + conv backward, publish per layer
-            if constexpr (NCONV >= 3) {
-                st.stage(wb, P + O::c3w, C3::WFL + C3::BFL);
-                conv_bwd<C3, NT, MODE, true>(a, slot, a2, a3, am3, wb, O::c3w, O::c3b, cnt);
+            if constexpr (NCONV == 3) {
+                // W3 is still staged from the forward pass (the exact snapshot it used)
+                conv_din<C3, NT>(wb, a3, am3, a2, sS, cnt);  // delta for the pool2 outputs -> S
+                __syncthreads();
+                conv_gw<C3, NT, MODE, true>(a, slot, a2, a3, am3, wb, O::c3w, cnt, sc);
+                fence_proxy_async();
+                wait_publish_reads();
+                L1.issue(wb, P + O::c2w, C2::BLK);  // W2 again (pre-update snapshot for delta_in)
+                L1.wait();
+                conv_gw<C2, NT, MODE, true>(a, slot, a1, sS, am2, wb + C2::BLK, O::c2w, cnt, sc);
+                __syncthreads();
+                conv_din<C2, NT>(wb, sS, am2, a1, a1, cnt);
+                __syncthreads();
+            } else if constexpr (NCONV == 2) {
+                // W2 is still staged from the forward pass at W2OFF
+                conv_gw<C2, NT, MODE, false>(a, slot, a1, a2, am2, nullptr, O::c2w, cnt, sc);
+                __syncthreads();
+                conv_din<C2, NT>(wb + W2OFF, a2, am2, a1, a1, cnt);
+                __syncthreads();
             }
-            if constexpr (NCONV >= 2) {
-                st.stage(wb, P + O::c2w, C2::WFL + C2::BFL);
-                conv_bwd<C2, NT, MODE, true>(a, slot, a1, a2, am2, wb, O::c2w, O::c2b, cnt);
+            // conv1: the images again (S was reused as scratch), then its gradient
+            fence_proxy_async();
+            wait_publish_reads();
+            if (x_bulk) {
+                L0.issue(sS, xsrc, cnt * IMG);
+                L0.wait();
+            } else {
+                for (int i = threadIdx.x; i < cnt * IMG; i += NT) sS[i] = __ldg(xsrc + i);
+                __syncthreads();
             }
-            __syncthreads();
-            conv_bwd<C1, NT, MODE, false>(a, slot, xs, a1, am1, wb, O::c1w, O::c1b, cnt);
-            if constexpr (MODE == kHogwild) __threadfence();
+            conv_gw<C1, NT, MODE, true>(a, slot, sS, a1, am1, wb, O::c1w, cnt, sc);
+            if (threadIdx.x == 0) bulk_wait_all<0>();  // publishes complete before the next claim
         }
         __syncthreads();
     }
+    if (threadIdx.x == 0) bulk_wait_all<0>();
 }
 
 // w[j] -= lr * sum_{s < nslots} partial[s][j]  (fixed order: the sync-mode update)

@@ -23,26 +23,26 @@ using namespace chaos;
 namespace {
 
 struct TinyNet {  // configs[0], configs[1]: conv5 4x4 -> tanh -> pool2 -> FC 845->10
-    static constexpr int NCONV = 1, NFULL = 1, GDEF = 8, NT = 256;
-    using C1 = Conv<1, 29, 29, 5, 4, 2, /*MT*/ 5, /*TT*/ 1, /*GS*/ 4, /*NCH*/ 1>;
+    static constexpr int NCONV = 1, NFULL = 1, GDEF = 4, NT = 256, SFL = 2 * 8456;
+    using C1 = Conv<1, 29, 29, 5, 4, 2, /*MT*/ 5, /*TT*/ 16, /*GS*/ 32, /*RB*/ 2>;
     using C2 = C1;
     using C3 = C1;
     using F1 = Full<845, 10, false>;
     using F2 = F1;
 };
 struct MediumNet {  // configs[2] = Table I medium
-    static constexpr int NCONV = 2, NFULL = 2, GDEF = 4, NT = 512;
-    using C1 = Conv<1, 29, 29, 20, 4, 2, 10, 1, 1, 1>;
-    using C2 = Conv<20, 13, 13, 40, 5, 3, 4, 25, 1, 10>;
+    static constexpr int NCONV = 2, NFULL = 2, GDEF = 4, NT = 512, SFL = 6000;
+    using C1 = Conv<1, 29, 29, 20, 4, 2, 10, 16, 16, 2>;
+    using C2 = Conv<20, 13, 13, 40, 5, 3, 4, 25, 1, 3>;
     using C3 = C2;
     using F1 = Full<360, 150, true>;
     using F2 = Full<150, 10, false>;
 };
 struct LargeNet {  // configs[3], configs[4]
-    static constexpr int NCONV = 3, NFULL = 2, GDEF = 4, NT = 512;
-    using C1 = Conv<1, 29, 29, 20, 4, 2, 10, 1, 1, 1>;
-    using C2 = Conv<20, 13, 13, 60, 3, 2, 12, 9, 1, 10>;
-    using C3 = Conv<60, 5, 5, 100, 2, 2, 4, 4, 1, 10>;
+    static constexpr int NCONV = 3, NFULL = 2, GDEF = 4, NT = 512, SFL = 6000;
+    using C1 = Conv<1, 29, 29, 20, 4, 2, 10, 16, 16, 2>;
+    using C2 = Conv<20, 13, 13, 60, 3, 2, 12, 9, 1, 4>;
+    using C3 = Conv<60, 5, 5, 100, 2, 2, 4, 4, 1, 5>;
     using F1 = Full<400, 150, true>;
     using F2 = Full<150, 10, false>;
 };
