@@ -262,7 +262,8 @@ def main():
     tp = os.path.join(ROOT, "profiles", "latest_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(args.arch)
+            t = json.load(open(tp)).get(args.arch)
+            traffic = t["dram_bytes_per_launch"] if t else None
         except Exception:
             traffic = None
     line = {

@@ -42,7 +42,18 @@ def run(name):
     rec = {"run": name, "workload": wname, "arch": w.arch, "mode": mode, "batch": batch, "epochs": epochs,
            "data_sha256": d.sha256(), "lr0": w.lr0, "per_epoch": []}
     t0 = time.time()
-    for e in range(epochs):
+    ckpt = os.path.join(OUT, name + "_ckpt.npy")
+    start = 0
+    prev = os.path.join(OUT, name + ".json")
+    if os.path.exists(ckpt) and os.path.exists(prev):
+        old = json.load(open(prev))
+        if old.get("data_sha256") == rec["data_sha256"] and old["per_epoch"]:
+            # resume after the last completed epoch (the checkpoint holds its parameters)
+            rec["per_epoch"] = old["per_epoch"]
+            start = len(old["per_epoch"])
+            p = np.load(ckpt)
+            t0 -= old["per_epoch"][-1]["elapsed_s"]
+    for e in range(start, epochs):
         lr = w.lr0 * 0.9 ** e
         if mode == "seq":
             p, sl = o.train_sgd(p, d.x_train, d.y_train, lr)
@@ -56,6 +67,8 @@ def run(name):
         os.makedirs(OUT, exist_ok=True)
         with open(os.path.join(OUT, name + ".json"), "w") as f:
             json.dump(rec, f, indent=1)
+        if epochs > 1:
+            np.save(ckpt, p)
     if epochs == 1 or name.startswith("config0"):
         np.save(os.path.join(OUT, name + "_params.npy"), p)
 

@@ -1,0 +1,136 @@
+"""Multi-GPU host logic on CPU: world_size-2 ``gloo`` process groups.
+
+The product path averages the replicas' weights with NCCL every K local images
+(BASELINE.json configs[3..4]; reading R11: average weights).  Here the
+same ``DistTrainer`` runs over gloo with a CPU stand-in for ``chaos.Net`` that has
+the two methods the trainer uses, so sharding, interval boundaries, the number of
+collectives and the averaging semantics are checked without a GPU.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1506_09067_b200.dist import DistTrainer, intervals, n_averages, shard_range
+
+
+def test_shard_range_partitions_and_aligns():
+    for n in (0, 4, 60000, 480000, 1001):
+        for world in (1, 2, 3, 4, 8):
+            edges = [shard_range(n, r, world) for r in range(world)]
+            assert edges[0][0] == 0 and edges[-1][1] == n
+            for (a, b), (c, d) in zip(edges, edges[1:]):
+                assert b == c and a <= b
+            for a, _ in edges:
+                assert a % 4 == 0  # 16-B aligned image groups for the bulk copies
+
+
+def test_intervals_and_average_counts():
+    assert intervals(0, 10, 4) == [(0, 4), (4, 8), (8, 10)]
+    assert intervals(5, 5, 4) == []
+    assert intervals(0, 10, 0) == [(0, 10)]
+    # averages per epoch
+    assert n_averages(30000, 1024) == 30
+    assert n_averages(15000, 1024) == 15
+    assert n_averages(7500, 1024) == 8
+    assert n_averages(60000, 256) == 235
+    assert n_averages(60000, 1024) == 59
+    assert n_averages(60000, 8192) == 8
+
+
+class FakeNet:
+    """CPU stand-in for chaos.Net: 'training' adds lr * (rank+1) * sum(images) to every weight."""
+
+    def __init__(self, n, rank):
+        self.w = torch.arange(n, dtype=torch.float32)
+        self.rank = rank
+        self.calls = []
+
+    def device_params(self):
+        return self.w
+
+    def train_epoch(self, images, labels, lr):
+        self.calls.append(int(labels.shape[0]))
+        self.w += lr * (self.rank + 1) * float(images.sum())
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, k, lr, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = 1000
+        lo, hi = shard_range(n, rank, world)
+        X = torch.ones(n, 3)
+        Y = torch.zeros(n, dtype=torch.int32)
+        net = FakeNet(16, rank)
+        w0 = net.w.clone()
+        tr = DistTrainer(net, rank, world, k)
+        tr.epoch(X[lo:hi], Y[lo:hi], lr)
+        gathered = [torch.zeros_like(net.w) for _ in range(world)]
+        dist.all_gather(gathered, net.w)
+        q.put((rank, net.calls, tr.n_collectives, w0.numpy(), net.w.numpy(), [g.numpy() for g in gathered]))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, k, lr):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, k, lr, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return sorted(out, key=lambda t: t[0])
+
+
+def test_gloo_world2_average_every_k():
+    world, k, lr = 2, 128, 0.01
+    out = _run(world, k, lr)
+    for rank, calls, ncoll, w0, w, gathered in out:
+        lo, hi = shard_range(1000, rank, world)
+        assert sum(calls) == hi - lo
+        assert all(c <= k for c in calls)
+        assert ncoll == n_averages(hi - lo, k)
+        # after the final average every rank holds bitwise-identical parameters
+        for g in gathered:
+            np.testing.assert_array_equal(g, gathered[0])
+    # averaged model = mean of the replicas: each interval of c images (all-ones rows of
+    # 3 features) moves rank r by lr*(r+1)*3c, then the average takes the mean over ranks
+    w0 = out[0][3]
+    expect = w0.astype(np.float64).copy()
+    ncalls = [out[r][1] for r in range(world)]
+    for i in range(max(len(c) for c in ncalls)):
+        delta = np.mean([lr * (r + 1) * 3 * (ncalls[r][i] if i < len(ncalls[r]) else 0) for r in range(world)])
+        expect += delta
+    np.testing.assert_allclose(out[0][4], expect, rtol=1e-5)
+
+
+def test_gloo_world2_lr0_leaves_params_unchanged():
+    out = _run(2, 256, 0.0)
+    for _, _, _, w0, w, _ in out:
+        np.testing.assert_array_equal(w, w0)
+
+
+def test_single_process_skips_collective():
+    net = FakeNet(4, 0)
+    tr = DistTrainer(net, 0, 1, 8)
+    tr.epoch(torch.ones(20, 3), torch.zeros(20, dtype=torch.int32), 0.1)
+    assert tr.n_collectives == 0
+    assert net.calls == [20]  # one launch over the whole shard
