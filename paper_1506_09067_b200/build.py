@@ -7,20 +7,25 @@ ROOT = os.path.dirname(HERE)
 SRC = [os.path.join(HERE, "csrc", "chaos_runtime.cu")]
 DEPS = SRC + [os.path.join(HERE, "csrc", "chaos_kernels.cuh"), os.path.join(ROOT, "include", "chaos.h")]
 OUT = os.path.join(HERE, "libchaos.so")
+# instrumented variant (per-phase clock64 timing, chaos_debug_phase_times); profiling only
+OUT_TIMING = os.path.join(HERE, "libchaos_timing.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "550"]
 
 
-def build(force=False, verbose=False):
-    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= max(os.path.getmtime(p) for p in DEPS):
-        return OUT
-    cmd = ["nvcc", *NVCC_FLAGS, "-I" + os.path.join(ROOT, "include"), "-o", OUT, *SRC]
+def build(force=False, verbose=False, timing=False):
+    out = OUT_TIMING if timing else OUT
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(p) for p in DEPS):
+        return out
+    cmd = ["nvcc", *NVCC_FLAGS, "-I" + os.path.join(ROOT, "include"), "-o", out, *SRC]
+    if timing:
+        cmd.insert(1, "-DCHAOS_TIMING")
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
     import sys
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv, timing="--timing" in sys.argv)

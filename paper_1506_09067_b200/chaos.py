@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libchaos.so")
+# CHAOS_LIB selects the instrumented build (libchaos_timing.so) for profiling scripts
+LIB_PATH = os.environ.get("CHAOS_LIB") or os.path.join(HERE, "libchaos.so")
 
 CHAOS_CONV, CHAOS_MAXPOOL, CHAOS_FULL = 1, 2, 3
 CHAOS_TANH, CHAOS_IDENTITY = 0, 1
@@ -27,7 +28,7 @@ EXPORTS = ["chaos_net_create", "chaos_net_destroy", "chaos_net_set_option", "cha
            "chaos_net_num_params", "chaos_net_get_params", "chaos_net_set_params", "chaos_net_device_params",
            "chaos_net_device_params_len", "chaos_train_epoch", "chaos_train_epoch_host", "chaos_last_train_loss",
            "chaos_evaluate", "chaos_forward", "chaos_compute_gradients", "chaos_debug_claims", "chaos_net_sync",
-           "chaos_net_launch_info", "chaos_last_error", "chaos_last_status"]
+           "chaos_net_launch_info", "chaos_last_error", "chaos_last_status", "chaos_debug_phase_times"]
 
 
 class ChaosError(RuntimeError):
@@ -77,8 +78,11 @@ def lib():
             "chaos_net_launch_info": ([vp, ip, ip, ip, ip], C.c_int),
             "chaos_last_error": ([], C.c_char_p),
             "chaos_last_status": ([], C.c_int),
+            "chaos_debug_phase_times": ([vp, C.POINTER(C.c_uint64), C.c_int32], C.c_int),
         }
         for name, (args, res) in sig.items():
+            if name == "chaos_debug_phase_times" and os.environ.get("CHAOS_LIB") and not hasattr(L, name):
+                continue  # an older library picked for an A/B experiment
             f = getattr(L, name)
             f.argtypes = args
             f.restype = res
@@ -233,6 +237,15 @@ class Net:
         out = np.zeros(n, np.int32)
         _check(lib().chaos_debug_claims(self._h, out.ctypes.data_as(C.POINTER(C.c_int32)), n))
         return out
+
+    PHASES = ["claim", "stage", "conv1_fwd", "conv2_fwd", "conv3_fwd", "fc_fwd", "loss", "fc2_bwd", "fc1_bwd",
+              "conv3_din", "conv3_gw", "w2_load", "conv2_gw", "conv2_din", "img_reload", "conv1_gw"]
+
+    def phase_times(self):
+        """Per-phase clock64 cycles of the last hogwild epoch, summed over CTAs (timing build only)."""
+        out = (C.c_uint64 * 16)()
+        _check(lib().chaos_debug_phase_times(self._h, out, 16))
+        return dict(zip(self.PHASES, [int(x) for x in out]))
 
     def sync(self):
         _check(lib().chaos_net_sync(self._h))

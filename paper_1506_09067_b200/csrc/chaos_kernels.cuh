@@ -47,7 +47,8 @@ __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 // Convolution block: conv (valid, stride 1, C->M maps, KxK) -> tanh -> KPxKP max-pool (floor).
 // Tuning knobs: MT maps per thread in the forward; TT taps per thread and GS split of the
 // (image, window) sum in the weight gradient; RB input rows per band in delta_in.
-template <int C_, int H_, int W_, int M_, int K_, int KP_, int MT_, int TT_, int GS_, int RB_>
+template <int C_, int H_, int W_, int M_, int K_, int KP_, int MT_, int TT_, int GS_, int RB_, int PB_ = 0,
+          int NN_ = 0, int MS_ = 0>
 struct Conv {
     static constexpr int C = C_, H = H_, W = W_, M = M_, K = K_, KP = KP_;
     static constexpr int OH = H - K + 1, OW = W - K + 1;
@@ -59,6 +60,16 @@ struct Conv {
     static constexpr int IN_SZ = C * H * W, OUT_SZ = M * P;
     static constexpr int MT = MT_, TT = TT_, GS = GS_, RB = RB_;
     static constexpr int NB = (H + RB - 1) / RB;
+    // delta_in by window-row bands (conv_din2) when PB > 0: PB window rows per band
+    static constexpr int PB = PB_;
+    static constexpr int HR = PH * KP + K - 1, WR = PW * KP + K - 1;  // input rows/cols that receive delta
+    static constexpr int NBAND = PB > 0 ? (PH + PB - 1) / PB : 0;
+    static constexpr int BR = PB * KP + K - 1;                        // input rows per band
+    static constexpr int HAND = NBAND > 1 ? (NBAND - 1) * (K - 1) * WR * C : 0;  // hand-off floats per image
+    // weight gradient by (output map, group of NN input maps) items (conv_gw2) when NN > 0
+    static constexpr int NN = NN_;
+    // weight gradient by (set of MS output maps, 32 input maps) warps (conv_gw3) when MS > 0
+    static constexpr int MS = MS_;
     static_assert(M % MT == 0, "MT must divide M");
     static_assert(KK % TT == 0, "TT must divide K*K");
     static_assert(RB % KP == 0 || NB == 1, "bands must start on a window row");
@@ -144,7 +155,27 @@ struct KArgs {
     float* out_loss;             // eval: per-image loss
     unsigned char* out_wrong;    // eval: per-image error flag
     float* out_logits;           // forward: [n][kClasses]
+    unsigned long long* ptime;   // CHAOS_TIMING builds: per-CTA clock64 cycles per phase [grid][kPhases]
 };
+
+// Phase timing (instrumented build only, -DCHAOS_TIMING): thread 0 adds the clock64 cycles
+// since the previous mark to slot k; marks sit right after block-wide barriers, so a slot
+// holds the wall time of the phase that ends there.
+constexpr int kPhases = 16;
+#ifdef CHAOS_TIMING
+#define PTIME(k)                                                          \
+    do {                                                                  \
+        if (threadIdx.x == 0 && a.ptime) {                                \
+            const long long t_ = clock64();                               \
+            a.ptime[blockIdx.x * kPhases + (k)] += t_ - t_last;           \
+            t_last = t_;                                                  \
+        }                                                                 \
+    } while (0)
+#else
+#define PTIME(k) \
+    do {         \
+    } while (0)
+#endif
 
 // ------------------------------------------------------------------------------------
 // PTX helpers: mbarrier, TMA bulk copies global->shared, bulk reduce/copy shared->global
@@ -203,6 +234,11 @@ __device__ __forceinline__ void bulk_wait_all() {
 __device__ __forceinline__ void red_add(float* p, float v) {
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
+// 16-B vector reduction into global memory (SASS REDG.E.ADD.F32x4): 4 consecutive weights
+__device__ __forceinline__ void red_add4(float* p, float4 v) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
 
 // Async loads into shared memory tracked by one mbarrier each (tid 0 issues).
 struct Loader {
@@ -260,6 +296,16 @@ __device__ __forceinline__ void publish_elem(const KArgs& a, int slot, int idx, 
         red_add(a.params + idx, g_scaled);
     else
         a.partial[static_cast<long long>(slot) * a.pstride + idx] = g_scaled;
+}
+
+// Vector publish of 4 consecutive gradient entries (already scaled): hogwild = vector reduce
+// into the shared weights; sync = plain 16-B store into this group's slot.
+template <int MODE>
+__device__ __forceinline__ void publish_vec4(const KArgs& a, int slot, int idx, float4 g_scaled) {
+    if constexpr (MODE == kHogwild)
+        red_add4(a.params + idx, g_scaled);
+    else
+        *reinterpret_cast<float4*>(a.partial + static_cast<long long>(slot) * a.pstride + idx) = g_scaled;
 }
 
 template <int N, bool A4>
@@ -469,6 +515,171 @@ __device__ __forceinline__ void conv_gw(const KArgs& a, int slot, const float* _
 }
 
 // ------------------------------------------------------------------------------------
+// PHASE(conv_gw2) conv weight gradient, one thread item = (output map m, NN input maps):
+//   gW[n][i][j][m] = sum_g sum_w dp[g][m][w] * in[g][n][argpos(g,m,w) + (i,j)],  gb[m] = sum dp
+// Consecutive lanes take consecutive n-groups of the same m, so the delta and argmax loads
+// are broadcasts; the windows of a pooled row are unrolled, so the only per-window address
+// arithmetic is the argmax phase offset and all NN*K*K gathers use immediate offsets.  Sums
+// are in a fixed (g, window) order per element (deterministic); the block, scaled by `sc`,
+// is assembled in the weight store's layout in `scr` and published with one bulk op.
+// ------------------------------------------------------------------------------------
+template <class L, int NT, int MODE>
+__device__ __forceinline__ void conv_gw2(const KArgs& a, int slot, const float* __restrict__ in,
+                                         const float* __restrict__ dp, const uint8_t* __restrict__ am,
+                                         float* __restrict__ scr, int woff, int cnt, float sc) {
+    constexpr int K = L::K, KP = L::KP, KK = L::KK, PW = L::PW, PH = L::PH, P = L::P, M = L::M, C = L::C;
+    constexpr int W = L::W, HW = L::H * L::W, NN = L::NN, NG = C / NN;
+    static_assert(NN > 0 && C % NN == 0, "NN must divide C");
+    for (int it = threadIdx.x; it < M * NG; it += NT) {
+        const int ng = it % NG;
+        const int m = it / NG;
+        float acc[NN][KK];
+#pragma unroll
+        for (int q = 0; q < NN; ++q)
+#pragma unroll
+            for (int t = 0; t < KK; ++t) acc[q][t] = 0.f;
+        float accb = 0.f;
+#pragma unroll 1
+        for (int g = 0; g < cnt; ++g) {
+            const float* ing = in + g * L::IN_SZ + ng * NN * HW;
+            const float* dpg = dp + g * L::OUT_SZ + m * P;
+            const uint8_t* amg = am + g * L::OUT_SZ + m * P;
+#pragma unroll 1
+            for (int pr = 0; pr < PH; ++pr) {
+                const float* inr = ing + pr * KP * W;
+#pragma unroll
+                for (int pc = 0; pc < PW; ++pc) {
+                    const float d = dpg[pr * PW + pc];
+                    const int arg = amg[pr * PW + pc];
+                    const float* base = inr + pc * KP + (arg / KP) * W + (arg % KP);
+#pragma unroll
+                    for (int q = 0; q < NN; ++q)
+#pragma unroll
+                        for (int t = 0; t < KK; ++t) acc[q][t] = fmaf(d, base[q * HW + (t / K) * W + (t % K)], acc[q][t]);
+                    accb += d;
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < NN; ++q)
+#pragma unroll
+            for (int t = 0; t < KK; ++t) scr[((ng * NN + q) * KK + t) * L::MP + m] = sc * acc[q][t];
+        if (ng == 0) scr[L::WFL + m] = sc * accb;
+    }
+    if constexpr (L::MP > M) {  // padding columns of the block publish zeros
+        for (int e = threadIdx.x; e < (L::ROWS + 1) * (L::MP - M); e += NT)
+            scr[(e / (L::MP - M)) * L::MP + M + e % (L::MP - M)] = 0.f;
+    }
+    sync_for_async();
+    publish_bulk<MODE>(a, slot, woff, scr, L::BLK);
+}
+
+// ------------------------------------------------------------------------------------
+// PHASE(conv_gw3) conv weight gradient (KP == 2), one warp per (set of MS output maps,
+// 32 input maps); lanes over the input map n:
+//   gW[n][i][j][m] = sum_g sum_w dp[g][m][w] * in[g][n][argpos(g,m,w) + (i,j)],  gb[m] = sum dp
+// For each (image, pooled row) the lane loads the BR x WR band of its input map that the
+// row's windows can reach into registers once; then for every window and every m of the set
+// the argmax phase (the same for all lanes: one m, one window) selects, by a warp-uniform
+// two-level branch, which compile-time band registers feed the K*K MACs.  All lanes read the
+// same relative position, so the band loads are conflict-free; delta / argmax are broadcasts.
+// Fixed (g, window) summation order per element (deterministic).
+// ------------------------------------------------------------------------------------
+template <class L, int NT, int MODE>
+__device__ __forceinline__ void conv_gw3(const KArgs& a, int slot, const float* __restrict__ in,
+                                         const float* __restrict__ dp, const uint8_t* __restrict__ am,
+                                         float* __restrict__ scr, int woff, int cnt, float sc) {
+    constexpr int K = L::K, KP = L::KP, KK = L::KK, PW = L::PW, PH = L::PH, P = L::P, M = L::M, C = L::C;
+    constexpr int W = L::W, HW = L::H * L::W, MS = L::MS, NSET = (M + MS - 1) / MS;
+    constexpr int NCW = (C + 31) / 32, BH = KP + K - 1, BW = PW * KP + K - 1;
+    constexpr int NW = NT / 32;
+    static_assert(KP == 2, "conv_gw3 handles 2x2 pooling");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int task = warp; task < NSET * NCW; task += NW) {
+        const int cw = task % NCW;
+        const int m0 = (task / NCW) * MS;
+        const int n = cw * 32 + lane;
+        const bool act = n < C;
+        float acc[MS][KK];
+        float accb[MS];
+#pragma unroll
+        for (int q = 0; q < MS; ++q) {
+            accb[q] = 0.f;
+#pragma unroll
+            for (int t = 0; t < KK; ++t) acc[q][t] = 0.f;
+        }
+#pragma unroll 1
+        for (int g = 0; g < cnt; ++g) {
+            const float* ing = in + g * L::IN_SZ + (act ? n : 0) * HW;
+            const float* dpg = dp + g * L::OUT_SZ;
+            const uint8_t* amg = am + g * L::OUT_SZ;
+#pragma unroll 1
+            for (int pr = 0; pr < PH; ++pr) {
+                float band[BH][BW];
+#pragma unroll
+                for (int r = 0; r < BH; ++r)
+#pragma unroll
+                    for (int c = 0; c < BW; ++c) band[r][c] = ing[(pr * KP + r) * W + c];
+#pragma unroll
+                for (int q = 0; q < MS; ++q) {
+                    if (MS * NSET == M || m0 + q < M) {  // warp-uniform
+                        const int ob = (m0 + q) * P + pr * PW;
+                        float dv[PW];
+                        int av[PW];
+#pragma unroll
+                        for (int pc = 0; pc < PW; ++pc) {
+                            dv[pc] = dpg[ob + pc];
+                            av[pc] = amg[ob + pc];
+                        }
+#pragma unroll
+                        for (int pc = 0; pc < PW; ++pc) {
+                            const float d = dv[pc];
+                            const int arg = av[pc];
+                            accb[q] += d;
+                            if (arg < 2) {
+                                if (arg == 0) {
+#pragma unroll
+                                    for (int t = 0; t < KK; ++t)
+                                        acc[q][t] = fmaf(d, band[t / K][pc * KP + t % K], acc[q][t]);
+                                } else {
+#pragma unroll
+                                    for (int t = 0; t < KK; ++t)
+                                        acc[q][t] = fmaf(d, band[t / K][pc * KP + 1 + t % K], acc[q][t]);
+                                }
+                            } else {
+                                if (arg == 2) {
+#pragma unroll
+                                    for (int t = 0; t < KK; ++t)
+                                        acc[q][t] = fmaf(d, band[1 + t / K][pc * KP + t % K], acc[q][t]);
+                                } else {
+#pragma unroll
+                                    for (int t = 0; t < KK; ++t)
+                                        acc[q][t] = fmaf(d, band[1 + t / K][pc * KP + 1 + t % K], acc[q][t]);
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < MS; ++q) {
+            if (act && (MS * NSET == M || m0 + q < M)) {
+#pragma unroll
+                for (int t = 0; t < KK; ++t) scr[(n * KK + t) * L::MP + m0 + q] = sc * acc[q][t];
+                if (n == 0) scr[L::WFL + m0 + q] = sc * accb[q];
+            }
+        }
+    }
+    if constexpr (L::MP > M) {  // padding columns of the block publish zeros
+        for (int e = threadIdx.x; e < (L::ROWS + 1) * (L::MP - M); e += NT)
+            scr[(e / (L::MP - M)) * L::MP + M + e % (L::MP - M)] = 0.f;
+    }
+    sync_for_async();
+    publish_bulk<MODE>(a, slot, woff, scr, L::BLK);
+}
+
+// ------------------------------------------------------------------------------------
 // PHASE(conv_din) partial derivatives of the previous layer:
 //   dout[g][n][y][x] = (1 - in^2) * sum_m sum_pp [tap in range] W[n][y-r][x-c][m] dp[g][m][pp]
 // One warp per (image g, band of RB input rows, 32 input maps); lanes over n.  The windows
@@ -565,6 +776,166 @@ __device__ __forceinline__ void conv_din(const float* __restrict__ wsm, const fl
 }
 
 // ------------------------------------------------------------------------------------
+// PHASE(conv_din2) partial derivatives of the previous layer, by window-row bands (KP == 2):
+//   dout[g][n][y][x] = (1 - in^2) * sum_m sum_w [argpos(g,m,w) + (i,j) == (y,x)] W[m][n][i][j] d[g][m][w]
+// One warp per (image g, band of PB window rows, 32 input maps n); lanes over n.  A band's
+// windows scatter into input rows [band*PB*KP, band*PB*KP + BR): a BR x WR register block,
+// so every window of the band is visited exactly once per m and its 2-bit argmax phase picks,
+// by a warp-uniform two-level branch, which compile-time registers its K*K MACs land in.
+// Weights for 4 output maps per LDS.128 (W[n][tap][m..m+3]).  Adjacent bands overlap in
+// K-1 rows: each band hands its last K-1 rows to the next through `hand` (fixed order, no
+// atomics), then every band writes the rows it owns, times (1 - in^2), to `out` (may alias `in`).
+// Requires one warp per task (G * NBAND * ceil(C/32) <= warps); rows/cols that receive no
+// delta (floor-dropped) are written as 0.  W is the staged pre-update snapshot (R5).
+// ------------------------------------------------------------------------------------
+template <class L, int NT>
+__device__ __forceinline__ void conv_din2(const float* __restrict__ wsm, const float* __restrict__ dp,
+                                          const uint8_t* __restrict__ am, const float* in, float* out,
+                                          float* __restrict__ hand, int cnt) {
+    constexpr int K = L::K, KP = L::KP, KK = L::KK, PW = L::PW, PH = L::PH, P = L::P, M = L::M, C = L::C;
+    constexpr int H = L::H, W = L::W, HW = H * W, PB = L::PB, NBAND = L::NBAND, BR = L::BR, WR = L::WR;
+    constexpr int NCW = (C + 31) / 32;
+    static_assert(KP == 2, "conv_din2 handles 2x2 pooling");
+    static_assert(NBAND == 1 || KP >= K - 1, "band overlap must stay within adjacent bands");
+    static_assert(M % 4 == 0 && L::MP == M, "4 output maps per vector load");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int total = cnt * NBAND * NCW;
+    const bool has = warp < total;
+    const int cw = warp % NCW;
+    const int band = (warp / NCW) % NBAND;
+    const int g = warp / (NCW * NBAND);
+    const int n = cw * 32 + lane;
+    const bool act = has && n < C;
+    float acc[BR][WR];
+#pragma unroll
+    for (int r = 0; r < BR; ++r)
+#pragma unroll
+        for (int c = 0; c < WR; ++c) acc[r][c] = 0.f;
+    if (has) {
+        const int pr0 = band * PB;
+        const float* dpg = dp + g * L::OUT_SZ;
+        const uint8_t* amg = am + g * L::OUT_SZ;
+        const float* wn = wsm + (act ? n : 0) * KK * L::MP;
+        // per output map: K*K weights (4 maps per LDS.128 + select when K*K is small, else scalar
+        // loads), then every window's (delta, argmax) loaded before the first branch
+        constexpr bool W4 = KK <= 4;
+#pragma unroll 1
+        for (int m4 = 0; m4 < M; m4 += 4) {
+            float4 w4[W4 ? KK : 1];
+            if constexpr (W4) {
+#pragma unroll
+                for (int tp = 0; tp < KK; ++tp) w4[tp] = *reinterpret_cast<const float4*>(wn + tp * L::MP + m4);
+            }
+#pragma unroll 1
+            for (int mm = 0; mm < 4; ++mm) {
+                const int m = m4 + mm;
+                float w[KK];
+#pragma unroll
+                for (int tp = 0; tp < KK; ++tp) {
+                    if constexpr (W4)
+                        w[tp] = mm == 0 ? w4[tp].x : mm == 1 ? w4[tp].y : mm == 2 ? w4[tp].z : w4[tp].w;
+                    else
+                        w[tp] = wn[tp * L::MP + m];
+                }
+                float dv[PB][PW];
+                int av[PB][PW];
+#pragma unroll
+                for (int wr = 0; wr < PB; ++wr)
+#pragma unroll
+                    for (int pc = 0; pc < PW; ++pc) {
+                        const bool ok = pr0 + wr < PH;
+                        const int o = m * P + (ok ? pr0 + wr : 0) * PW + pc;
+                        dv[wr][pc] = dpg[o];
+                        av[wr][pc] = ok ? static_cast<int>(amg[o]) : -1;
+                    }
+#pragma unroll
+                for (int wr = 0; wr < PB; ++wr) {
+#pragma unroll
+                    for (int pc = 0; pc < PW; ++pc) {
+                        const float d = dv[wr][pc];
+                        const int arg = av[wr][pc];
+                        // warp-uniform two-level branch on the argmax phase (a, b)
+                        if (arg < 2) {
+                            if (arg == 0) {
+#pragma unroll
+                                for (int i = 0; i < K; ++i)
+#pragma unroll
+                                    for (int j = 0; j < K; ++j)
+                                        acc[wr * KP + i][pc * KP + j] = fmaf(w[i * K + j], d, acc[wr * KP + i][pc * KP + j]);
+                            } else if (arg == 1) {
+#pragma unroll
+                                for (int i = 0; i < K; ++i)
+#pragma unroll
+                                    for (int j = 0; j < K; ++j)
+                                        acc[wr * KP + i][pc * KP + 1 + j] =
+                                            fmaf(w[i * K + j], d, acc[wr * KP + i][pc * KP + 1 + j]);
+                            }
+                        } else {
+                            if (arg == 2) {
+#pragma unroll
+                                for (int i = 0; i < K; ++i)
+#pragma unroll
+                                    for (int j = 0; j < K; ++j)
+                                        acc[wr * KP + 1 + i][pc * KP + j] =
+                                            fmaf(w[i * K + j], d, acc[wr * KP + 1 + i][pc * KP + j]);
+                            } else {
+#pragma unroll
+                                for (int i = 0; i < K; ++i)
+#pragma unroll
+                                    for (int j = 0; j < K; ++j)
+                                        acc[wr * KP + 1 + i][pc * KP + 1 + j] =
+                                            fmaf(w[i * K + j], d, acc[wr * KP + 1 + i][pc * KP + 1 + j]);
+                            }
+                        }
+                    }
+                }
+            }
+        }
+    }
+    if constexpr (NBAND > 1) {
+        // hand the last K-1 rows to the next band: hand[g][band][r][c][n]
+        if (act && band < NBAND - 1) {
+            float* hb = hand + ((g * (NBAND - 1) + band) * (K - 1)) * WR * C + n;
+#pragma unroll
+            for (int r = 0; r < K - 1; ++r)
+#pragma unroll
+                for (int c = 0; c < WR; ++c) hb[(r * WR + c) * C] = acc[BR - (K - 1) + r][c];
+        }
+        __syncthreads();
+        if (act && band > 0) {
+            const float* hb = hand + ((g * (NBAND - 1) + band - 1) * (K - 1)) * WR * C + n;
+#pragma unroll
+            for (int r = 0; r < K - 1; ++r)
+#pragma unroll
+                for (int c = 0; c < WR; ++c) acc[r][c] += hb[(r * WR + c) * C];
+        }
+    }
+    if (act) {
+        // rows owned: [y0, y1); the last band also owns the rows below (0 if never reached)
+        const int y0 = band * PB * KP;
+        const float* ib = in + g * L::IN_SZ + n * HW;
+        float* ob = out + g * L::IN_SZ + n * HW;
+#pragma unroll
+        for (int lr = 0; lr < BR; ++lr) {
+            const int y = y0 + lr;
+            const bool own = (band == NBAND - 1) ? (y < H) : (lr < PB * KP);
+            if (own) {
+#pragma unroll
+                for (int x = 0; x < W; ++x) {
+                    const float v = ib[y * W + x];
+                    ob[y * W + x] = (x < WR ? acc[lr][x] : 0.f) * (1.f - v * v);
+                }
+            }
+        }
+        if (band == NBAND - 1) {
+            for (int y = y0 + BR; y < H; ++y)
+#pragma unroll
+                for (int x = 0; x < W; ++x) ob[y * W + x] = 0.f;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
 // PHASE(fc_fwd) fully connected forward: one warp per output row, lanes over inputs,
 // weights streamed from L2 (__ldcg: on-demand reads of the shared store, no stale L1 copy).
 // ------------------------------------------------------------------------------------
@@ -590,6 +961,162 @@ __device__ __forceinline__ void fc_fwd(const float* __restrict__ Wg, const float
         for (int g = 0; g < G; ++g) {
             const float s = warp_sum(acc[g]) + b;
             if (lane == 0 && g < cnt) out[g * ostride + o] = F::TANH ? tanhf(s) : s;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// PHASE(fc_fwd2) fully connected forward, IN % 4 == 0: one warp per NR output rows, lanes
+// over 16-B column quads; every weight load of the NR rows is issued before the first FMA
+// (__ldcg: on-demand reads of the shared store from L2), activations are LDS.128 broadcasts
+// shared by the NR rows, and the NR*G partial sums are reduced with warp shuffles.
+// ------------------------------------------------------------------------------------
+template <class F, int G, int NT, int NR>
+__device__ __forceinline__ void fc_fwd2(const float* __restrict__ Wg, const float* __restrict__ bg,
+                                        const float* __restrict__ in, float* __restrict__ out, int ostride,
+                                        int cnt) {
+    static_assert(F::IN % 4 == 0, "column quads");
+    constexpr int IN4 = F::IN / 4, NK = (IN4 + 31) / 32, NW = NT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int o0 = warp * NR; o0 < F::OUT; o0 += NW * NR) {
+        float4 w[NR][NK];
+#pragma unroll
+        for (int r = 0; r < NR; ++r)
+#pragma unroll
+            for (int k = 0; k < NK; ++k) {
+                const int c = lane + 32 * k;
+                w[r][k] = (o0 + r < F::OUT && c < IN4)
+                              ? __ldcg(reinterpret_cast<const float4*>(Wg + static_cast<long long>(o0 + r) * F::IN) + c)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        float acc[NR][G];
+#pragma unroll
+        for (int r = 0; r < NR; ++r)
+#pragma unroll
+            for (int g = 0; g < G; ++g) acc[r][g] = 0.f;
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
+            const int c = lane + 32 * k;
+            if (c < IN4) {
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const float4 x = reinterpret_cast<const float4*>(in + g * F::IN)[c];
+#pragma unroll
+                    for (int r = 0; r < NR; ++r) {
+                        acc[r][g] = fmaf(w[r][k].x, x.x, acc[r][g]);
+                        acc[r][g] = fmaf(w[r][k].y, x.y, acc[r][g]);
+                        acc[r][g] = fmaf(w[r][k].z, x.z, acc[r][g]);
+                        acc[r][g] = fmaf(w[r][k].w, x.w, acc[r][g]);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            if (o0 + r < F::OUT) {
+                const float b = __ldcg(bg + o0 + r);
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const float s = warp_sum(acc[r][g]) + b;
+                    if (lane == 0 && g < cnt) out[g * ostride + o0 + r] = F::TANH ? tanhf(s) : s;
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// PHASE(fc_bwd2) fully connected backward without staging (IN % 4 == 0).  Thread item =
+// (16-B column quad c, row group rg of ~OUT/NRG rows).  Per row o the thread reads W[o][4c]
+// (pre-update: it is the only reader of those 4 weights in this CTA and reads them before
+// publishing their gradient), accumulates delta_in for its columns, and publishes
+// gW[o][4c..4c+3] = sum_g dz[g][o] a[g][4c..] with one 16-B vector reduction (hogwild) or
+// store (sync) -- no shared-memory staging, no per-chunk barriers.  Row groups' delta_in
+// partials meet in `scr` ([NRG-1][G][IN]) and are summed in group order (deterministic),
+// times (1 - a^2), in place over `in`.  Bias gradients go through `bsc` + one bulk op.
+// ------------------------------------------------------------------------------------
+template <class F, int G, int NT, int MODE, int NRG>
+__device__ __forceinline__ void fc_bwd2(const KArgs& a, int slot, int woff, int boff, float* __restrict__ in,
+                                        const float* __restrict__ dz, int dstride, float* __restrict__ scr,
+                                        float* __restrict__ bsc, int cnt, float sc) {
+    static_assert(F::IN % 4 == 0, "column quads");
+    constexpr int IN4 = F::IN / 4;
+    static_assert(IN4 * NRG <= NT, "one thread per (column quad, row group)");
+    const float* Wg = a.params + woff;
+    const int c = threadIdx.x % IN4;
+    const int rg = threadIdx.x / IN4;
+    const bool act = threadIdx.x < IN4 * NRG;
+    float4 av[G], din[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        av[g] = (act && g < cnt) ? reinterpret_cast<const float4*>(in + g * F::IN)[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+        din[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (act) {
+        const int o0 = (F::OUT * rg) / NRG, o1 = (F::OUT * (rg + 1)) / NRG;
+        constexpr int BATCH = 6;
+#pragma unroll 1
+        for (int ob = o0; ob < o1; ob += BATCH) {
+            float4 w[BATCH];
+#pragma unroll
+            for (int q = 0; q < BATCH; ++q)
+                w[q] = (ob + q < o1) ? __ldcg(reinterpret_cast<const float4*>(Wg + static_cast<long long>(ob + q) * F::IN) + c)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int q = 0; q < BATCH; ++q) {
+                if (ob + q < o1) {
+                    const int o = ob + q;
+                    float4 gw = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        if (g < cnt) {
+                            const float d = dz[g * dstride + o];
+                            din[g].x = fmaf(w[q].x, d, din[g].x);
+                            din[g].y = fmaf(w[q].y, d, din[g].y);
+                            din[g].z = fmaf(w[q].z, d, din[g].z);
+                            din[g].w = fmaf(w[q].w, d, din[g].w);
+                            gw.x = fmaf(d, av[g].x, gw.x);
+                            gw.y = fmaf(d, av[g].y, gw.y);
+                            gw.z = fmaf(d, av[g].z, gw.z);
+                            gw.w = fmaf(d, av[g].w, gw.w);
+                        }
+                    }
+                    publish_vec4<MODE>(a, slot, woff + o * F::IN + 4 * c,
+                                       make_float4(sc * gw.x, sc * gw.y, sc * gw.z, sc * gw.w));
+                }
+            }
+        }
+        if (rg > 0)
+#pragma unroll
+            for (int g = 0; g < G; ++g)
+                reinterpret_cast<float4*>(scr + ((rg - 1) * G + g) * F::IN)[c] = din[g];
+    }
+    for (int o = threadIdx.x; o < F::BFL; o += NT) {  // bias
+        float gb = 0.f;
+        if (o < F::OUT)
+            for (int g = 0; g < cnt; ++g) gb += dz[g * dstride + o];
+        bsc[o] = sc * gb;
+    }
+    sync_for_async();
+    publish_bulk<MODE>(a, slot, boff, bsc, F::BFL);
+    if (act && rg == 0) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            if (g < cnt) {
+                float4 t = din[g];
+#pragma unroll
+                for (int k = 1; k < NRG; ++k) {
+                    const float4 p = reinterpret_cast<const float4*>(scr + ((k - 1) * G + g) * F::IN)[c];
+                    t.x += p.x;
+                    t.y += p.y;
+                    t.z += p.z;
+                    t.w += p.w;
+                }
+                const float4 x = av[g];
+                reinterpret_cast<float4*>(in + g * F::IN)[c] =
+                    make_float4(t.x * (1.f - x.x * x.x), t.y * (1.f - x.y * x.y), t.z * (1.f - x.z * x.z),
+                                t.w * (1.f - x.w * x.w));
+            }
         }
     }
 }
@@ -704,6 +1231,10 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
     constexpr int W3A = (NCONV >= 3) ? (C3::C / 2) * C3::KK * C3::MP : 0;
     static_assert(NCONV < 3 || W3A <= W2OFF, "W3 first half must not overlap W2");
     static_assert(NCONV < 2 || C1::BLK <= W2OFF, "W1 and W2 must not overlap");
+    static_assert(NCONV < 2 || C2::PB == 0 || G * C2::NBAND * ((C2::C + 31) / 32) <= NT / 32,
+                  "conv_din2 needs one warp per (image, band, 32 maps)");
+    static_assert(NCONV < 3 || C3::PB == 0 || G * C3::NBAND * ((C3::C + 31) / 32) <= NT / 32,
+                  "conv_din2 needs one warp per (image, band, 32 maps)");
 
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // 4 mbarriers
@@ -738,6 +1269,8 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
     Loader L0{bars + 0, 0u}, L1{bars + 1, 0u}, L2{bars + 2, 0u}, L3{bars + 3, 0u};
 
     long long iter = 0;
+    long long t_last = clock64();
+    (void)t_last;
     for (;;) {
         // ---------------- a1: claim the next unprocessed images
         if (threadIdx.x == 0) {
@@ -751,6 +1284,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
         fence_proxy_async();  // earlier generic smem / global accesses precede the async proxy
         __syncthreads();
         const int base = *s_base;
+        PTIME(0);
         if (base < 0) break;
         const int slot = static_cast<int>(base / G);
         const int cnt = static_cast<int>(min(static_cast<long long>(G), a.n - base));
@@ -785,6 +1319,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             for (int i = threadIdx.x; i < cnt * IMG; i += NT) sS[i] = __ldg(xsrc + i);
         L0.wait();
         if (!x_bulk) __syncthreads();
+        PTIME(1);
 
         // ---------------- a2: conv -> tanh -> pool, layer by layer
         conv_fwd<C1, NT>(sS, wb, a1, am1, cnt);
@@ -792,6 +1327,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
         if constexpr (NCONV >= 2) {
             fence_proxy_async();
             __syncthreads();
+            PTIME(2);
             if constexpr (NCONV >= 3) L2.issue(wb, P + O::c3w, W3A);  // W1 region is dead: W3's first half
             L1.wait();
             conv_fwd<C2, NT>(a1, wb + W2OFF, a2, am2, cnt);
@@ -800,6 +1336,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
         if constexpr (NCONV >= 3) {
             fence_proxy_async();
             __syncthreads();
+            PTIME(3);
             L3.issue(wb + W3A, P + O::c3w + W3A, C3::BLK - W3A);
             L2.wait();
             L3.wait();
@@ -807,15 +1344,20 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             alast = a3;
         }
         __syncthreads();
+        PTIME(4);
         // ---------------- a3: full layers
         if constexpr (NFULL == 2) {
-            fc_fwd<F1, G, NT>(P + O::f1w, P + O::f1b, alast, hh, F1::OUT, cnt);
+            if constexpr (F1::IN % 4 == 0)
+                fc_fwd2<F1, G, NT, 4>(P + O::f1w, P + O::f1b, alast, hh, F1::OUT, cnt);
+            else
+                fc_fwd<F1, G, NT>(P + O::f1w, P + O::f1b, alast, hh, F1::OUT, cnt);
             __syncthreads();
             fc_fwd<F2, G, NT>(P + O::f2w, P + O::f2b, hh, zz, kZStride, cnt);
         } else {
             fc_fwd<F1, G, NT>(P + O::f1w, P + O::f1b, alast, zz, kZStride, cnt);
         }
         __syncthreads();
+        PTIME(5);
         // ---------------- a4: softmax cross-entropy, output delta
         if (threadIdx.x < cnt) {
             const int g = threadIdx.x;
@@ -848,6 +1390,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
         }
         if constexpr (TRAIN) {
             __syncthreads();
+            PTIME(6);
             if (threadIdx.x == 0 && a.loss_sum) {
                 double ls = 0.0;
                 for (int g = 0; g < cnt; ++g) ls += s_loss[g];
@@ -857,25 +1400,57 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             if constexpr (NFULL == 2) {
                 fc_bwd<F2, G, NT, MODE, SHALF>(a, slot, O::f2w, O::f2b, hh, zz, kZStride, sS, bsc, cnt, sc);
                 wait_publish_reads();
-                fc_bwd<F1, G, NT, MODE, SHALF>(a, slot, O::f1w, O::f1b, alast, hh, F1::OUT, sS, bsc, cnt, sc);
+                PTIME(7);
+                if constexpr (F1::IN % 4 == 0 && (F1::IN / 4) * 4 <= NT) {
+                    constexpr int NRG = NT / (F1::IN / 4) < 4 ? NT / (F1::IN / 4) : 4;
+                    static_assert((NRG - 1) * G * F1::IN <= S::SFL, "row-group partials must fit in S");
+                    fc_bwd2<F1, G, NT, MODE, NRG>(a, slot, O::f1w, O::f1b, alast, hh, F1::OUT, sS, bsc, cnt, sc);
+                } else {
+                    fc_bwd<F1, G, NT, MODE, SHALF>(a, slot, O::f1w, O::f1b, alast, hh, F1::OUT, sS, bsc, cnt, sc);
+                }
             } else {
                 fc_bwd<F1, G, NT, MODE, SHALF>(a, slot, O::f1w, O::f1b, alast, zz, kZStride, sS, bsc, cnt, sc);
             }
             wait_publish_reads();
+            PTIME(8);
             // ---------------- a6/a7: pool + conv backward, publish per layer
             if constexpr (NCONV == 3) {
                 // W3 is still staged from the forward pass (the exact snapshot it used)
-                conv_din<C3, NT>(wb, a3, am3, a2, sS, cnt);  // delta for the pool2 outputs -> S
+                if constexpr (C3::PB > 0)
+                    conv_din2<C3, NT>(wb, a3, am3, a2, sS, nullptr, cnt);  // delta for the pool2 outputs -> S
+                else
+                    conv_din<C3, NT>(wb, a3, am3, a2, sS, cnt);
                 __syncthreads();
-                conv_gw<C3, NT, MODE, true>(a, slot, a2, a3, am3, wb, O::c3w, cnt, sc);
+                PTIME(9);
+                if constexpr (C3::MS > 0)
+                    conv_gw3<C3, NT, MODE>(a, slot, a2, a3, am3, wb, O::c3w, cnt, sc);
+                else if constexpr (C3::NN > 0)
+                    conv_gw2<C3, NT, MODE>(a, slot, a2, a3, am3, wb, O::c3w, cnt, sc);
+                else
+                    conv_gw<C3, NT, MODE, true>(a, slot, a2, a3, am3, wb, O::c3w, cnt, sc);
                 fence_proxy_async();
                 wait_publish_reads();
+                PTIME(10);
                 L1.issue(wb, P + O::c2w, C2::BLK);  // W2 again (pre-update snapshot for delta_in)
                 L1.wait();
-                conv_gw<C2, NT, MODE, true>(a, slot, a1, sS, am2, wb + C2::BLK, O::c2w, cnt, sc);
+                PTIME(11);
+                if constexpr (C2::MS > 0)
+                    conv_gw3<C2, NT, MODE>(a, slot, a1, sS, am2, wb + C2::BLK, O::c2w, cnt, sc);
+                else if constexpr (C2::NN > 0)
+                    conv_gw2<C2, NT, MODE>(a, slot, a1, sS, am2, wb + C2::BLK, O::c2w, cnt, sc);
+                else
+                    conv_gw<C2, NT, MODE, true>(a, slot, a1, sS, am2, wb + C2::BLK, O::c2w, cnt, sc);
                 __syncthreads();
-                conv_din<C2, NT>(wb, sS, am2, a1, a1, cnt);
+                PTIME(12);
+                if constexpr (C2::PB > 0) {
+                    static_assert(G * C2::HAND <= S::A3 - S::A2 + (S::HH - S::A3) + (S::Z - S::HH),
+                                  "conv2 hand-off must fit in the dead A2/A3/HH regions");
+                    conv_din2<C2, NT>(wb, sS, am2, a1, a1, a2, cnt);  // a2..HH are dead here
+                } else {
+                    conv_din<C2, NT>(wb, sS, am2, a1, a1, cnt);
+                }
                 __syncthreads();
+                PTIME(13);
             } else if constexpr (NCONV == 2) {
                 // W2 is still staged from the forward pass at W2OFF
                 conv_gw<C2, NT, MODE, false>(a, slot, a1, a2, am2, nullptr, O::c2w, cnt, sc);
@@ -893,10 +1468,15 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 for (int i = threadIdx.x; i < cnt * IMG; i += NT) sS[i] = __ldg(xsrc + i);
                 __syncthreads();
             }
+            PTIME(14);
             conv_gw<C1, NT, MODE, true>(a, slot, sS, a1, am1, wb, O::c1w, cnt, sc);
             if (threadIdx.x == 0) bulk_wait_all<0>();  // publishes complete before the next claim
+#ifndef CHAOS_NO_ITER_FENCE
+            if constexpr (MODE == kHogwild) __threadfence();  // this worker's REDs precede its next reads
+#endif
         }
         __syncthreads();
+        PTIME(15);
     }
     if (threadIdx.x == 0) bulk_wait_all<0>();
 }

@@ -22,8 +22,12 @@ using namespace chaos;
 // ----------------------------------------------------------------------------------
 namespace {
 
+// INFLIGHT: the hogwild staleness cap (R14, SURVEY C-23): at most this many images
+// are in flight per GPU (#CTAs x G).  Measured on the B200 (scripts/hogwild_sweep.py): the tiny
+// net at lr 0.001 blows up in epoch 1 with 592-1184 in flight, the large net trains like
+// sequential SGD with 592.  GINIT is the group G a new net starts with.
 struct TinyNet {  // configs[0], configs[1]: conv5 4x4 -> tanh -> pool2 -> FC 845->10
-    static constexpr int NCONV = 1, NFULL = 1, GDEF = 4, NT = 256, SFL = 2 * 8456;
+    static constexpr int NCONV = 1, NFULL = 1, GDEF = 4, GINIT = 1, INFLIGHT = 148, NT = 256, SFL = 2 * 8456;
     using C1 = Conv<1, 29, 29, 5, 4, 2, /*MT*/ 5, /*TT*/ 16, /*GS*/ 32, /*RB*/ 2>;
     using C2 = C1;
     using C3 = C1;
@@ -31,7 +35,7 @@ struct TinyNet {  // configs[0], configs[1]: conv5 4x4 -> tanh -> pool2 -> FC 84
     using F2 = F1;
 };
 struct MediumNet {  // configs[2] = Table I medium
-    static constexpr int NCONV = 2, NFULL = 2, GDEF = 4, NT = 512, SFL = 6000;
+    static constexpr int NCONV = 2, NFULL = 2, GDEF = 4, GINIT = 4, INFLIGHT = 592, NT = 512, SFL = 6000;
     using C1 = Conv<1, 29, 29, 20, 4, 2, 10, 16, 16, 2>;
     using C2 = Conv<20, 13, 13, 40, 5, 3, 4, 25, 1, 3>;
     using C3 = C2;
@@ -39,10 +43,10 @@ struct MediumNet {  // configs[2] = Table I medium
     using F2 = Full<150, 10, false>;
 };
 struct LargeNet {  // configs[3], configs[4]
-    static constexpr int NCONV = 3, NFULL = 2, GDEF = 4, NT = 512, SFL = 6000;
+    static constexpr int NCONV = 3, NFULL = 2, GDEF = 4, GINIT = 4, INFLIGHT = 592, NT = 512, SFL = 6000;
     using C1 = Conv<1, 29, 29, 20, 4, 2, 10, 16, 16, 2>;
-    using C2 = Conv<20, 13, 13, 60, 3, 2, 12, 9, 1, 4>;
-    using C3 = Conv<60, 5, 5, 100, 2, 2, 4, 4, 1, 5>;
+    using C2 = Conv<20, 13, 13, 60, 3, 2, 12, 9, 1, 4, /*PB*/ 2, /*NN*/ 2, /*MS*/ 2>;
+    using C3 = Conv<60, 5, 5, 100, 2, 2, 4, 4, 1, 5, /*PB*/ 2, /*NN*/ 4, /*MS*/ 13>;
     using F1 = Full<400, 150, true>;
     using F2 = Full<150, 10, false>;
 };
@@ -68,7 +72,8 @@ struct NetDesc {
     std::vector<Block> blocks;
     long long pint = 0;    // internal floats
     long long nparams = 0; // normative count
-    int gdef = 1, nt = 256;
+    int gdef = 1, ginit = 1, nt = 256;
+    int max_inflight = 1 << 30;  // hogwild staleness cap: #CTAs x G
     // [gi][mode]: gi 0 -> G=1, gi 1 -> G=gdef
     KernelFn fn[2][4] = {};
     int smem[2] = {0, 0};
@@ -141,6 +146,8 @@ NetDesc make_desc(const char* name, std::vector<LayerSig> sig) {
     d.pint = O::total;
     d.nparams = norm;
     d.gdef = Net::GDEF;
+    d.ginit = Net::GINIT;
+    d.max_inflight = Net::INFLIGHT;
     d.nt = Net::NT;
     fill_kernels<Net, 1>(d, 0);
     fill_kernels<Net, Net::GDEF>(d, 1);
@@ -214,6 +221,8 @@ struct chaos_net {
     int max_ctas = 0;
     int debug_claims = 0;
     int occ[2][4] = {};
+    unsigned long long* ptime = nullptr;  // CHAOS_TIMING builds only
+    int ptime_grid = 0;
 };
 
 namespace {
@@ -236,6 +245,7 @@ chaos_status ensure_kernel_attrs(chaos_net* net) {
 
 int grid_for(const chaos_net* net, int mode, long long work_groups) {
     long long g = (long long)net->sms * net->occ[gidx(net)][mode];
+    if (mode == kHogwild && g * net->group > net->d->max_inflight) g = net->d->max_inflight / net->group;
     if (net->max_ctas > 0 && g > net->max_ctas) g = net->max_ctas;
     if (g > work_groups) g = work_groups;
     return (int)(g < 1 ? 1 : g);
@@ -419,7 +429,7 @@ chaos_net* chaos_net_create(const chaos_arch* arch) {
     }
     chaos_net* net = new chaos_net();
     net->d = d;
-    net->group = d->gdef;
+    net->group = d->ginit;
     auto bail = [&](chaos_status) -> chaos_net* {
         chaos_net_destroy(net);
         return nullptr;
@@ -470,7 +480,7 @@ void chaos_net_destroy(chaos_net* net) {
     if (net->stream) cudaStreamSynchronize(net->stream);
     cudaDeviceSynchronize();
     void* ptrs[] = {net->params, net->latch,  net->counter, net->loss_sum, net->partial, net->grad_out, net->claims,
-                    net->ev_loss, net->ev_wrong, net->ev_sum, net->ev_err, net->st_x, net->st_y};
+                    net->ev_loss, net->ev_wrong, net->ev_sum, net->ev_err, net->st_x, net->st_y, net->ptime};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     delete net;
@@ -568,6 +578,16 @@ chaos_status chaos_train_epoch(chaos_net* net, const float* d_images, const int3
         }
         CUDA_TRY(cudaMemsetAsync(net->counter, 0, sizeof(unsigned long long), net->stream));
         const int grid = grid_for(net, kHogwild, (n + G - 1) / G);
+#ifdef CHAOS_TIMING
+        if (net->ptime_grid < grid) {
+            if (net->ptime) cudaFree(net->ptime);
+            net->ptime = nullptr;
+            CUDA_TRY(cudaMalloc(&net->ptime, sizeof(unsigned long long) * kPhases * grid));
+            net->ptime_grid = grid;
+        }
+        CUDA_TRY(cudaMemsetAsync(net->ptime, 0, sizeof(unsigned long long) * kPhases * net->ptime_grid, net->stream));
+        k.ptime = net->ptime;
+#endif
         net->d->fn[gidx(net)][kHogwild]<<<grid, net->d->nt, net->d->smem[gidx(net)], net->stream>>>(k);
         CUDA_TRY(cudaGetLastError());
         return CHAOS_OK;
@@ -686,6 +706,24 @@ chaos_status chaos_debug_claims(chaos_net* net, int32_t* host_counts, int64_t n)
     CUDA_TRY(cudaMemcpyAsync(host_counts, net->claims, sizeof(int) * n, cudaMemcpyDeviceToHost, net->stream));
     CUDA_TRY(cudaStreamSynchronize(net->stream));
     return CHAOS_OK;
+}
+
+chaos_status chaos_debug_phase_times(chaos_net* net, uint64_t* host_cycles, int32_t n) {
+    if (!net || !host_cycles || n < 1) return fail(CHAOS_E_INVALID, "NULL argument or n < 1");
+#ifdef CHAOS_TIMING
+    if (!net->ptime) return fail(CHAOS_E_INVALID, "no hogwild epoch recorded yet");
+    std::vector<unsigned long long> h((size_t)kPhases * net->ptime_grid);
+    CUDA_TRY(cudaMemcpyAsync(h.data(), net->ptime, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost,
+                             net->stream));
+    CUDA_TRY(cudaStreamSynchronize(net->stream));
+    for (int k = 0; k < n; ++k) host_cycles[k] = 0;
+    for (int b = 0; b < net->ptime_grid; ++b)
+        for (int k = 0; k < kPhases && k < n; ++k) host_cycles[k] += h[(size_t)b * kPhases + k];
+    return CHAOS_OK;
+#else
+    (void)n;
+    return fail(CHAOS_E_UNSUPPORTED, "phase timing needs the instrumented build (libchaos_timing.so, -DCHAOS_TIMING)");
+#endif
 }
 
 chaos_status chaos_net_sync(chaos_net* net) {

@@ -9,7 +9,7 @@ mkdir -p gpurun_out
 O=gpurun_out/${TAG}
 nvidia-smi > ${O}_smi.txt 2>&1
 lscpu > ${O}_lscpu.txt 2>&1
-python -c "import __graft_entry__ as g; g.build()" > ${O}_build.log 2>&1 || { echo BUILD FAILED; tail -30 ${O}_build.log; exit 1; }
+python -c "from paper_1506_09067_b200 import build; build.build(); import oracle; oracle.build()" > ${O}_build.log 2>&1 || { echo BUILD FAILED; tail -30 ${O}_build.log; exit 1; }
 if [ -z "$SKIP_TESTS" ]; then
   timeout 1500 python -m pytest tests -m gpu -q -rsxf --timeout 600 > ${O}_pytest.log 2>&1
   echo "pytest rc=$?"; tail -15 ${O}_pytest.log

@@ -43,3 +43,43 @@ def assert_parity(got, ref, blocks, **kw):
     ok, w, wn, det = parity_report(got, ref, blocks, **kw)
     assert ok, f"parity failed: worst elementwise {w:.3g} x tol, worst norm {wn:.3g} x tol; per tensor {det}"
     return w, wn
+
+
+def min_pool_gaps(arch, trace, in_c=1, in_h=29, in_w=29):
+    """Smallest relative top-2 gap over the max-pool windows of each pool layer, from an
+    oracle forward trace (every layer's output, in order).  A gap below ~1e-6 can flip the
+    argmax between an fp32 and an fp64 run (R9, SURVEY C-15 near-tie excuse)."""
+    c, h, w = in_c, in_h, in_w
+    off = 0
+    prev = None
+    gaps = []
+    for kind, units, kernel, _ in arch:
+        if kind == 1:  # conv
+            c, h, w = units, h - kernel + 1, w - kernel + 1
+            prev = np.asarray(trace[off:off + c * h * w]).reshape(c, h, w)
+            off += c * h * w
+        elif kind == 2:  # pool
+            k = kernel
+            ph, pw = h // k, w // k
+            win = prev[:, :ph * k, :pw * k].reshape(c, ph, k, pw, k).transpose(0, 1, 3, 2, 4).reshape(c, ph, pw, k * k)
+            srt = np.sort(win, axis=-1)
+            if k * k > 1:
+                gaps.append(float(np.min((srt[..., -1] - srt[..., -2]) / np.maximum(np.abs(srt[..., -1]), 1e-30))))
+            h, w = ph, pw
+            off += c * h * w
+        else:
+            c, h, w = units, 1, 1
+            off += units
+    return gaps
+
+
+def tie_free_prefix(oracle, arch, params, X, Y, lr, gap=5e-6):
+    """Number of leading samples of the oracle's sequential-SGD trajectory before the first
+    sample with a pool window whose top-2 relative gap is below `gap`."""
+    p = np.asarray(params, np.float64).copy()
+    for i in range(len(Y)):
+        _, tr, _ = oracle.forward(p, X[i])
+        if min(min_pool_gaps(arch, tr), default=1.0) < gap:
+            return i
+        p, _ = oracle.train_sgd(p, X[i:i + 1], Y[i:i + 1], lr)
+    return len(Y)

@@ -13,7 +13,7 @@ import pytest
 
 import synthdata as sd
 from oracle import Oracle
-from helpers import assert_parity, parity_report
+from helpers import assert_parity, parity_report, tie_free_prefix
 
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden", "oracle_runs")
@@ -63,7 +63,7 @@ def test_set_get_roundtrip(name, torch_cuda):
 
 
 @pytest.mark.parametrize("name", NETS)
-@pytest.mark.parametrize("group", [None, 1])
+@pytest.mark.parametrize("group", [None, 1, 4])
 def test_forward_logits(name, group, torch_cuda):
     o, net, p = make(name, 4, torch_cuda, group)
     d = sd.prototype_dataset(4, 0, 37)  # ragged vs G
@@ -95,7 +95,7 @@ def test_gradients_group1_equal_default_group(name, torch_cuda):
     d = sd.prototype_dataset(6, 9, 0)
     X, Y = dev(torch_cuda, d.x_train, d.y_train)
     g1 = net.compute_gradients(X, Y)
-    _, net2, _ = make(name, 6, torch_cuda)
+    _, net2, _ = make(name, 6, torch_cuda, 4)
     g4 = net2.compute_gradients(X, Y)
     assert_parity(g1, g4.astype(np.float64), o.blocks())
 
@@ -170,16 +170,21 @@ def test_sync_epoch_loss_vs_oracle_run(run, torch_cuda):
 
 
 @pytest.mark.parametrize("name", NETS)
-def test_hogwild_single_worker_is_sequential_sgd(name, torch_cuda):
-    # one CTA, G = 1: CHAOS with one worker = sequential SGD (SURVEY C-9)
+@pytest.mark.parametrize("seed", [9, 21])
+def test_hogwild_single_worker_is_sequential_sgd(name, seed, torch_cuda):
+    # one CTA, G = 1: CHAOS with one worker = sequential SGD (SURVEY C-9).  The comparison
+    # runs over the trajectory's leading samples before the first pool near-tie (top-2 gap
+    # < 5e-6 relative), where fp32 vs fp64 may legitimately pick different argmaxes (R9).
     from paper_1506_09067_b200 import OPT_MAX_CTAS
-    o, net, p = make(name, 9, torch_cuda, 1)
+    o, net, p = make(name, seed, torch_cuda, 1)
     net.set_option(OPT_MAX_CTAS, 1)
-    d = sd.prototype_dataset(9, 24, 0)
-    X, Y = dev(torch_cuda, d.x_train, d.y_train)
+    d = sd.prototype_dataset(seed, 24, 0)
+    n = tie_free_prefix(o, sd.ARCHS[name], p, d.x_train, d.y_train, 0.05)
+    assert n >= 6, f"near-tie too early on this trajectory (sample {n}); pick another seed"
+    X, Y = dev(torch_cuda, d.x_train[:n], d.y_train[:n])
     net.train_epoch(X, Y, 0.05)
     got = net.get_params()
-    ref, _ = o.train_sgd(p, d.x_train, d.y_train, 0.05)
+    ref, _ = o.train_sgd(p, d.x_train[:n], d.y_train[:n], 0.05)
     assert_parity(got, ref, o.blocks())
 
 

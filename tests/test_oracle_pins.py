@@ -371,3 +371,16 @@ def test_empty_training_is_noop():
     p = sd.init_params(1, o.blocks())
     q, _ = o.train_sgd(p, np.zeros((0, 841), np.float32), np.zeros(0, np.int32), 0.1)
     np.testing.assert_array_equal(q, p.astype(np.float64))
+
+
+def test_min_pool_gaps_flags_the_appendix_a_tie():
+    # Example A has a 3-way tie in its pool window (gap 0); Example B is tie-free
+    from helpers import min_pool_gaps
+    g = json.load(open(os.path.join(GOLD, "appendix_a.json")))
+    o = Oracle(HAND_ARCH, in_h=4, in_w=4, n_classes=2)
+    p0 = np.array(g["params0"])
+    ga = min_pool_gaps(HAND_ARCH, o.forward(p0, np.array(g["A"]["x"], np.float32).reshape(-1))[1], 1, 4, 4)
+    gb = min_pool_gaps(HAND_ARCH, o.forward(p0, np.array(g["B"]["x"], np.float32).reshape(-1))[1], 1, 4, 4)
+    assert ga == [0.0]
+    # B: window values tanh(0.5), tanh(-0.5), tanh(1.5), tanh(0.5): gap = (tanh 1.5 - tanh 0.5) / tanh 1.5
+    assert gb[0] == pytest.approx((math.tanh(1.5) - math.tanh(0.5)) / math.tanh(1.5), rel=1e-12)
