@@ -48,7 +48,7 @@ __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 // Tuning knobs: MT maps per thread in the forward; TT taps per thread and GS split of the
 // (image, window) sum in the weight gradient; RB input rows per band in delta_in.
 template <int C_, int H_, int W_, int M_, int K_, int KP_, int MT_, int TT_, int GS_, int RB_, int PB_ = 0,
-          int NN_ = 0, int MS_ = 0>
+          int NN_ = 0, int MS_ = 0, bool GWMMA_ = false, bool DIN3_ = false>
 struct Conv {
     static constexpr int C = C_, H = H_, W = W_, M = M_, K = K_, KP = KP_;
     static constexpr int OH = H - K + 1, OW = W - K + 1;
@@ -70,6 +70,10 @@ struct Conv {
     static constexpr int NN = NN_;
     // weight gradient by (set of MS output maps, 32 input maps) warps (conv_gw3) when MS > 0
     static constexpr int MS = MS_;
+    // weight gradient on the tensor cores (conv_gw_mma)
+    static constexpr bool GWMMA = GWMMA_;
+    // delta_in with the compact shifted-block loop (conv_din3)
+    static constexpr bool DIN3 = DIN3_;
     static_assert(M % MT == 0, "MT must divide M");
     static_assert(KK % TT == 0, "TT must divide K*K");
     static_assert(RB % KP == 0 || NB == 1, "bands must start on a window row");
@@ -333,6 +337,35 @@ __device__ __forceinline__ void load_vec(float (&v)[N], const float* p) {
     }
 }
 
+// ------------------------------------------------------------------------------------
+// Tensor-core helpers: mma.sync m16n8k8 TF32 with the 3-pass split (a = a_hi + a_lo,
+// b = b_hi + b_lo; D += a_hi b_lo + a_lo b_hi + a_hi b_hi), which keeps the products to
+// ~2^-21 relative -- fp32-level accuracy for the R9 tolerance (a single TF32 pass is 2^-11).
+// Fragment layout (lane = 4*g8 + t): A 16x8 row-major {(g8,t), (g8+8,t), (g8,t+4), (g8+8,t+4)};
+// B 8x8 {(t,g8), (t+4,g8)}; C 16x8 {(g8,2t), (g8,2t+1), (g8+8,2t), (g8+8,2t+1)}.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+    hi = to_tf32(x);
+    lo = to_tf32(x - __uint_as_float(hi));
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void mma3(float (&d)[4], const uint32_t (&ah)[4], const uint32_t (&al)[4], uint32_t bh0,
+                                     uint32_t bh1, uint32_t bl0, uint32_t bl1) {
+    mma_tf32(d, ah, bl0, bl1);
+    mma_tf32(d, al, bh0, bh1);
+    mma_tf32(d, ah, bh0, bh1);
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -568,6 +601,98 @@ __device__ __forceinline__ void conv_gw2(const KArgs& a, int slot, const float* 
     }
     if constexpr (L::MP > M) {  // padding columns of the block publish zeros
         for (int e = threadIdx.x; e < (L::ROWS + 1) * (L::MP - M); e += NT)
+            scr[(e / (L::MP - M)) * L::MP + M + e % (L::MP - M)] = 0.f;
+    }
+    sync_for_async();
+    publish_bulk<MODE>(a, slot, woff, scr, L::BLK);
+}
+
+// ------------------------------------------------------------------------------------
+// PHASE(conv_gw_mma) conv weight gradient on the tensor cores (KP == 2), as the dense GEMM
+//   gW[k][m] = sum_g sum_p in[g][n(k)][r(p)+i(k)][c(p)+j(k)] * Dz[g][m][p]
+// over the conv positions p that lie in a pooling window (k = n*K*K + i*K + j, the row of the
+// internal weight block; Dz = the pooled delta routed to its argmax, zero elsewhere, built
+// on the fly from (dp, am) in the B fragment).  One warp per 16-row tile of k and all output
+// maps m; the A fragment is an implicit im2col gather.  Dense work is KP^2 = 4x the
+// argmax-sparse MACs, on a pipe ~4x faster than FFMA that also frees the issue slots.
+// Fixed k-step order per element (deterministic).  Bias gradient: fixed-order sums of dp.
+// ------------------------------------------------------------------------------------
+template <class L, int NT, int MODE>
+__device__ __forceinline__ void conv_gw_mma(const KArgs& a, int slot, const float* __restrict__ in,
+                                            const float* __restrict__ dp, const uint8_t* __restrict__ am,
+                                            float* __restrict__ scr, int woff, int cnt, float sc) {
+    constexpr int K = L::K, KK = L::KK, PW = L::PW, PH = L::PH, P = L::P, M = L::M, C = L::C;
+    constexpr int W = L::W, HW = L::H * L::W;
+    constexpr int RR = C * KK, MTL = (RR + 15) / 16, NTL = (M + 7) / 8;
+    constexpr int CW = PW * 2, KPOS = PH * 2 * CW, KSTEPS = (KPOS + 7) / 8;
+    constexpr int NW = NT / 32;
+    static_assert(L::KP == 2, "2x2 pooling");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g8 = lane >> 2, t = lane & 3;
+    for (int unit = warp; unit < MTL; unit += NW) {
+        const int kA = unit * 16 + g8, kB = kA + 8;
+        const bool vA = kA < RR, vB = kB < RR;
+        const int koA = vA ? (kA / KK) * HW + ((kA % KK) / K) * W + (kA % KK) % K : 0;
+        const int koB = vB ? (kB / KK) * HW + ((kB % KK) / K) * W + (kB % KK) % K : 0;
+        float acc[NTL][4];
+#pragma unroll
+        for (int nt = 0; nt < NTL; ++nt)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[nt][q] = 0.f;
+#pragma unroll 1
+        for (int g = 0; g < cnt; ++g) {
+            const float* ing = in + g * L::IN_SZ;
+            const float* dpg = dp + g * L::OUT_SZ;
+            const uint8_t* amg = am + g * L::OUT_SZ;
+#pragma unroll 1
+            for (int ks = 0; ks < KSTEPS; ++ks) {
+                const int p0 = ks * 8 + t, p1 = p0 + 4;
+                const bool v0 = p0 < KPOS, v1 = p1 < KPOS;
+                const int r0 = p0 / CW, c0 = p0 % CW, r1 = p1 / CW, c1 = p1 % CW;
+                const int po0 = r0 * W + c0, po1 = r1 * W + c1;
+                uint32_t ah[4], al[4];
+                split_tf32((vA && v0) ? ing[koA + po0] : 0.f, ah[0], al[0]);
+                split_tf32((vB && v0) ? ing[koB + po0] : 0.f, ah[1], al[1]);
+                split_tf32((vA && v1) ? ing[koA + po1] : 0.f, ah[2], al[2]);
+                split_tf32((vB && v1) ? ing[koB + po1] : 0.f, ah[3], al[3]);
+                const int w0 = (r0 >> 1) * PW + (c0 >> 1), ph0 = ((r0 & 1) << 1) | (c0 & 1);
+                const int w1 = (r1 >> 1) * PW + (c1 >> 1), ph1 = ((r1 & 1) << 1) | (c1 & 1);
+#pragma unroll
+                for (int nt = 0; nt < NTL; ++nt) {
+                    const int m = nt * 8 + g8;
+                    const bool vm = (NTL * 8 == M) || m < M;
+                    const int o0 = m * P + w0, o1 = m * P + w1;
+                    const float b0 = (vm && v0 && amg[o0] == ph0) ? dpg[o0] : 0.f;
+                    const float b1 = (vm && v1 && amg[o1] == ph1) ? dpg[o1] : 0.f;
+                    uint32_t bh0, bl0, bh1, bl1;
+                    split_tf32(b0, bh0, bl0);
+                    split_tf32(b1, bh1, bl1);
+                    mma3(acc[nt], ah, al, bh0, bh1, bl0, bl1);
+                }
+            }
+        }
+#pragma unroll
+        for (int nt = 0; nt < NTL; ++nt) {
+            const int m = nt * 8 + 2 * t;
+            if (vA) {
+                if (m < M) scr[kA * L::MP + m] = sc * acc[nt][0];
+                if (m + 1 < M) scr[kA * L::MP + m + 1] = sc * acc[nt][1];
+            }
+            if (vB) {
+                if (m < M) scr[kB * L::MP + m] = sc * acc[nt][2];
+                if (m + 1 < M) scr[kB * L::MP + m + 1] = sc * acc[nt][3];
+            }
+        }
+    }
+    for (int m = threadIdx.x; m < L::MP; m += NT) {  // bias: fixed-order sum over (g, window)
+        float s = 0.f;
+        if (m < M)
+            for (int g = 0; g < cnt; ++g)
+                for (int w = 0; w < P; ++w) s += dp[g * L::OUT_SZ + m * P + w];
+        scr[L::WFL + m] = sc * s;
+    }
+    if constexpr (L::MP > M) {  // padding columns of the block publish zeros
+        for (int e = threadIdx.x; e < L::ROWS * (L::MP - M); e += NT)
             scr[(e / (L::MP - M)) * L::MP + M + e % (L::MP - M)] = 0.f;
     }
     sync_for_async();
@@ -966,6 +1091,188 @@ __device__ __forceinline__ void fc_fwd(const float* __restrict__ Wg, const float
 }
 
 // ------------------------------------------------------------------------------------
+// PHASE(conv_din3) conv_din2 with a compact loop body: the task's PB window rows are a
+// runtime loop over ONE window row's (KP+K-1) x WR register block, which shifts down by KP
+// rows after each window row (its first KP rows are then final for this task).  The
+// unrolled code is one window row (PW windows x 4 phases), so it stays in the instruction
+// cache.  The first window row's KP rows wait in `pend` for the previous band's hand-off.
+// ------------------------------------------------------------------------------------
+template <class L, int NT>
+__device__ __forceinline__ void conv_din3(const float* __restrict__ wsm, const float* __restrict__ dp,
+                                          const uint8_t* __restrict__ am, const float* in, float* out,
+                                          float* __restrict__ hand, int cnt) {
+    constexpr int K = L::K, KP = L::KP, KK = L::KK, PW = L::PW, PH = L::PH, P = L::P, M = L::M, C = L::C;
+    constexpr int H = L::H, W = L::W, HW = H * W, PB = L::PB, NBAND = L::NBAND, WR = L::WR;
+    constexpr int R1 = KP + K - 1, OV = K - 1;
+    constexpr int NCW = (C + 31) / 32;
+    static_assert(KP == 2, "2x2 pooling");
+    static_assert(KP >= OV, "a window row's block overlaps only the next one");
+    static_assert(M % 4 == 0 && L::MP == M, "4 output maps per vector load");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int total = cnt * NBAND * NCW;
+    const bool has = warp < total;
+    const int cw = warp % NCW;
+    const int band = (warp / NCW) % NBAND;
+    const int g = warp / (NCW * NBAND);
+    const int n = cw * 32 + lane;
+    const bool act = has && n < C;
+    const int y0 = band * PB * KP;
+    const float* ib = in + g * L::IN_SZ + (act ? n : 0) * HW;
+    float* ob = out + g * L::IN_SZ + (act ? n : 0) * HW;
+    float acc[R1][WR], pend[KP][WR];
+#pragma unroll
+    for (int r = 0; r < R1; ++r)
+#pragma unroll
+        for (int c = 0; c < WR; ++c) acc[r][c] = 0.f;
+#pragma unroll
+    for (int r = 0; r < KP; ++r)
+#pragma unroll
+        for (int c = 0; c < WR; ++c) pend[r][c] = 0.f;
+    int nwr = 0;
+    if (has) {
+        const float* dpg = dp + g * L::OUT_SZ;
+        const uint8_t* amg = am + g * L::OUT_SZ;
+        const float* wn = wsm + (act ? n : 0) * KK * L::MP;
+        constexpr bool W4 = KK <= 4;
+#pragma unroll 1
+        for (int wr = 0; wr < PB; ++wr) {
+            const int pr = band * PB + wr;
+            if (pr >= PH) break;  // warp-uniform (short last band)
+            ++nwr;
+#pragma unroll 1
+            for (int m4 = 0; m4 < M; m4 += 4) {
+                float4 w4[W4 ? KK : 1];
+                if constexpr (W4) {
+#pragma unroll
+                    for (int tp = 0; tp < KK; ++tp) w4[tp] = *reinterpret_cast<const float4*>(wn + tp * L::MP + m4);
+                }
+#pragma unroll 1
+                for (int mm = 0; mm < 4; ++mm) {
+                    const int m = m4 + mm;
+                    float w[KK];
+#pragma unroll
+                    for (int tp = 0; tp < KK; ++tp) {
+                        if constexpr (W4)
+                            w[tp] = mm == 0 ? w4[tp].x : mm == 1 ? w4[tp].y : mm == 2 ? w4[tp].z : w4[tp].w;
+                        else
+                            w[tp] = wn[tp * L::MP + m];
+                    }
+                    float dv[PW];
+                    int av[PW];
+#pragma unroll
+                    for (int pc = 0; pc < PW; ++pc) {
+                        dv[pc] = dpg[m * P + pr * PW + pc];
+                        av[pc] = amg[m * P + pr * PW + pc];
+                    }
+#pragma unroll
+                    for (int pc = 0; pc < PW; ++pc) {
+                        const float d = dv[pc];
+                        const int arg = av[pc];
+                        if (arg < 2) {  // warp-uniform two-level branch on the argmax phase
+                            if (arg == 0) {
+#pragma unroll
+                                for (int i = 0; i < K; ++i)
+#pragma unroll
+                                    for (int j = 0; j < K; ++j)
+                                        acc[i][pc * KP + j] = fmaf(w[i * K + j], d, acc[i][pc * KP + j]);
+                            } else {
+#pragma unroll
+                                for (int i = 0; i < K; ++i)
+#pragma unroll
+                                    for (int j = 0; j < K; ++j)
+                                        acc[i][pc * KP + 1 + j] = fmaf(w[i * K + j], d, acc[i][pc * KP + 1 + j]);
+                            }
+                        } else {
+                            if (arg == 2) {
+#pragma unroll
+                                for (int i = 0; i < K; ++i)
+#pragma unroll
+                                    for (int j = 0; j < K; ++j)
+                                        acc[1 + i][pc * KP + j] = fmaf(w[i * K + j], d, acc[1 + i][pc * KP + j]);
+                            } else {
+#pragma unroll
+                                for (int i = 0; i < K; ++i)
+#pragma unroll
+                                    for (int j = 0; j < K; ++j)
+                                        acc[1 + i][pc * KP + 1 + j] =
+                                            fmaf(w[i * K + j], d, acc[1 + i][pc * KP + 1 + j]);
+                            }
+                        }
+                    }
+                }
+            }
+            // the block's first KP rows are final for this task
+            if (wr == 0) {
+#pragma unroll
+                for (int r = 0; r < KP; ++r)
+#pragma unroll
+                    for (int c = 0; c < WR; ++c) pend[r][c] = acc[r][c];
+            } else if (act) {
+#pragma unroll
+                for (int r = 0; r < KP; ++r) {
+                    const int y = y0 + wr * KP + r;
+#pragma unroll
+                    for (int x = 0; x < W; ++x) {
+                        const float v = ib[y * W + x];
+                        ob[y * W + x] = (x < WR ? acc[r][x] : 0.f) * (1.f - v * v);
+                    }
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < R1; ++r)
+#pragma unroll
+                for (int c = 0; c < WR; ++c) acc[r][c] = (r + KP < R1) ? acc[r + KP][c] : 0.f;
+        }
+    }
+    // acc rows [0, OV) now hold the task's last OV rows: input rows y0 + nwr*KP + r
+    if constexpr (NBAND > 1) {
+        if (act && band < NBAND - 1) {
+            float* hb = hand + ((g * (NBAND - 1) + band) * OV) * WR * C + n;
+#pragma unroll
+            for (int r = 0; r < OV; ++r)
+#pragma unroll
+                for (int c = 0; c < WR; ++c) hb[(r * WR + c) * C] = acc[r][c];
+        }
+        __syncthreads();
+        if (act && band > 0) {
+            const float* hb = hand + ((g * (NBAND - 1) + band - 1) * OV) * WR * C + n;
+#pragma unroll
+            for (int r = 0; r < OV; ++r)
+#pragma unroll
+                for (int c = 0; c < WR; ++c) pend[r][c] += hb[(r * WR + c) * C];
+        }
+    }
+    if (act) {
+#pragma unroll
+        for (int r = 0; r < KP; ++r) {  // the first window row's KP rows
+            const int y = y0 + r;
+#pragma unroll
+            for (int x = 0; x < W; ++x) {
+                const float v = ib[y * W + x];
+                ob[y * W + x] = (x < WR ? pend[r][x] : 0.f) * (1.f - v * v);
+            }
+        }
+        if (band == NBAND - 1) {  // the last band also owns the carried rows and everything below
+            const int ye = y0 + nwr * KP;
+#pragma unroll
+            for (int r = 0; r < OV; ++r) {
+                const int y = ye + r;
+                if (y < H) {
+#pragma unroll
+                    for (int x = 0; x < W; ++x) {
+                        const float v = ib[y * W + x];
+                        ob[y * W + x] = (x < WR ? acc[r][x] : 0.f) * (1.f - v * v);
+                    }
+                }
+            }
+            for (int y = ye + OV; y < H; ++y)
+#pragma unroll
+                for (int x = 0; x < W; ++x) ob[y * W + x] = 0.f;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
 // PHASE(fc_fwd2) fully connected forward, IN % 4 == 0: one warp per NR output rows, lanes
 // over 16-B column quads; every weight load of the NR rows is issued before the first FMA
 // (__ldcg: on-demand reads of the shared store from L2), activations are LDS.128 broadcasts
@@ -1348,7 +1655,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
         // ---------------- a3: full layers
         if constexpr (NFULL == 2) {
             if constexpr (F1::IN % 4 == 0)
-                fc_fwd2<F1, G, NT, 4>(P + O::f1w, P + O::f1b, alast, hh, F1::OUT, cnt);
+                fc_fwd2<F1, G, NT, (NT > 512 ? 2 : 4)>(P + O::f1w, P + O::f1b, alast, hh, F1::OUT, cnt);
             else
                 fc_fwd<F1, G, NT>(P + O::f1w, P + O::f1b, alast, hh, F1::OUT, cnt);
             __syncthreads();
@@ -1416,13 +1723,17 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             // ---------------- a6/a7: pool + conv backward, publish per layer
             if constexpr (NCONV == 3) {
                 // W3 is still staged from the forward pass (the exact snapshot it used)
-                if constexpr (C3::PB > 0)
-                    conv_din2<C3, NT>(wb, a3, am3, a2, sS, nullptr, cnt);  // delta for the pool2 outputs -> S
+                if constexpr (C3::DIN3)
+                    conv_din3<C3, NT>(wb, a3, am3, a2, sS, nullptr, cnt);  // delta for the pool2 outputs -> S
+                else if constexpr (C3::PB > 0)
+                    conv_din2<C3, NT>(wb, a3, am3, a2, sS, nullptr, cnt);
                 else
                     conv_din<C3, NT>(wb, a3, am3, a2, sS, cnt);
                 __syncthreads();
                 PTIME(9);
-                if constexpr (C3::MS > 0)
+                if constexpr (C3::GWMMA)
+                    conv_gw_mma<C3, NT, MODE>(a, slot, a2, a3, am3, wb, O::c3w, cnt, sc);
+                else if constexpr (C3::MS > 0)
                     conv_gw3<C3, NT, MODE>(a, slot, a2, a3, am3, wb, O::c3w, cnt, sc);
                 else if constexpr (C3::NN > 0)
                     conv_gw2<C3, NT, MODE>(a, slot, a2, a3, am3, wb, O::c3w, cnt, sc);
@@ -1434,7 +1745,9 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 L1.issue(wb, P + O::c2w, C2::BLK);  // W2 again (pre-update snapshot for delta_in)
                 L1.wait();
                 PTIME(11);
-                if constexpr (C2::MS > 0)
+                if constexpr (C2::GWMMA)
+                    conv_gw_mma<C2, NT, MODE>(a, slot, a1, sS, am2, wb + C2::BLK, O::c2w, cnt, sc);
+                else if constexpr (C2::MS > 0)
                     conv_gw3<C2, NT, MODE>(a, slot, a1, sS, am2, wb + C2::BLK, O::c2w, cnt, sc);
                 else if constexpr (C2::NN > 0)
                     conv_gw2<C2, NT, MODE>(a, slot, a1, sS, am2, wb + C2::BLK, O::c2w, cnt, sc);
@@ -1445,7 +1758,10 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 if constexpr (C2::PB > 0) {
                     static_assert(G * C2::HAND <= S::A3 - S::A2 + (S::HH - S::A3) + (S::Z - S::HH),
                                   "conv2 hand-off must fit in the dead A2/A3/HH regions");
-                    conv_din2<C2, NT>(wb, sS, am2, a1, a1, a2, cnt);  // a2..HH are dead here
+                    if constexpr (C2::DIN3)
+                        conv_din3<C2, NT>(wb, sS, am2, a1, a1, a2, cnt);  // a2..HH are dead here
+                    else
+                        conv_din2<C2, NT>(wb, sS, am2, a1, a1, a2, cnt);
                 } else {
                     conv_din<C2, NT>(wb, sS, am2, a1, a1, cnt);
                 }

@@ -43,10 +43,16 @@ struct MediumNet {  // configs[2] = Table I medium
     using F2 = Full<150, 10, false>;
 };
 struct LargeNet {  // configs[3], configs[4]
+#ifdef CHAOS_NT768
+    static constexpr int NCONV = 3, NFULL = 2, GDEF = 4, GINIT = 4, INFLIGHT = 592, NT = 768, SFL = 6000;
+    using C1 = Conv<1, 29, 29, 20, 4, 2, 5, 16, 16, 2>;
+    using C2 = Conv<20, 13, 13, 60, 3, 2, 4, 9, 1, 4, /*PB*/ 1, /*NN*/ 2, /*MS*/ 2, /*GWMMA*/ false>;
+#else
     static constexpr int NCONV = 3, NFULL = 2, GDEF = 4, GINIT = 4, INFLIGHT = 592, NT = 512, SFL = 6000;
     using C1 = Conv<1, 29, 29, 20, 4, 2, 10, 16, 16, 2>;
-    using C2 = Conv<20, 13, 13, 60, 3, 2, 12, 9, 1, 4, /*PB*/ 2, /*NN*/ 2, /*MS*/ 2>;
-    using C3 = Conv<60, 5, 5, 100, 2, 2, 4, 4, 1, 5, /*PB*/ 2, /*NN*/ 4, /*MS*/ 13>;
+    using C2 = Conv<20, 13, 13, 60, 3, 2, 12, 9, 1, 4, /*PB*/ 2, /*NN*/ 2, /*MS*/ 2, /*GWMMA*/ false, /*DIN3*/ true>;
+#endif
+    using C3 = Conv<60, 5, 5, 100, 2, 2, 4, 4, 1, 5, /*PB*/ 2, /*NN*/ 4, /*MS*/ 13, /*GWMMA*/ false, /*DIN3*/ false>;
     using F1 = Full<400, 150, true>;
     using F2 = Full<150, 10, false>;
 };
@@ -402,6 +408,16 @@ chaos_status sync_batch(chaos_net* net, const float* X, const int32_t* Y, long l
     k.n = nb;
     k.loss_sum = loss_sum;
     const int grid = grid_for(net, kSync, slots);
+#ifdef CHAOS_TIMING
+    if (net->ptime_grid < grid) {
+        if (net->ptime) cudaFree(net->ptime);
+        net->ptime = nullptr;
+        CUDA_TRY(cudaMalloc(&net->ptime, sizeof(unsigned long long) * kPhases * grid));
+        CUDA_TRY(cudaMemsetAsync(net->ptime, 0, sizeof(unsigned long long) * kPhases * grid, net->stream));
+        net->ptime_grid = grid;
+    }
+    k.ptime = net->ptime;  // accumulates over the epoch's batches (reset by a hogwild epoch)
+#endif
     net->d->fn[gidx(net)][kSync]<<<grid, net->d->nt, net->d->smem[gidx(net)], net->stream>>>(k);
     CUDA_TRY(cudaGetLastError());
     const long long np = net->d->pint;
@@ -592,6 +608,9 @@ chaos_status chaos_train_epoch(chaos_net* net, const float* d_images, const int3
         CUDA_TRY(cudaGetLastError());
         return CHAOS_OK;
     }
+#ifdef CHAOS_TIMING
+    if (net->ptime) CUDA_TRY(cudaMemsetAsync(net->ptime, 0, sizeof(unsigned long long) * kPhases * net->ptime_grid, net->stream));
+#endif
     for (long long b0 = 0; b0 < n; b0 += net->sync_batch) {
         const long long nb = (n - b0) < net->sync_batch ? (n - b0) : net->sync_batch;
         chaos_status s = sync_batch(net, d_images + b0 * 841, d_labels + b0, nb, lr, nullptr, net->loss_sum);

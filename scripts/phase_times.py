@@ -18,7 +18,7 @@ import synthdata as sd  # noqa: E402
 from paper_1506_09067_b200 import Net  # noqa: E402
 
 
-def main(arch="large", epochs=2):
+def main(arch="large", epochs=2, sync_batch=0):
     w = sd.WORKLOADS["config3"]
     xs, ys = sd.prototype_samples(w.seed, 0, 60000)
     X, Y = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
@@ -27,7 +27,12 @@ def main(arch="large", epochs=2):
     for e in range(epochs):
         st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         st.record()
-        net.train_epoch(X, Y, w.lr0 * 0.9 ** e)
+        if sync_batch:
+            from paper_1506_09067_b200 import OPT_SYNC_BATCH, SYNC
+            net.set_option(OPT_SYNC_BATCH, sync_batch)
+            net.train_epoch(X, Y, w.lr0 * 0.9 ** e, SYNC)
+        else:
+            net.train_epoch(X, Y, w.lr0 * 0.9 ** e)
         en.record()
         torch.cuda.synchronize()
         ms = st.elapsed_time(en)
@@ -43,4 +48,5 @@ def main(arch="large", epochs=2):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "large", int(sys.argv[2]) if len(sys.argv) > 2 else 2)
+    main(sys.argv[1] if len(sys.argv) > 1 else "large", int(sys.argv[2]) if len(sys.argv) > 2 else 2,
+         int(sys.argv[3]) if len(sys.argv) > 3 else 0)
