@@ -48,7 +48,7 @@ __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 // Tuning knobs: MT maps per thread in the forward; TT taps per thread and GS split of the
 // (image, window) sum in the weight gradient; RB input rows per band in delta_in.
 template <int C_, int H_, int W_, int M_, int K_, int KP_, int MT_, int TT_, int GS_, int RB_, int PB_ = 0,
-          int NN_ = 0, int MS_ = 0, bool GWMMA_ = false, bool DIN3_ = false>
+          int NN_ = 0, int MS_ = 0, bool GWMMA_ = false, bool DIN3_ = false, int GWIN_ = 0>
 struct Conv {
     static constexpr int C = C_, H = H_, W = W_, M = M_, K = K_, KP = KP_;
     static constexpr int OH = H - K + 1, OW = W - K + 1;
@@ -74,6 +74,9 @@ struct Conv {
     static constexpr bool GWMMA = GWMMA_;
     // delta_in with the compact shifted-block loop (conv_din3)
     static constexpr bool DIN3 = DIN3_;
+    // dense per-window weight gradient (conv_gw_win) with GWIN output maps per thread, run on the
+    // warps the delta_in phase leaves idle (0 = off)
+    static constexpr int GWIN = GWIN_;
     static_assert(M % MT == 0, "MT must divide M");
     static_assert(KK % TT == 0, "TT must divide K*K");
     static_assert(RB % KP == 0 || NB == 1, "bands must start on a window row");
@@ -605,6 +608,92 @@ __device__ __forceinline__ void conv_gw2(const KArgs& a, int slot, const float* 
     }
     sync_for_async();
     publish_bulk<MODE>(a, slot, woff, scr, L::BLK);
+}
+
+// ------------------------------------------------------------------------------------
+// PHASE(conv_gw_win) conv weight gradient, dense per pooling window, branch-free (KP == 2):
+//   gW[n][i][j][m] = sum_g sum_w sum_{phase q} Dz_q[g][m][w] * in[g][n][2pr+a(q)+i][2pc+b(q)+j]
+// where Dz_q = d[g][m][w] if the argmax of (g, m, w) has phase q, else 0 (4x the argmax-sparse
+// MACs, but no per-window branch).  Thread tile = (input map n, NM consecutive output maps);
+// per window the (KP+K-1)^2 input block of n is loaded once and reused by the NM maps x 4
+// phases x K*K taps from registers.  Runs on warps [W0, W0 + NWARP) so it can overlap a
+// latency-bound phase on the other warps.  No shared-memory scratch: each thread publishes
+// its K*K x NM block directly, 16-B vector reductions into the shared weights (hogwild) or
+// stores into its group's slot (sync) -- NM % 4 == 0.  Fixed (g, w, q) order (deterministic).
+// Bias gradient: tiles with n == 0.
+// ------------------------------------------------------------------------------------
+template <class L, int NT, int MODE, int NM, int W0, int NWARP>
+__device__ __forceinline__ void conv_gw_win(const KArgs& a, int slot, const float* __restrict__ in,
+                                            const float* __restrict__ dp, const uint8_t* __restrict__ am, int woff,
+                                            int cnt, float sc) {
+    constexpr int K = L::K, KP = L::KP, KK = L::KK, PW = L::PW, PH = L::PH, P = L::P, M = L::M, C = L::C;
+    constexpr int W = L::W, HW = L::H * L::W, BS = KP + K - 1;
+    constexpr int NG = (M + NM - 1) / NM, TILES = C * NG;
+    static_assert(KP == 2 && NM % 4 == 0 && M % 4 == 0, "2x2 pooling, vector publish");
+    const int tid = static_cast<int>(threadIdx.x) - W0 * 32;
+    if (tid < 0 || tid >= NWARP * 32) return;
+    for (int tile = tid; tile < TILES; tile += NWARP * 32) {
+        const int n = tile % C;
+        const int m0 = (tile / C) * NM;
+        float acc[NM][KK];
+        float accb[NM];
+#pragma unroll
+        for (int q = 0; q < NM; ++q) {
+            accb[q] = 0.f;
+#pragma unroll
+            for (int t = 0; t < KK; ++t) acc[q][t] = 0.f;
+        }
+#pragma unroll 1
+        for (int g = 0; g < cnt; ++g) {
+            const float* ing = in + g * L::IN_SZ + n * HW;
+            const float* dpg = dp + g * L::OUT_SZ;
+            const uint8_t* amg = am + g * L::OUT_SZ;
+#pragma unroll 1
+            for (int w = 0; w < P; ++w) {
+                const int pr = w / PW, pc = w - (w / PW) * PW;
+                float blk[BS][BS];
+#pragma unroll
+                for (int u = 0; u < BS; ++u)
+#pragma unroll
+                    for (int v = 0; v < BS; ++v) blk[u][v] = ing[(pr * KP + u) * W + pc * KP + v];
+#pragma unroll
+                for (int q = 0; q < NM; ++q) {
+                    const int m = m0 + q;
+                    const bool vm = (NG * NM == M) || m < M;
+                    const float d = vm ? dpg[m * P + w] : 0.f;
+                    const int ph = vm ? amg[m * P + w] : 0;
+                    accb[q] += d;
+#pragma unroll
+                    for (int aa = 0; aa < KP; ++aa)
+#pragma unroll
+                        for (int bb = 0; bb < KP; ++bb) {
+                            const float dq = (ph == aa * KP + bb) ? d : 0.f;
+#pragma unroll
+                            for (int i = 0; i < K; ++i)
+#pragma unroll
+                                for (int j = 0; j < K; ++j)
+                                    acc[q][i * K + j] = fmaf(dq, blk[aa + i][bb + j], acc[q][i * K + j]);
+                        }
+                }
+            }
+        }
+        // publish: internal row (n*KK + t), columns m0 .. m0+NM-1 (16-B aligned groups)
+#pragma unroll
+        for (int t = 0; t < KK; ++t)
+#pragma unroll
+            for (int q4 = 0; q4 < NM; q4 += 4)
+                if ((NG * NM == M) || m0 + q4 < M)
+                    publish_vec4<MODE>(a, slot, woff + (n * KK + t) * L::MP + m0 + q4,
+                                       make_float4(sc * acc[q4][t], sc * acc[q4 + 1][t], sc * acc[q4 + 2][t],
+                                                   sc * acc[q4 + 3][t]));
+        if (n == 0)
+#pragma unroll
+            for (int q4 = 0; q4 < NM; q4 += 4)
+                if ((NG * NM == M) || m0 + q4 < M)
+                    publish_vec4<MODE>(a, slot, woff + L::WFL + m0 + q4,
+                                       make_float4(sc * accb[q4], sc * accb[q4 + 1], sc * accb[q4 + 2],
+                                                   sc * accb[q4 + 3]));
+    }
 }
 
 // ------------------------------------------------------------------------------------
@@ -1723,6 +1812,17 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             // ---------------- a6/a7: pool + conv backward, publish per layer
             if constexpr (NCONV == 3) {
                 // W3 is still staged from the forward pass (the exact snapshot it used)
+                if constexpr (C3::GWIN > 0) {
+                    // delta_in (latency-bound, one warp per (image, 32 maps)) and the dense
+                    // weight gradient (issue-bound, published from registers) side by side
+                    constexpr int DW = G * C3::NBAND * ((C3::C + 31) / 32);
+                    static_assert(C3::PB > 0 && C3::NBAND == 1 && DW < NT / 32, "conv3 split");
+                    if (threadIdx.x < DW * 32)
+                        conv_din2<C3, NT>(wb, a3, am3, a2, sS, nullptr, cnt);
+                    conv_gw_win<C3, NT, MODE, C3::GWIN, DW, NT / 32 - DW>(a, slot, a2, a3, am3, O::c3w, cnt, sc);
+                    __syncthreads();
+                    PTIME(9);
+                } else {
                 if constexpr (C3::DIN3)
                     conv_din3<C3, NT>(wb, a3, am3, a2, sS, nullptr, cnt);  // delta for the pool2 outputs -> S
                 else if constexpr (C3::PB > 0)
@@ -1739,6 +1839,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                     conv_gw2<C3, NT, MODE>(a, slot, a2, a3, am3, wb, O::c3w, cnt, sc);
                 else
                     conv_gw<C3, NT, MODE, true>(a, slot, a2, a3, am3, wb, O::c3w, cnt, sc);
+                }
                 fence_proxy_async();
                 wait_publish_reads();
                 PTIME(10);
