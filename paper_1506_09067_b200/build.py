@@ -10,7 +10,7 @@ OUT = os.path.join(HERE, "libchaos.so")
 # instrumented variant (per-phase clock64 timing, chaos_debug_phase_times); profiling only
 OUT_TIMING = os.path.join(HERE, "libchaos_timing.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "550"]
+              "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "550,177"]
 
 
 def build(force=False, verbose=False, timing=False):

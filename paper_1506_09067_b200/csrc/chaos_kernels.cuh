@@ -48,7 +48,8 @@ __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 // Tuning knobs: MT maps per thread in the forward; TT taps per thread and GS split of the
 // (image, window) sum in the weight gradient; RB input rows per band in delta_in.
 template <int C_, int H_, int W_, int M_, int K_, int KP_, int MT_, int TT_, int GS_, int RB_, int PB_ = 0,
-          int NN_ = 0, int MS_ = 0, bool GWMMA_ = false, bool DIN3_ = false, int GWIN_ = 0>
+          int NN_ = 0, int MS_ = 0, bool GWMMA_ = false, bool DIN3_ = false, int GWIN_ = 0,
+          bool DWIN_ = false>
 struct Conv {
     static constexpr int C = C_, H = H_, W = W_, M = M_, K = K_, KP = KP_;
     static constexpr int OH = H - K + 1, OW = W - K + 1;
@@ -77,6 +78,8 @@ struct Conv {
     // dense per-window weight gradient (conv_gw_win) with GWIN output maps per thread, run on the
     // warps the delta_in phase leaves idle (0 = off)
     static constexpr int GWIN = GWIN_;
+    // dense branch-free per-window delta_in, whole map per lane (conv_din_win)
+    static constexpr bool DWIN = DWIN_;
     static_assert(M % MT == 0, "MT must divide M");
     static_assert(KK % TT == 0, "TT must divide K*K");
     static_assert(RB % KP == 0 || NB == 1, "bands must start on a window row");
@@ -1362,6 +1365,79 @@ __device__ __forceinline__ void conv_din3(const float* __restrict__ wsm, const f
 }
 
 // ------------------------------------------------------------------------------------
+// PHASE(conv_din_win) partial derivatives of the previous layer, dense per window and
+// branch-free (KP == 2, whole input map per lane: small layers such as conv3):
+//   dout[g][n][y][x] = (1 - in^2) * sum_m sum_w sum_q Dz_q[g][m][w] W[m][n][y-2pr-a(q)][x-2pc-b(q)]
+// One warp per (image, 32 input maps); lanes over n hold the whole HR x WR delta map in
+// registers; the phase selects d with a predicate-free select (4x the sparse MACs, no
+// branches, so the warp issues back to back).  Weights: 4 output maps per LDS.128.
+// ------------------------------------------------------------------------------------
+template <class L, int NT>
+__device__ __forceinline__ void conv_din_win(const float* __restrict__ wsm, const float* __restrict__ dp,
+                                             const uint8_t* __restrict__ am, const float* __restrict__ in,
+                                             float* __restrict__ out, int cnt) {
+    constexpr int K = L::K, KP = L::KP, KK = L::KK, PW = L::PW, P = L::P, M = L::M, C = L::C;
+    constexpr int H = L::H, W = L::W, HW = H * W, HR = L::HR, WR = L::WR;
+    constexpr int NCW = (C + 31) / 32;
+    static_assert(KP == 2 && M % 4 == 0 && L::MP == M, "2x2 pooling, 4 maps per vector load");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (warp >= cnt * NCW) return;
+    const int cw = warp % NCW, g = warp / NCW;
+    const int n = cw * 32 + lane;
+    const bool act = n < C;
+    const float* wn = wsm + (act ? n : 0) * KK * L::MP;
+    const float* dpg = dp + g * L::OUT_SZ;
+    const uint8_t* amg = am + g * L::OUT_SZ;
+    float acc[HR][WR];
+#pragma unroll
+    for (int y = 0; y < HR; ++y)
+#pragma unroll
+        for (int x = 0; x < WR; ++x) acc[y][x] = 0.f;
+#pragma unroll 1
+    for (int m4 = 0; m4 < M; m4 += 4) {
+        float4 w4[KK];
+#pragma unroll
+        for (int tp = 0; tp < KK; ++tp) w4[tp] = *reinterpret_cast<const float4*>(wn + tp * L::MP + m4);
+#pragma unroll
+        for (int mm = 0; mm < 4; ++mm) {
+            const int m = m4 + mm;
+#pragma unroll
+            for (int w = 0; w < P; ++w) {
+                const int pr = w / PW, pc = w % PW;
+                const float d = dpg[m * P + w];
+                const int ph = amg[m * P + w];
+#pragma unroll
+                for (int aa = 0; aa < KP; ++aa)
+#pragma unroll
+                    for (int bb = 0; bb < KP; ++bb) {
+                        const float dq = (ph == aa * KP + bb) ? d : 0.f;
+#pragma unroll
+                        for (int i = 0; i < K; ++i)
+#pragma unroll
+                            for (int j = 0; j < K; ++j) {
+                                const float4 t = w4[i * K + j];
+                                const float wv = mm == 0 ? t.x : mm == 1 ? t.y : mm == 2 ? t.z : t.w;
+                                acc[pr * KP + aa + i][pc * KP + bb + j] =
+                                    fmaf(wv, dq, acc[pr * KP + aa + i][pc * KP + bb + j]);
+                            }
+                    }
+            }
+        }
+    }
+    if (act) {
+        const float* ib = in + g * L::IN_SZ + n * HW;
+        float* ob = out + g * L::IN_SZ + n * HW;
+#pragma unroll
+        for (int y = 0; y < H; ++y)
+#pragma unroll
+            for (int x = 0; x < W; ++x) {
+                const float v = ib[y * W + x];
+                ob[y * W + x] = (y < HR && x < WR ? acc[y < HR ? y : 0][x < WR ? x : 0] : 0.f) * (1.f - v * v);
+            }
+    }
+}
+
+// ------------------------------------------------------------------------------------
 // PHASE(fc_fwd2) fully connected forward, IN % 4 == 0: one warp per NR output rows, lanes
 // over 16-B column quads; every weight load of the NR rows is issued before the first FMA
 // (__ldcg: on-demand reads of the shared store from L2), activations are LDS.128 broadcasts
@@ -1817,8 +1893,12 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                     // weight gradient (issue-bound, published from registers) side by side
                     constexpr int DW = G * C3::NBAND * ((C3::C + 31) / 32);
                     static_assert(C3::PB > 0 && C3::NBAND == 1 && DW < NT / 32, "conv3 split");
-                    if (threadIdx.x < DW * 32)
-                        conv_din2<C3, NT>(wb, a3, am3, a2, sS, nullptr, cnt);
+                    if (threadIdx.x < DW * 32) {
+                        if constexpr (C3::DWIN)
+                            conv_din_win<C3, NT>(wb, a3, am3, a2, sS, cnt);
+                        else
+                            conv_din2<C3, NT>(wb, a3, am3, a2, sS, nullptr, cnt);
+                    }
                     conv_gw_win<C3, NT, MODE, C3::GWIN, DW, NT / 32 - DW>(a, slot, a2, a3, am3, O::c3w, cnt, sc);
                     __syncthreads();
                     PTIME(9);
