@@ -49,7 +49,7 @@ __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 // (image, window) sum in the weight gradient; RB input rows per band in delta_in.
 template <int C_, int H_, int W_, int M_, int K_, int KP_, int MT_, int TT_, int GS_, int RB_, int PB_ = 0,
           int NN_ = 0, int MS_ = 0, bool GWMMA_ = false, bool DIN3_ = false, int GWIN_ = 0,
-          bool DWIN_ = false>
+          bool DWIN_ = false, bool GW5_ = false>
 struct Conv {
     static constexpr int C = C_, H = H_, W = W_, M = M_, K = K_, KP = KP_;
     static constexpr int OH = H - K + 1, OW = W - K + 1;
@@ -80,6 +80,8 @@ struct Conv {
     static constexpr int GWIN = GWIN_;
     // dense branch-free per-window delta_in, whole map per lane (conv_din_win)
     static constexpr bool DWIN = DWIN_;
+    // weight gradient with the compact sliding-block loop (conv_gw5, uses MS)
+    static constexpr bool GW5 = GW5_;
     static_assert(M % MT == 0, "MT must divide M");
     static_assert(KK % TT == 0, "TT must divide K*K");
     static_assert(RB % KP == 0 || NB == 1, "bands must start on a window row");
@@ -897,6 +899,117 @@ __device__ __forceinline__ void conv_gw3(const KArgs& a, int slot, const float* 
 }
 
 // ------------------------------------------------------------------------------------
+// PHASE(conv_gw5) conv_gw3 with a compact loop body (KP == 2): the windows of a pooled row
+// are a runtime loop over a (KP+K-1)^2 register block that slides KP columns per window
+// (KP new columns loaded per step), so the unrolled code is one window x MS maps x 4 phases
+// and stays in the instruction cache.  Same mapping, order and publish as conv_gw3.
+// ------------------------------------------------------------------------------------
+template <class L, int NT, int MODE>
+__device__ __forceinline__ void conv_gw5(const KArgs& a, int slot, const float* __restrict__ in,
+                                         const float* __restrict__ dp, const uint8_t* __restrict__ am,
+                                         float* __restrict__ scr, int woff, int cnt, float sc) {
+    constexpr int K = L::K, KP = L::KP, KK = L::KK, PW = L::PW, PH = L::PH, P = L::P, M = L::M, C = L::C;
+    constexpr int W = L::W, HW = L::H * L::W, MS = L::MS, NSET = (M + MS - 1) / MS;
+    constexpr int NCW = (C + 31) / 32, BS = KP + K - 1;
+    constexpr int NW = NT / 32;
+    static_assert(KP == 2, "2x2 pooling");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int task = warp; task < NSET * NCW; task += NW) {
+        const int cw = task % NCW;
+        const int m0 = (task / NCW) * MS;
+        const int n = cw * 32 + lane;
+        const bool act = n < C;
+        float acc[MS][KK];
+        float accb[MS];
+#pragma unroll
+        for (int q = 0; q < MS; ++q) {
+            accb[q] = 0.f;
+#pragma unroll
+            for (int t = 0; t < KK; ++t) acc[q][t] = 0.f;
+        }
+#pragma unroll 1
+        for (int g = 0; g < cnt; ++g) {
+            const float* ing = in + g * L::IN_SZ + (act ? n : 0) * HW;
+            const float* dpg = dp + g * L::OUT_SZ;
+            const uint8_t* amg = am + g * L::OUT_SZ;
+#pragma unroll 1
+            for (int pr = 0; pr < PH; ++pr) {
+                const float* rowp = ing + pr * KP * W;
+                float blk[BS][BS];
+#pragma unroll
+                for (int r = 0; r < BS; ++r)
+#pragma unroll
+                    for (int c = 0; c < BS; ++c) blk[r][c] = rowp[r * W + c];
+#pragma unroll 1
+                for (int pc = 0; pc < PW; ++pc) {
+                    float dv[MS];
+                    int av[MS];
+#pragma unroll
+                    for (int q = 0; q < MS; ++q) {
+                        const bool vq = (MS * NSET == M) || m0 + q < M;
+                        const int o = (vq ? m0 + q : 0) * P + pr * PW + pc;
+                        dv[q] = vq ? dpg[o] : 0.f;
+                        av[q] = vq ? static_cast<int>(amg[o]) : -1;
+                    }
+                    // next block's new columns, loaded before the branches
+                    float nxt[BS][KP];
+                    const bool more = pc + 1 < PW;
+#pragma unroll
+                    for (int r = 0; r < BS; ++r)
+#pragma unroll
+                        for (int c = 0; c < KP; ++c) nxt[r][c] = more ? rowp[r * W + (pc + 1) * KP + (BS - KP) + c] : 0.f;
+#pragma unroll
+                    for (int q = 0; q < MS; ++q) {
+                        const float d = dv[q];
+                        const int arg = av[q];
+                        accb[q] += d;
+                        if (arg < 2) {  // warp-uniform two-level branch on the argmax phase
+                            if (arg == 0) {
+#pragma unroll
+                                for (int t = 0; t < KK; ++t) acc[q][t] = fmaf(d, blk[t / K][t % K], acc[q][t]);
+                            } else if (arg == 1) {
+#pragma unroll
+                                for (int t = 0; t < KK; ++t) acc[q][t] = fmaf(d, blk[t / K][1 + t % K], acc[q][t]);
+                            }
+                        } else {
+                            if (arg == 2) {
+#pragma unroll
+                                for (int t = 0; t < KK; ++t) acc[q][t] = fmaf(d, blk[1 + t / K][t % K], acc[q][t]);
+                            } else {
+#pragma unroll
+                                for (int t = 0; t < KK; ++t) acc[q][t] = fmaf(d, blk[1 + t / K][1 + t % K], acc[q][t]);
+                            }
+                        }
+                    }
+                    // slide KP columns
+#pragma unroll
+                    for (int r = 0; r < BS; ++r) {
+#pragma unroll
+                        for (int c = 0; c < BS - KP; ++c) blk[r][c] = blk[r][c + KP];
+#pragma unroll
+                        for (int c = 0; c < KP; ++c) blk[r][BS - KP + c] = nxt[r][c];
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < MS; ++q) {
+            if (act && (MS * NSET == M || m0 + q < M)) {
+#pragma unroll
+                for (int t = 0; t < KK; ++t) scr[(n * KK + t) * L::MP + m0 + q] = sc * acc[q][t];
+                if (n == 0) scr[L::WFL + m0 + q] = sc * accb[q];
+            }
+        }
+    }
+    if constexpr (L::MP > M) {  // padding columns of the block publish zeros
+        for (int e = threadIdx.x; e < (L::ROWS + 1) * (L::MP - M); e += NT)
+            scr[(e / (L::MP - M)) * L::MP + M + e % (L::MP - M)] = 0.f;
+    }
+    sync_for_async();
+    publish_bulk<MODE>(a, slot, woff, scr, L::BLK);
+}
+
+// ------------------------------------------------------------------------------------
 // PHASE(conv_din) partial derivatives of the previous layer:
 //   dout[g][n][y][x] = (1 - in^2) * sum_m sum_pp [tap in range] W[n][y-r][x-c][m] dp[g][m][pp]
 // One warp per (image g, band of RB input rows, 32 input maps); lanes over n.  The windows
@@ -1189,10 +1302,12 @@ __device__ __forceinline__ void fc_fwd(const float* __restrict__ Wg, const float
 // unrolled code is one window row (PW windows x 4 phases), so it stays in the instruction
 // cache.  The first window row's KP rows wait in `pend` for the previous band's hand-off.
 // ------------------------------------------------------------------------------------
-template <class L, int NT>
+template <class L, int NT, bool DEFER = false>
 __device__ __forceinline__ void conv_din3(const float* __restrict__ wsm, const float* __restrict__ dp,
                                           const uint8_t* __restrict__ am, const float* in, float* out,
                                           float* __restrict__ hand, int cnt) {
+    // DEFER: every write of `out` waits for the hand-off barrier (another phase running on other
+    // warps may still be reading `in`, which `out` aliases)
     constexpr int K = L::K, KP = L::KP, KK = L::KK, PW = L::PW, PH = L::PH, P = L::P, M = L::M, C = L::C;
     constexpr int H = L::H, W = L::W, HW = H * W, PB = L::PB, NBAND = L::NBAND, WR = L::WR;
     constexpr int R1 = KP + K - 1, OV = K - 1;
@@ -1212,6 +1327,9 @@ __device__ __forceinline__ void conv_din3(const float* __restrict__ wsm, const f
     const float* ib = in + g * L::IN_SZ + (act ? n : 0) * HW;
     float* ob = out + g * L::IN_SZ + (act ? n : 0) * HW;
     float acc[R1][WR], pend[KP][WR];
+    constexpr int NFIN = DEFER ? (PB > 1 ? PB - 1 : 1) : 1;
+    float fin[NFIN][KP][WR];  // DEFER: rows of window rows 1..PB-1, written after the barrier
+    static_assert(!DEFER || NBAND > 1, "DEFER needs the hand-off barrier");
 #pragma unroll
     for (int r = 0; r < R1; ++r)
 #pragma unroll
@@ -1299,6 +1417,14 @@ __device__ __forceinline__ void conv_din3(const float* __restrict__ wsm, const f
                 for (int r = 0; r < KP; ++r)
 #pragma unroll
                     for (int c = 0; c < WR; ++c) pend[r][c] = acc[r][c];
+            } else if constexpr (DEFER) {
+#pragma unroll
+                for (int f = 0; f < NFIN; ++f)
+                    if (f + 1 == wr)
+#pragma unroll
+                        for (int r = 0; r < KP; ++r)
+#pragma unroll
+                            for (int c = 0; c < WR; ++c) fin[f][r][c] = acc[r][c];
             } else if (act) {
 #pragma unroll
                 for (int r = 0; r < KP; ++r) {
@@ -1332,6 +1458,24 @@ __device__ __forceinline__ void conv_din3(const float* __restrict__ wsm, const f
             for (int r = 0; r < OV; ++r)
 #pragma unroll
                 for (int c = 0; c < WR; ++c) pend[r][c] += hb[(r * WR + c) * C];
+        }
+    }
+    if constexpr (DEFER) {
+        if (act) {
+#pragma unroll
+            for (int f = 0; f < NFIN; ++f) {
+                if (f + 1 < nwr) {
+#pragma unroll
+                    for (int r = 0; r < KP; ++r) {
+                        const int y = y0 + (f + 1) * KP + r;
+#pragma unroll
+                        for (int x = 0; x < W; ++x) {
+                            const float v = ib[y * W + x];
+                            ob[y * W + x] = (x < WR ? fin[f][r][x] : 0.f) * (1.f - v * v);
+                        }
+                    }
+                }
+            }
         }
     }
     if (act) {
@@ -1926,7 +2070,27 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 L1.issue(wb, P + O::c2w, C2::BLK);  // W2 again (pre-update snapshot for delta_in)
                 L1.wait();
                 PTIME(11);
-                if constexpr (C2::GWMMA)
+                if constexpr (C2::GWIN > 0) {
+                    // delta_in (din3: one warp per (image, band), latency-bound) and the dense
+                    // weight gradient (issue-bound, published from registers) side by side; the
+                    // delta_in writes over a1 wait for its hand-off barrier, by which time the
+                    // weight-gradient warps have finished reading a1
+                    constexpr int DW = G * C2::NBAND * ((C2::C + 31) / 32);
+                    static_assert(C2::DIN3 && C2::NBAND > 1 && DW < NT / 32, "conv2 split");
+                    static_assert(G * C2::HAND <= S::Z - S::A2, "conv2 hand-off must fit in the dead A2/A3/HH regions");
+                    if (threadIdx.x < DW * 32) {
+                        conv_din3<C2, NT, true>(wb, sS, am2, a1, a1, a2, cnt);
+                    } else {
+                        conv_gw_win<C2, NT, MODE, C2::GWIN, DW, NT / 32 - DW>(a, slot, a1, sS, am2, O::c2w, cnt, sc);
+                        __syncthreads();  // pairs with conv_din3's hand-off barrier
+                    }
+                    __syncthreads();
+                    PTIME(12);
+                    PTIME(13);
+                } else {
+                if constexpr (C2::GW5)
+                    conv_gw5<C2, NT, MODE>(a, slot, a1, sS, am2, wb + C2::BLK, O::c2w, cnt, sc);
+                else if constexpr (C2::GWMMA)
                     conv_gw_mma<C2, NT, MODE>(a, slot, a1, sS, am2, wb + C2::BLK, O::c2w, cnt, sc);
                 else if constexpr (C2::MS > 0)
                     conv_gw3<C2, NT, MODE>(a, slot, a1, sS, am2, wb + C2::BLK, O::c2w, cnt, sc);
@@ -1948,6 +2112,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 }
                 __syncthreads();
                 PTIME(13);
+                }
             } else if constexpr (NCONV == 2) {
                 // W2 is still staged from the forward pass at W2OFF
                 conv_gw<C2, NT, MODE, false>(a, slot, a1, a2, am2, nullptr, O::c2w, cnt, sc);
