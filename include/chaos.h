@@ -130,8 +130,8 @@ chaos_status chaos_compute_gradients(chaos_net* net, const float* d_images, cons
 chaos_status chaos_debug_claims(chaos_net* net, int32_t* host_counts, int64_t n);
 
 /* Profiling hook: per-phase clock64 cycles of the last hogwild epoch, summed over CTAs, into
- * host_cycles[0..n) (16 phases: claim, stage, conv1..3 fwd, fc fwd, loss, fc2 bwd, fc1 bwd,
- * conv3 din, conv3 gW, W2 load, conv2 gW, conv2 din, image reload, conv1 gW).  Only the
+ * host_cycles[0..n) (20 slots: claim, stage, conv1..3 fwd, fc2 fwd, loss, fc2 bwd, fc1 bwd,
+ * conv3 din, conv3 gW, W2 load, conv2 gW, conv2 din, image reload, conv1 gW, fc1 fwd, 3 spare).  Only the
  * instrumented build (libchaos_timing.so, -DCHAOS_TIMING) records them; the product build
  * returns CHAOS_E_UNSUPPORTED.  Synchronizing. */
 chaos_status chaos_debug_phase_times(chaos_net* net, uint64_t* host_cycles, int32_t n);

@@ -239,12 +239,13 @@ class Net:
         return out
 
     PHASES = ["claim", "stage", "conv1_fwd", "conv2_fwd", "conv3_fwd", "fc_fwd", "loss", "fc2_bwd", "fc1_bwd",
-              "conv3_din", "conv3_gw", "w2_load", "conv2_gw", "conv2_din", "img_reload", "conv1_gw"]
+              "conv3_din", "conv3_gw", "w2_load", "conv2_gw", "conv2_din", "img_reload", "conv1_gw",
+              "fc1_fwd", "p17", "p18", "p19"]
 
     def phase_times(self):
         """Per-phase clock64 cycles of the last hogwild epoch, summed over CTAs (timing build only)."""
-        out = (C.c_uint64 * 16)()
-        _check(lib().chaos_debug_phase_times(self._h, out, 16))
+        out = (C.c_uint64 * 20)()
+        _check(lib().chaos_debug_phase_times(self._h, out, 20))
         return dict(zip(self.PHASES, [int(x) for x in out]))
 
     def sync(self):

@@ -173,7 +173,7 @@ struct KArgs {
 // Phase timing (instrumented build only, -DCHAOS_TIMING): thread 0 adds the clock64 cycles
 // since the previous mark to slot k; marks sit right after block-wide barriers, so a slot
 // holds the wall time of the phase that ends there.
-constexpr int kPhases = 16;
+constexpr int kPhases = 20;
 #ifdef CHAOS_TIMING
 #define PTIME(k)                                                          \
     do {                                                                  \
@@ -1738,6 +1738,169 @@ __device__ __forceinline__ void fc_bwd2(const KArgs& a, int slot, int woff, int 
 }
 
 // ------------------------------------------------------------------------------------
+// PHASE(fc_fwd3) fully connected forward with the weights staged in shared memory: chunks of
+// RCH rows are TMA bulk-copied (cp.async.bulk) into two buffers, the copy of chunk c+2
+// overlapping the compute of chunk c+1; one warp per row, lanes over 16-B column quads.
+// ------------------------------------------------------------------------------------
+template <class F, int G, int NT, int RCH>
+__device__ __forceinline__ void fc_fwd3(const float* __restrict__ Wg, const float* __restrict__ bg,
+                                        const float* __restrict__ in, float* __restrict__ out, int ostride, int cnt,
+                                        float* __restrict__ buf, Loader& LA, Loader& LB, float* __restrict__ sb) {
+    // sb: F::OUT floats of shared scratch for the biases (loaded once, up front)
+    static_assert(F::IN % 4 == 0 && (RCH * F::IN) % 4 == 0, "16-B chunks");
+    constexpr int IN4 = F::IN / 4, NK = (IN4 + 31) / 32, NW = NT / 32;
+    constexpr int NCH = (F::OUT + RCH - 1) / RCH;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    auto rows = [](int c) { return (c + 1) * RCH <= F::OUT ? RCH : F::OUT - c * RCH; };
+    LA.issue(buf, Wg, rows(0) * F::IN);
+    if (NCH > 1) LB.issue(buf + RCH * F::IN, Wg + RCH * F::IN, rows(1) * F::IN);
+    for (int o = threadIdx.x; o < F::OUT; o += NT) sb[o] = __ldcg(bg + o);
+    __syncthreads();
+    for (int c = 0; c < NCH; ++c) {
+        const float* cb = buf + (c & 1) * RCH * F::IN;
+        if (c & 1)
+            LB.wait();
+        else
+            LA.wait();
+        for (int r = warp; r < rows(c); r += NW) {
+            const int o = c * RCH + r;
+            float acc[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) acc[g] = 0.f;
+#pragma unroll
+            for (int k = 0; k < NK; ++k) {
+                const int q = lane + 32 * k;
+                if (q < IN4) {
+                    const float4 w = reinterpret_cast<const float4*>(cb + r * F::IN)[q];
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        const float4 x = reinterpret_cast<const float4*>(in + g * F::IN)[q];
+                        acc[g] = fmaf(w.x, x.x, acc[g]);
+                        acc[g] = fmaf(w.y, x.y, acc[g]);
+                        acc[g] = fmaf(w.z, x.z, acc[g]);
+                        acc[g] = fmaf(w.w, x.w, acc[g]);
+                    }
+                }
+            }
+            const float b = sb[o];
+            // reduce the G partial sums; lane g finishes image g (tanh spread over lanes)
+            float mine = 0.f;
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const float s = warp_sum(acc[g]) + b;
+                if (lane == g) mine = s;
+            }
+            if (lane < cnt) out[lane * ostride + o] = F::TANH ? tanhf(mine) : mine;
+        }
+        if (c + 2 < NCH) {
+            sync_for_async();  // every warp is done reading this buffer
+            if (c & 1)
+                LB.issue(buf + RCH * F::IN, Wg + (c + 2) * RCH * F::IN, rows(c + 2) * F::IN);
+            else
+                LA.issue(buf, Wg + (c + 2) * RCH * F::IN, rows(c + 2) * F::IN);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// PHASE(fc_bwd3) fc_bwd2 with the weights staged chunk by chunk in shared memory (as in
+// fc_fwd3).  Thread item = (16-B column quad, row group); within a chunk the row group takes
+// every NRG-th row.  W is the pre-update snapshot: this CTA publishes gW[o][4c..] only after
+// its thread read W[o][4c..] from the chunk (the chunk was copied before any publish of it).
+// ------------------------------------------------------------------------------------
+template <class F, int G, int NT, int MODE, int NRG, int RCH>
+__device__ __forceinline__ void fc_bwd3(const KArgs& a, int slot, int woff, int boff, float* __restrict__ in,
+                                        const float* __restrict__ dz, int dstride, float* __restrict__ scr,
+                                        float* __restrict__ bsc, int cnt, float sc, float* __restrict__ buf,
+                                        Loader& LA, Loader& LB) {
+    static_assert(F::IN % 4 == 0 && (RCH * F::IN) % 4 == 0, "16-B chunks");
+    constexpr int IN4 = F::IN / 4;
+    constexpr int NCH = (F::OUT + RCH - 1) / RCH;
+    static_assert(IN4 * NRG <= NT, "one thread per (column quad, row group)");
+    const float* Wg = a.params + woff;
+    auto rows = [](int c) { return (c + 1) * RCH <= F::OUT ? RCH : F::OUT - c * RCH; };
+    LA.issue(buf, Wg, rows(0) * F::IN);
+    if (NCH > 1) LB.issue(buf + RCH * F::IN, Wg + RCH * F::IN, rows(1) * F::IN);
+    const int c4 = threadIdx.x % IN4;
+    const int rg = threadIdx.x / IN4;
+    const bool act = threadIdx.x < IN4 * NRG;
+    float4 av[G], din[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        av[g] = (act && g < cnt) ? reinterpret_cast<const float4*>(in + g * F::IN)[c4] : make_float4(0.f, 0.f, 0.f, 0.f);
+        din[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (int c = 0; c < NCH; ++c) {
+        const float* cb = buf + (c & 1) * RCH * F::IN;
+        if (c & 1)
+            LB.wait();
+        else
+            LA.wait();
+        if (act) {
+            for (int r = rg; r < rows(c); r += NRG) {
+                const int o = c * RCH + r;
+                const float4 w = reinterpret_cast<const float4*>(cb + r * F::IN)[c4];
+                float4 gw = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    if (g < cnt) {
+                        const float d = dz[g * dstride + o];
+                        din[g].x = fmaf(w.x, d, din[g].x);
+                        din[g].y = fmaf(w.y, d, din[g].y);
+                        din[g].z = fmaf(w.z, d, din[g].z);
+                        din[g].w = fmaf(w.w, d, din[g].w);
+                        gw.x = fmaf(d, av[g].x, gw.x);
+                        gw.y = fmaf(d, av[g].y, gw.y);
+                        gw.z = fmaf(d, av[g].z, gw.z);
+                        gw.w = fmaf(d, av[g].w, gw.w);
+                    }
+                }
+                publish_vec4<MODE>(a, slot, woff + o * F::IN + 4 * c4,
+                                   make_float4(sc * gw.x, sc * gw.y, sc * gw.z, sc * gw.w));
+            }
+        }
+        if (c + 2 < NCH) {
+            sync_for_async();
+            if (c & 1)
+                LB.issue(buf + RCH * F::IN, Wg + (c + 2) * RCH * F::IN, rows(c + 2) * F::IN);
+            else
+                LA.issue(buf, Wg + (c + 2) * RCH * F::IN, rows(c + 2) * F::IN);
+        }
+    }
+    if (act && rg > 0)
+#pragma unroll
+        for (int g = 0; g < G; ++g) reinterpret_cast<float4*>(scr + ((rg - 1) * G + g) * F::IN)[c4] = din[g];
+    for (int o = threadIdx.x; o < F::BFL; o += NT) {  // bias
+        float gb = 0.f;
+        if (o < F::OUT)
+            for (int g = 0; g < cnt; ++g) gb += dz[g * dstride + o];
+        bsc[o] = sc * gb;
+    }
+    sync_for_async();
+    publish_bulk<MODE>(a, slot, boff, bsc, F::BFL);
+    if (act && rg == 0) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            if (g < cnt) {
+                float4 t = din[g];
+#pragma unroll
+                for (int k = 1; k < NRG; ++k) {
+                    const float4 p = reinterpret_cast<const float4*>(scr + ((k - 1) * G + g) * F::IN)[c4];
+                    t.x += p.x;
+                    t.y += p.y;
+                    t.z += p.z;
+                    t.w += p.w;
+                }
+                const float4 x = av[g];
+                reinterpret_cast<float4*>(in + g * F::IN)[c4] =
+                    make_float4(t.x * (1.f - x.x * x.x), t.y * (1.f - x.y * x.y), t.z * (1.f - x.z * x.z),
+                                t.w * (1.f - x.w * x.w));
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
 // PHASE(fc_bwd) fully connected backward: one thread per input column i, outputs o in
 // chunks.  Reads W[o][i] (pre-update, on demand) for delta_in; gW[o][i] = sum_g dz[g][o] a[g][i]
 // goes (scaled) into a shared-memory chunk that is published with one bulk op while the
@@ -1846,6 +2009,11 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
     constexpr int W2OFF = (NCONV >= 2) ? S::WBUF - C2::BLK : 0;
     constexpr int W3A = (NCONV >= 3) ? (C3::C / 2) * C3::KK * C3::MP : 0;
     static_assert(NCONV < 3 || W3A <= W2OFF, "W3 first half must not overlap W2");
+    // FC1 weights staged through WB in two chunks of FRCH rows (large net: WB is free between
+    // the conv3 forward and the conv3 backward, which re-fetches W3)
+    constexpr bool FCSTAGE = (NCONV == 3) && (NFULL == 2) && (F1::IN % 4 == 0);
+    constexpr int FRCH = FCSTAGE ? (S::WBUF / (2 * F1::IN)) : 1;
+    static_assert(!FCSTAGE || FRCH >= 1, "FC1 chunk must hold a row");
     static_assert(NCONV < 2 || C1::BLK <= W2OFF, "W1 and W2 must not overlap");
     static_assert(NCONV < 2 || C2::PB == 0 || G * C2::NBAND * ((C2::C + 31) / 32) <= NT / 32,
                   "conv_din2 needs one warp per (image, band, 32 maps)");
@@ -1853,10 +2021,10 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                   "conv_din2 needs one warp per (image, band, 32 maps)");
 
     extern __shared__ __align__(128) unsigned char smem[];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // 4 mbarriers
-    int* s_base = reinterpret_cast<int*>(smem + 32);
-    int* s_lab = reinterpret_cast<int*>(smem + 48);                // G labels (<= 16)
-    float* s_loss = reinterpret_cast<float*>(smem + 48 + 4 * 16);  // G losses
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // 6 mbarriers
+    int* s_base = reinterpret_cast<int*>(smem + 64);
+    int* s_lab = reinterpret_cast<int*>(smem + 80);                // G labels (<= 16)
+    float* s_loss = reinterpret_cast<float*>(smem + 80 + 4 * 16);  // G losses
     float* fa = reinterpret_cast<float*>(smem + kHdrBytes);
     float* sS = fa + S::S;
     float* a1 = fa + S::A1;
@@ -1878,11 +2046,14 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
     (void)am3;
 
     if (threadIdx.x == 0) {
-        for (int k = 0; k < 4; ++k) mbar_init(bars + k, 1);
+        for (int k = 0; k < 6; ++k) mbar_init(bars + k, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     Loader L0{bars + 0, 0u}, L1{bars + 1, 0u}, L2{bars + 2, 0u}, L3{bars + 3, 0u};
+    Loader L4{bars + 4, 0u}, L5{bars + 5, 0u};  // FC1 weight chunks (double buffer)
+    (void)L4;
+    (void)L5;
 
     long long iter = 0;
     long long t_last = clock64();
@@ -1959,15 +2130,19 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             conv_fwd<C3, NT>(a2, wb, a3, am3, cnt);
             alast = a3;
         }
+        fence_proxy_async();  // WB (read by the conv forward) is refilled by the async proxy next
         __syncthreads();
         PTIME(4);
         // ---------------- a3: full layers
         if constexpr (NFULL == 2) {
-            if constexpr (F1::IN % 4 == 0)
+            if constexpr (FCSTAGE)
+                fc_fwd3<F1, G, NT, FRCH>(P + O::f1w, P + O::f1b, alast, hh, F1::OUT, cnt, wb, L4, L5, sS);
+            else if constexpr (F1::IN % 4 == 0)
                 fc_fwd2<F1, G, NT, (NT > 512 ? 2 : 4)>(P + O::f1w, P + O::f1b, alast, hh, F1::OUT, cnt);
             else
                 fc_fwd<F1, G, NT>(P + O::f1w, P + O::f1b, alast, hh, F1::OUT, cnt);
             __syncthreads();
+            PTIME(16);
             fc_fwd<F2, G, NT>(P + O::f2w, P + O::f2b, hh, zz, kZStride, cnt);
         } else {
             fc_fwd<F1, G, NT>(P + O::f1w, P + O::f1b, alast, zz, kZStride, cnt);
@@ -2017,7 +2192,14 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 fc_bwd<F2, G, NT, MODE, SHALF>(a, slot, O::f2w, O::f2b, hh, zz, kZStride, sS, bsc, cnt, sc);
                 wait_publish_reads();
                 PTIME(7);
-                if constexpr (F1::IN % 4 == 0 && (F1::IN / 4) * 4 <= NT) {
+                if constexpr (FCSTAGE) {
+                    constexpr int NRG = NT / (F1::IN / 4) < 4 ? NT / (F1::IN / 4) : 4;
+                    static_assert((NRG - 1) * G * F1::IN <= S::SFL, "row-group partials must fit in S");
+                    fence_proxy_async();
+                    wait_publish_reads();  // the FC2 publish has read its buffers; WB is free
+                    fc_bwd3<F1, G, NT, MODE, NRG, FRCH>(a, slot, O::f1w, O::f1b, alast, hh, F1::OUT, sS, bsc, cnt,
+                                                         sc, wb, L4, L5);
+                } else if constexpr (F1::IN % 4 == 0 && (F1::IN / 4) * 4 <= NT) {
                     constexpr int NRG = NT / (F1::IN / 4) < 4 ? NT / (F1::IN / 4) : 4;
                     static_assert((NRG - 1) * G * F1::IN <= S::SFL, "row-group partials must fit in S");
                     fc_bwd2<F1, G, NT, MODE, NRG>(a, slot, O::f1w, O::f1b, alast, hh, F1::OUT, sS, bsc, cnt, sc);
@@ -2031,7 +2213,15 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             PTIME(8);
             // ---------------- a6/a7: pool + conv backward, publish per layer
             if constexpr (NCONV == 3) {
-                // W3 is still staged from the forward pass (the exact snapshot it used)
+                if constexpr (FCSTAGE) {
+                    // W3 again (the FC1 chunks used its buffer); this worker has not published
+                    // layer 3 yet, so for one worker it is the snapshot the forward used (R5)
+                    fence_proxy_async();
+                    __syncthreads();
+                    L2.issue(wb, P + O::c3w, C3::BLK);
+                    L2.wait();
+                }
+                // otherwise W3 is still staged from the forward pass (the exact snapshot it used)
                 if constexpr (C3::GWIN > 0) {
                     // delta_in (latency-bound, one warp per (image, 32 maps)) and the dense
                     // weight gradient (issue-bound, published from registers) side by side
