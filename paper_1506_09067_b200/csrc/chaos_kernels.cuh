@@ -320,7 +320,8 @@ __device__ __forceinline__ void publish_vec4(const KArgs& a, int slot, int idx, 
         *reinterpret_cast<float4*>(a.partial + static_cast<long long>(slot) * a.pstride + idx) = g_scaled;
 }
 
-template <int N, bool A4>
+// A4: p is 16-B aligned; A2: p is 8-B aligned
+template <int N, bool A4, bool A2 = false>
 __device__ __forceinline__ void load_vec(float (&v)[N], const float* p) {
     if constexpr (A4 && N % 4 == 0) {
 #pragma unroll
@@ -339,6 +340,13 @@ __device__ __forceinline__ void load_vec(float (&v)[N], const float* p) {
         v[3] = t.w;
 #pragma unroll
         for (int q = 4; q < N; ++q) v[q] = p[q];
+    } else if constexpr (A2 && N % 2 == 0) {
+#pragma unroll
+        for (int q = 0; q < N / 2; ++q) {
+            const float2 t = *reinterpret_cast<const float2*>(p + 2 * q);
+            v[2 * q] = t.x;
+            v[2 * q + 1] = t.y;
+        }
     } else {
 #pragma unroll
         for (int q = 0; q < N; ++q) v[q] = p[q];
@@ -391,6 +399,7 @@ __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const flo
     constexpr int MT = L::MT, KP = L::KP, K = L::K, PW = L::PW, P = L::P, MG = L::M / MT;
     constexpr int PS = KP + K - 1;
     constexpr bool A4 = (MT % 4 == 0) || (MG == 1);
+    constexpr bool A2 = (MT % 2 == 0);  // row pitch MP is a multiple of 4, so mg*MT is even
     const int total = MG * cnt * P;
     for (int it = threadIdx.x; it < total; it += NT) {
         const int p = it % P;
@@ -401,7 +410,7 @@ __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const flo
         float acc[MT][KP * KP];
         {
             float b[MT];
-            load_vec<MT, A4>(b, wsm + L::WFL + mg * MT);
+            load_vec<MT, A4, A2>(b, wsm + L::WFL + mg * MT);
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -421,7 +430,7 @@ __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const flo
 #pragma unroll
                 for (int j = 0; j < K; ++j) {
                     float wv[MT];
-                    load_vec<MT, A4>(wv, wb + ((n * K + i) * K + j) * L::MP);
+                    load_vec<MT, A4, A2>(wv, wb + ((n * K + i) * K + j) * L::MP);
 #pragma unroll
                     for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -2112,7 +2121,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
         conv_fwd<C1, NT>(sS, wb, a1, am1, cnt);
         float* alast = a1;
         if constexpr (NCONV >= 2) {
-            fence_proxy_async();
+            fence_async_smem();
             __syncthreads();
             PTIME(2);
             if constexpr (NCONV >= 3) L2.issue(wb, P + O::c3w, W3A);  // W1 region is dead: W3's first half
@@ -2121,7 +2130,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             alast = a2;
         }
         if constexpr (NCONV >= 3) {
-            fence_proxy_async();
+            fence_async_smem();
             __syncthreads();
             PTIME(3);
             L3.issue(wb + W3A, P + O::c3w + W3A, C3::BLK - W3A);
@@ -2130,7 +2139,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             conv_fwd<C3, NT>(a2, wb, a3, am3, cnt);
             alast = a3;
         }
-        fence_proxy_async();  // WB (read by the conv forward) is refilled by the async proxy next
+        fence_async_smem();  // WB (read by the conv forward) is refilled by the async proxy next
         __syncthreads();
         PTIME(4);
         // ---------------- a3: full layers
@@ -2195,7 +2204,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 if constexpr (FCSTAGE) {
                     constexpr int NRG = NT / (F1::IN / 4) < 4 ? NT / (F1::IN / 4) : 4;
                     static_assert((NRG - 1) * G * F1::IN <= S::SFL, "row-group partials must fit in S");
-                    fence_proxy_async();
+                    fence_async_smem();
                     wait_publish_reads();  // the FC2 publish has read its buffers; WB is free
                     fc_bwd3<F1, G, NT, MODE, NRG, FRCH>(a, slot, O::f1w, O::f1b, alast, hh, F1::OUT, sS, bsc, cnt,
                                                          sc, wb, L4, L5);
@@ -2216,7 +2225,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 if constexpr (FCSTAGE) {
                     // W3 again (the FC1 chunks used its buffer); this worker has not published
                     // layer 3 yet, so for one worker it is the snapshot the forward used (R5)
-                    fence_proxy_async();
+                    fence_async_smem();
                     __syncthreads();
                     L2.issue(wb, P + O::c3w, C3::BLK);
                     L2.wait();
@@ -2254,7 +2263,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 else
                     conv_gw<C3, NT, MODE, true>(a, slot, a2, a3, am3, wb, O::c3w, cnt, sc);
                 }
-                fence_proxy_async();
+                fence_async_smem();
                 wait_publish_reads();
                 PTIME(10);
                 L1.issue(wb, P + O::c2w, C2::BLK);  // W2 again (pre-update snapshot for delta_in)
@@ -2311,7 +2320,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 __syncthreads();
             }
             // conv1: the images again (S was reused as scratch), then its gradient
-            fence_proxy_async();
+            fence_async_smem();
             wait_publish_reads();
             if (x_bulk) {
                 L0.issue(sS, xsrc, cnt * IMG);
