@@ -1771,35 +1771,51 @@ __device__ __forceinline__ void fc_fwd3(const float* __restrict__ Wg, const floa
             LB.wait();
         else
             LA.wait();
-        for (int r = warp; r < rows(c); r += NW) {
-            const int o = c * RCH + r;
-            float acc[G];
+        // RPW rows per warp pass: each activation quad loaded from shared memory feeds RPW rows
+        constexpr int RPW = 2;
+        for (int r0 = warp * RPW; r0 < rows(c); r0 += NW * RPW) {
+            float acc[RPW][G];
 #pragma unroll
-            for (int g = 0; g < G; ++g) acc[g] = 0.f;
+            for (int rr = 0; rr < RPW; ++rr)
+#pragma unroll
+                for (int g = 0; g < G; ++g) acc[rr][g] = 0.f;
 #pragma unroll
             for (int k = 0; k < NK; ++k) {
                 const int q = lane + 32 * k;
                 if (q < IN4) {
-                    const float4 w = reinterpret_cast<const float4*>(cb + r * F::IN)[q];
+                    float4 x[G];
 #pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        const float4 x = reinterpret_cast<const float4*>(in + g * F::IN)[q];
-                        acc[g] = fmaf(w.x, x.x, acc[g]);
-                        acc[g] = fmaf(w.y, x.y, acc[g]);
-                        acc[g] = fmaf(w.z, x.z, acc[g]);
-                        acc[g] = fmaf(w.w, x.w, acc[g]);
+                    for (int g = 0; g < G; ++g) x[g] = reinterpret_cast<const float4*>(in + g * F::IN)[q];
+#pragma unroll
+                    for (int rr = 0; rr < RPW; ++rr) {
+                        if (r0 + rr < rows(c)) {
+                            const float4 w = reinterpret_cast<const float4*>(cb + (r0 + rr) * F::IN)[q];
+#pragma unroll
+                            for (int g = 0; g < G; ++g) {
+                                acc[rr][g] = fmaf(w.x, x[g].x, acc[rr][g]);
+                                acc[rr][g] = fmaf(w.y, x[g].y, acc[rr][g]);
+                                acc[rr][g] = fmaf(w.z, x[g].z, acc[rr][g]);
+                                acc[rr][g] = fmaf(w.w, x[g].w, acc[rr][g]);
+                            }
+                        }
                     }
                 }
             }
-            const float b = sb[o];
-            // reduce the G partial sums; lane g finishes image g (tanh spread over lanes)
-            float mine = 0.f;
 #pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const float s = warp_sum(acc[g]) + b;
-                if (lane == g) mine = s;
+            for (int rr = 0; rr < RPW; ++rr) {
+                if (r0 + rr < rows(c)) {
+                    const int o = c * RCH + r0 + rr;
+                    const float b = sb[o];
+                    // reduce the G partial sums; lane g finishes image g (tanh spread over lanes)
+                    float mine = 0.f;
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        const float s = warp_sum(acc[rr][g]) + b;
+                        if (lane == g) mine = s;
+                    }
+                    if (lane < cnt) out[lane * ostride + o] = F::TANH ? tanhf(mine) : mine;
+                }
             }
-            if (lane < cnt) out[lane * ostride + o] = F::TANH ? tanhf(mine) : mine;
         }
         if (c + 2 < NCH) {
             sync_for_async();  // every warp is done reading this buffer
