@@ -46,7 +46,13 @@ struct LargeNet {  // configs[3], configs[4]
     // 20 warps (<= 96 registers): one warp per (image, window row) in conv2's delta_in and per
     // (3 maps, 32 input maps) in its weight gradient; see profiles/r1q (640-thread tile sweep)
     static constexpr int NCONV = 3, NFULL = 2, GDEF = 4, GINIT = 4, INFLIGHT = 592, NT = 640, SFL = 6000;
-    using C1 = Conv<1, 29, 29, 20, 4, 2, 10, 16, 16, 2>;
+#ifndef C1MT
+#define C1MT 10
+#endif
+#ifndef C1GS
+#define C1GS 16
+#endif
+    using C1 = Conv<1, 29, 29, 20, 4, 2, C1MT, 16, C1GS, 2>;
     using C2 = Conv<20, 13, 13, 60, 3, 2, 10, 9, 1, 4, /*PB*/ 1, /*NN*/ 2, /*MS*/ 3, /*GWMMA*/ false, /*DIN3*/ true,
                     /*GWIN*/ 0, /*DWIN*/ false, /*GW5*/ false>;
     using C3 = Conv<60, 5, 5, 100, 2, 2, 4, 4, 1, 5, /*PB*/ 2, /*NN*/ 4, /*MS*/ 13, /*GWMMA*/ false, /*DIN3*/ false, /*GWIN*/ 4, /*DWIN*/ true>;
