@@ -49,7 +49,7 @@ __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 // (image, window) sum in the weight gradient; RB input rows per band in delta_in.
 template <int C_, int H_, int W_, int M_, int K_, int KP_, int MT_, int TT_, int GS_, int RB_, int PB_ = 0,
           int NN_ = 0, int MS_ = 0, bool GWMMA_ = false, bool DIN3_ = false, int GWIN_ = 0,
-          bool DWIN_ = false, bool GW5_ = false>
+          bool DWIN_ = false, bool GW5_ = false, int NSPL_ = 1>
 struct Conv {
     static constexpr int C = C_, H = H_, W = W_, M = M_, K = K_, KP = KP_;
     static constexpr int OH = H - K + 1, OW = W - K + 1;
@@ -82,6 +82,10 @@ struct Conv {
     static constexpr bool DWIN = DWIN_;
     // weight gradient with the compact sliding-block loop (conv_gw5, uses MS)
     static constexpr bool GW5 = GW5_;
+    // forward: the input maps of one item split over NSPL adjacent lanes (partial sums combined
+    // with shfl_xor) -- more items for small layers
+    static constexpr int NSPL = NSPL_;
+    static_assert(NSPL == 1 || (NSPL == 2 && C % 2 == 0), "NSPL 1 or 2");
     static_assert(M % MT == 0, "MT must divide M");
     static_assert(KK % TT == 0, "TT must divide K*K");
     static_assert(RB % KP == 0 || NB == 1, "bands must start on a window row");
@@ -400,10 +404,13 @@ __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const flo
     constexpr int PS = KP + K - 1;
     constexpr bool A4 = (MT % 4 == 0) || (MG == 1);
     constexpr bool A2 = (MT % 2 == 0);  // row pitch MP is a multiple of 4, so mg*MT is even
-    const int total = MG * cnt * P;
+    constexpr int NSPL = L::NSPL, CH = L::C / NSPL;
+    static_assert(NT % 32 == 0, "lane pairs never straddle warps");
+    const int total = MG * cnt * P * NSPL;
     for (int it = threadIdx.x; it < total; it += NT) {
-        const int p = it % P;
-        const int t = it / P;
+        const int half = it % NSPL;
+        const int p = (it / NSPL) % P;
+        const int t = (it / NSPL) / P;
         const int g = t % cnt;
         const int mg = t / cnt;
         const int pr = p / PW, pc = p - (p / PW) * PW;
@@ -414,12 +421,12 @@ __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const flo
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-                for (int q = 0; q < KP * KP; ++q) acc[mt][q] = b[mt];
+                for (int q = 0; q < KP * KP; ++q) acc[mt][q] = half == 0 ? b[mt] : 0.f;
         }
         const float* ib = in + g * L::IN_SZ + (pr * KP) * L::W + pc * KP;
         const float* wb = wsm + mg * MT;
 #pragma unroll 1
-        for (int n = 0; n < L::C; ++n) {
+        for (int n = half * CH; n < (half + 1) * CH; ++n) {
             float patch[PS][PS];
 #pragma unroll
             for (int u = 0; u < PS; ++u)
@@ -439,6 +446,14 @@ __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const flo
                             for (int v = 0; v < KP; ++v)
                                 acc[mt][u * KP + v] = fmaf(wv[mt], patch[u + i][v + j], acc[mt][u * KP + v]);
                 }
+        }
+        if constexpr (NSPL == 2) {  // the two halves of an item sit in adjacent lanes
+            const unsigned mask = __activemask();
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                for (int q = 0; q < KP * KP; ++q) acc[mt][q] += __shfl_xor_sync(mask, acc[mt][q], 1);
+            if (half != 0) continue;
         }
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {

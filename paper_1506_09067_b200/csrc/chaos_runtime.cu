@@ -55,7 +55,8 @@ struct LargeNet {  // configs[3], configs[4]
     using C1 = Conv<1, 29, 29, 20, 4, 2, C1MT, 16, C1GS, 2>;
     using C2 = Conv<20, 13, 13, 60, 3, 2, 10, 9, 1, 4, /*PB*/ 1, /*NN*/ 2, /*MS*/ 3, /*GWMMA*/ false, /*DIN3*/ true,
                     /*GWIN*/ 0, /*DWIN*/ false, /*GW5*/ false>;
-    using C3 = Conv<60, 5, 5, 100, 2, 2, 4, 4, 1, 5, /*PB*/ 2, /*NN*/ 4, /*MS*/ 13, /*GWMMA*/ false, /*DIN3*/ false, /*GWIN*/ 4, /*DWIN*/ true>;
+    using C3 = Conv<60, 5, 5, 100, 2, 2, /*MT*/ 4, 4, 1, 5, /*PB*/ 2, /*NN*/ 4, /*MS*/ 13, /*GWMMA*/ false, /*DIN3*/ false,
+                    /*GWIN*/ 4, /*DWIN*/ true, /*GW5*/ false, /*NSPL*/ 1>;
     using F1 = Full<400, 150, true>;
     using F2 = Full<150, 10, false>;
 };
