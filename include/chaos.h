@@ -125,6 +125,20 @@ chaos_status chaos_forward(chaos_net* net, const float* d_images, int64_t n, flo
  * layout, no update; fixed-order sum).  Synchronizing. */
 chaos_status chaos_compute_gradients(chaos_net* net, const float* d_images, const int32_t* d_labels, int64_t n,
                                      float* host_grad_sum);
+/* Deterministic multi-GPU sync mode (BASELINE.json north_star "sums a fixed
+ * batch's gradients in a fixed order before one update"), in two steps so a collective can sit in
+ * between.  chaos_batch_gradient: d_grad[j] = sum_i dL_i/dparam_j over images [0, n) at the current
+ * weights (every g_i at the same weights; slot-ordered, fixed-order sum), in the INTERNAL layout
+ * (chaos_net_device_params_len floats; padding entries are written 0).  d_grad is caller-owned
+ * device memory; asynchronous on the net's stream; n == 0 writes zeros.  Device-detected label /
+ * non-finite errors are latched as for chaos_train_epoch.
+ * chaos_apply_gradient: param[j] -= lr * d_grad[j] over the internal layout (one rounding, the same
+ * expression as the single-GPU sync update, so batch_gradient + apply_gradient on one GPU reproduce
+ * chaos_train_epoch(SYNC) bitwise).  Asynchronous on the net's stream. */
+chaos_status chaos_batch_gradient(chaos_net* net, const float* d_images, const int32_t* d_labels, int64_t n,
+                                  float* d_grad);
+chaos_status chaos_apply_gradient(chaos_net* net, const float* d_grad, float lr);
+
 /* Debug: copies the per-image claim counts of the last hogwild epoch (needs
  * CHAOS_OPT_DEBUG_CLAIMS=1 before the epoch) into host_counts[n]. */
 chaos_status chaos_debug_claims(chaos_net* net, int32_t* host_counts, int64_t n);

@@ -28,7 +28,8 @@ EXPORTS = ["chaos_net_create", "chaos_net_destroy", "chaos_net_set_option", "cha
            "chaos_net_num_params", "chaos_net_get_params", "chaos_net_set_params", "chaos_net_device_params",
            "chaos_net_device_params_len", "chaos_train_epoch", "chaos_train_epoch_host", "chaos_last_train_loss",
            "chaos_evaluate", "chaos_forward", "chaos_compute_gradients", "chaos_debug_claims", "chaos_net_sync",
-           "chaos_net_launch_info", "chaos_last_error", "chaos_last_status", "chaos_debug_phase_times"]
+           "chaos_net_launch_info", "chaos_last_error", "chaos_last_status", "chaos_debug_phase_times",
+           "chaos_batch_gradient", "chaos_apply_gradient"]
 
 
 class ChaosError(RuntimeError):
@@ -74,6 +75,8 @@ def lib():
             "chaos_forward": ([vp, vp, C.c_int64, vp], C.c_int),
             "chaos_compute_gradients": ([vp, vp, vp, C.c_int64, fp], C.c_int),
             "chaos_debug_claims": ([vp, ip, C.c_int64], C.c_int),
+            "chaos_batch_gradient": ([vp, vp, vp, C.c_int64, vp], C.c_int),
+            "chaos_apply_gradient": ([vp, vp, C.c_float], C.c_int),
             "chaos_net_sync": ([vp], C.c_int),
             "chaos_net_launch_info": ([vp, ip, ip, ip, ip], C.c_int),
             "chaos_last_error": ([], C.c_char_p),
@@ -232,6 +235,21 @@ class Net:
         else:
             _check(lib().chaos_compute_gradients(self._h, _ptr(images), _ptr(labels), n, gp))
         return g
+
+    def batch_gradient(self, images, labels, grad):
+        """chaos_batch_gradient: grad (CUDA float32, device_params().numel()) = sum of the images'
+        gradients at the current weights, internal layout; asynchronous on the net's stream."""
+        n = int(labels.shape[0])
+        if grad.numel() != int(lib().chaos_net_device_params_len(self._h)) or grad.dtype.itemsize != 4:
+            raise ValueError("grad must hold chaos_net_device_params_len float32 values")
+        if n == 0:
+            _check(lib().chaos_batch_gradient(self._h, None, None, 0, _ptr(grad)))
+        else:
+            _check(lib().chaos_batch_gradient(self._h, _ptr(images), _ptr(labels), n, _ptr(grad)))
+
+    def apply_gradient(self, grad, lr):
+        """chaos_apply_gradient: params -= lr * grad (internal layout); asynchronous."""
+        _check(lib().chaos_apply_gradient(self._h, _ptr(grad), float(lr)))
 
     def debug_claims(self, n):
         out = np.zeros(n, np.int32)

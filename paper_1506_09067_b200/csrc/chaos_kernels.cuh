@@ -2384,7 +2384,15 @@ __global__ void chaos_reduce_update(float* __restrict__ params, const float* __r
     if (out)
         out[j] = s;
     else
-        params[j] -= lr * s;
+        params[j] = fmaf(-lr, s, params[j]);
+}
+
+// w[j] -= lr * grad[j] (the sync update from an externally reduced gradient: multi-GPU sync).
+// Same single-rounding expression as chaos_reduce_update, so one GPU reproduces it bitwise.
+__global__ void chaos_apply_gradient_kernel(float* __restrict__ params, const float* __restrict__ grad, float lr,
+                                            long long np) {
+    const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j < np) params[j] = fmaf(-lr, grad[j], params[j]);
 }
 
 // Fixed-order evaluation reduction: one CTA of 1024 threads.

@@ -723,6 +723,27 @@ chaos_status chaos_compute_gradients(chaos_net* net, const float* d_images, cons
     return check_latch(net);
 }
 
+chaos_status chaos_batch_gradient(chaos_net* net, const float* d_images, const int32_t* d_labels, int64_t n,
+                                  float* d_grad) {
+    if (!net || !d_grad) return fail(CHAOS_E_INVALID, "NULL argument");
+    if (n < 0) return fail(CHAOS_E_INVALID, "n < 0");
+    if (n == 0) {
+        CUDA_TRY(cudaMemsetAsync(d_grad, 0, sizeof(float) * net->d->pint, net->stream));
+        return CHAOS_OK;
+    }
+    if (!d_images || !d_labels) return fail(CHAOS_E_INVALID, "NULL images/labels");
+    return sync_batch(net, d_images, d_labels, n, 0.f, d_grad, nullptr);
+}
+
+chaos_status chaos_apply_gradient(chaos_net* net, const float* d_grad, float lr) {
+    if (!net || !d_grad) return fail(CHAOS_E_INVALID, "NULL argument");
+    if (!std::isfinite(lr)) return fail(CHAOS_E_INVALID, "lr is not finite");
+    const long long np = net->d->pint;
+    chaos_apply_gradient_kernel<<<(unsigned)((np + 255) / 256), 256, 0, net->stream>>>(net->params, d_grad, lr, np);
+    CUDA_TRY(cudaGetLastError());
+    return CHAOS_OK;
+}
+
 chaos_status chaos_debug_claims(chaos_net* net, int32_t* host_counts, int64_t n) {
     if (!net || !host_counts) return fail(CHAOS_E_INVALID, "NULL argument");
     if (!net->claims || n > net->claims_cap) return fail(CHAOS_E_INVALID, "no claim record of that size");

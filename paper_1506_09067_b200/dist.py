@@ -1,5 +1,6 @@
-"""Multi-GPU plumbing (BASELINE.json north_star): one process per GPU,
-contiguous data shards, and an allreduce-average of all parameters every K local images.
+"""Multi-GPU plumbing (BASELINE.json north_star): one process per
+GPU, contiguous data shards, and an allreduce-average of all parameters every K local images
+(hogwild replicas); or the deterministic multi-GPU sync mode, one gradient all-reduce per batch.
 
 Each rank trains its replica in hogwild mode on its shard; after every interval of K
 images (and at the end of the shard) the replicas are averaged, w <- (1/P) sum_r w_r
@@ -29,6 +30,19 @@ def n_averages(n_local: int, k: int) -> int:
     return len(intervals(0, n_local, k))
 
 
+def batch_part(b0: int, nb: int, rank: int, world: int) -> tuple[int, int]:
+    """Rank r's contiguous part [s, e) of the global sync batch [b0, b0 + nb) (fixed split)."""
+    return b0 + nb * rank // world, b0 + nb * (rank + 1) // world
+
+
+def sum_(tensor, world: int, group=None):
+    """In-place all-reduce sum (the sync-mode gradient exchange)."""
+    import torch.distributed as dist
+    if world > 1:
+        dist.all_reduce(tensor, op=dist.ReduceOp.SUM, group=group)
+    return tensor
+
+
 def average_(tensor, world: int, group=None):
     """In-place all-reduce average.  NCCL has ReduceOp.AVG; gloo does not (sum, then scale)."""
     import torch.distributed as dist
@@ -43,10 +57,12 @@ def average_(tensor, world: int, group=None):
 
 
 class DistTrainer:
-    """Trains one replica per rank with periodic averaging.
+    """Trains one replica per rank with periodic averaging (hogwild), or all ranks as one
+    deterministic sync-SGD trainer (``sync_epoch``).
 
-    ``net`` needs ``train_epoch(images, labels, lr)`` and ``device_params()`` (the
-    chaos.Net API); tests substitute a CPU stand-in with the same two methods."""
+    ``net`` needs ``train_epoch(images, labels, lr)`` and ``device_params()`` (the chaos.Net
+    API) -- plus ``batch_gradient`` / ``apply_gradient`` for the sync mode; tests substitute a
+    CPU stand-in with the same methods."""
 
     def __init__(self, net, rank: int, world: int, k: int, group=None):
         self.net, self.rank, self.world, self.k, self.group = net, rank, world, k, group
@@ -63,3 +79,26 @@ class DistTrainer:
             if self.world > 1:
                 average_(params, self.world, self.group)
                 self.n_collectives += 1
+
+    def sync_epoch(self, images, labels, lr: float, batch: int, grad=None):
+        """Deterministic multi-GPU sync SGD: for every consecutive global
+        batch of ``batch`` images, rank r computes the fixed-order gradient sum of its contiguous
+        part (``batch_part``), the parts are all-reduced (sum), and every rank applies
+        W -= lr * G.  ``images``/``labels`` hold the whole (replicated) training set.  With one
+        rank this is exactly chaos_train_epoch(SYNC); with P ranks it is the same update up to
+        the summation order, and bitwise reproducible for a fixed P and topology."""
+        import torch
+        params = self.net.device_params()
+        if grad is None:
+            grad = torch.zeros_like(params)
+        n = int(labels.shape[0])
+        for b0 in range(0, n, batch):
+            nb = min(batch, n - b0)
+            s, e = batch_part(b0, nb, self.rank, self.world)
+            self.net.batch_gradient(images[s:e], labels[s:e], grad)
+            self.n_launches += 2
+            if self.world > 1:
+                sum_(grad, self.world, self.group)
+                self.n_collectives += 1
+            self.net.apply_gradient(grad, lr)
+        return grad

@@ -15,7 +15,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1506_09067_b200.dist import DistTrainer, intervals, n_averages, shard_range
+from paper_1506_09067_b200.dist import DistTrainer, batch_part, intervals, n_averages, shard_range
 
 
 def test_shard_range_partitions_and_aligns():
@@ -43,7 +43,8 @@ def test_intervals_and_average_counts():
 
 
 class FakeNet:
-    """CPU stand-in for chaos.Net: 'training' adds lr * (rank+1) * sum(images) to every weight."""
+    """CPU stand-in for chaos.Net: 'training' adds lr * (rank+1) * sum(images) to every weight;
+    the 'gradient' of an image set is (sum of its rows, as a per-weight vector)."""
 
     def __init__(self, n, rank):
         self.w = torch.arange(n, dtype=torch.float32)
@@ -56,6 +57,16 @@ class FakeNet:
     def train_epoch(self, images, labels, lr):
         self.calls.append(int(labels.shape[0]))
         self.w += lr * (self.rank + 1) * float(images.sum())
+
+    def batch_gradient(self, images, labels, grad):
+        # a gradient that depends on the weights (like a real one) and on every image
+        self.calls.append(int(labels.shape[0]))
+        grad.zero_()
+        for row in images:
+            grad += row.sum() * torch.tanh(self.w)
+
+    def apply_gradient(self, grad, lr):
+        self.w -= lr * grad
 
 
 def _free_port():
@@ -134,3 +145,55 @@ def test_single_process_skips_collective():
     tr.epoch(torch.ones(20, 3), torch.zeros(20, dtype=torch.int32), 0.1)
     assert tr.n_collectives == 0
     assert net.calls == [20]  # one launch over the whole shard
+
+
+def test_batch_part_partitions_every_batch():
+    for nb in (0, 1, 7, 64, 65):
+        for world in (1, 2, 3, 8):
+            parts = [batch_part(100, nb, r, world) for r in range(world)]
+            assert parts[0][0] == 100 and parts[-1][1] == 100 + nb
+            for (a, b), (c, d) in zip(parts, parts[1:]):
+                assert b == c
+
+
+def _sync_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = torch.Generator().manual_seed(0)
+        X = torch.rand(37, 5, generator=g, dtype=torch.float64)
+        Y = torch.zeros(37, dtype=torch.int32)
+        net = FakeNet(16, rank)
+        net.w = net.w.double() / 16
+        tr = DistTrainer(net, rank, world, 0)
+        tr.sync_epoch(X, Y, 0.01, batch=8)
+        q.put((rank, net.w.numpy(), tr.n_collectives))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_sync_epoch_equals_single_process():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sync_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=120) for _ in range(2)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # the same sync SGD in one process: every batch's gradient at the batch-start weights, summed
+    g = torch.Generator().manual_seed(0)
+    X = torch.rand(37, 5, generator=g, dtype=torch.float64)
+    w = torch.arange(16, dtype=torch.float64) / 16
+    for b0 in range(0, 37, 8):
+        G = torch.zeros(16, dtype=torch.float64)
+        for row in X[b0:b0 + 8]:
+            G += row.sum() * torch.tanh(w)
+        w = w - 0.01 * G
+    for rank, wr, ncoll in out:
+        assert ncoll == 5  # one all-reduce per batch (37 = 4*8 + 5)
+        np.testing.assert_allclose(wr, w.numpy(), rtol=1e-12)
+    np.testing.assert_array_equal(out[0][1], out[1][1])  # replicas stay bitwise identical

@@ -362,3 +362,46 @@ def test_hogwild_accuracy_gate(run, torch_cuda):
     ref = rec["per_epoch"][-1]
     n = len(d.y_test)
     assert abs(curve[-1][1] - ref["test_errors"]) / n * 100 <= 0.5, (curve, ref)
+
+
+def test_batch_gradient_apply_equals_sync_epoch_bitwise(torch_cuda):
+    # NEXT-4 building blocks on one GPU: batch_gradient + apply_gradient per batch reproduce
+    # chaos_train_epoch(SYNC) bit for bit (same slot-ordered sum, same update expression)
+    from paper_1506_09067_b200 import OPT_SYNC_BATCH, SYNC
+    from paper_1506_09067_b200.dist import DistTrainer
+    d = sd.prototype_dataset(17, 150, 0)
+    o, a, p = make("large", 17, torch_cuda)
+    a.set_option(OPT_SYNC_BATCH, 64)
+    X, Y = dev(torch_cuda, d.x_train, d.y_train)
+    a.train_epoch(X, Y, 0.02, SYNC)
+    _, b, _ = make("large", 17, torch_cuda)
+    DistTrainer(b, 0, 1, 0).sync_epoch(X, Y, 0.02, batch=64)
+    np.testing.assert_array_equal(a.get_params(), b.get_params())
+
+
+def test_two_rank_sync_emulated_matches_oracle(torch_cuda):
+    # NEXT-4 semantics with 2 ranks, emulated on one GPU: each batch's two halves are computed
+    # separately (rank parts), summed (the all-reduce), applied; equals the oracle's sync SGD
+    # within the R9 tolerance, and is bitwise reproducible run to run
+    import torch
+    from paper_1506_09067_b200.dist import batch_part
+    d = sd.prototype_dataset(18, 150, 0)
+    o, _, p = make("medium", 18, torch_cuda)
+    X, Y = dev(torch_cuda, d.x_train, d.y_train)
+    runs = []
+    for _ in range(2):
+        _, net, _ = make("medium", 18, torch_cuda)
+        g0 = torch.zeros_like(net.device_params())
+        g1 = torch.zeros_like(g0)
+        for b0 in range(0, 150, 64):
+            nb = min(64, 150 - b0)
+            s0, e0 = batch_part(b0, nb, 0, 2)
+            s1, e1 = batch_part(b0, nb, 1, 2)
+            net.batch_gradient(X[s0:e0], Y[s0:e0], g0)
+            net.batch_gradient(X[s1:e1], Y[s1:e1], g1)
+            g0 += g1
+            net.apply_gradient(g0, 0.05)
+        runs.append(net.get_params())
+    np.testing.assert_array_equal(runs[0], runs[1])
+    ref, _ = o.train_sync(p, d.x_train, d.y_train, 0.05, 64)
+    assert_parity(runs[0], ref, o.blocks())
