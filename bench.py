@@ -166,6 +166,10 @@ def main():
     ap.add_argument("--ref-images", type=int, default=400)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="hogwild", choices=["hogwild", "sync"],
+                    help="hogwild (CHAOS, the headline) or the deterministic sync mode (multi-GPU: one "
+                         "gradient all-reduce per global batch, SURVEY NEXT-4)")
+    ap.add_argument("--sync-batch", type=int, default=64, help="global batch of --mode sync")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -180,7 +184,15 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    w, xs, ys, xt, yt = make_data(world, rank)
+    if args.mode == "sync" and world > 1:
+        # sync mode: every rank holds the global training set (60,000 per GPU, weak scaling) and
+        # computes its contiguous part of every global batch
+        wl = sd.WORKLOADS["config4"]
+        xs, ys = sd.prototype_samples(wl.seed, 0, PER_GPU * world)
+        xt, yt = sd.prototype_samples(wl.seed, wl.n_train, 10000)
+        w = wl
+    else:
+        w, xs, ys, xt, yt = make_data(world, rank)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     net = Net(sd.ARCHS[args.arch], init_seed=w.seed, stream=stream)
@@ -190,6 +202,13 @@ def main():
     Xt = torch.from_numpy(xt).cuda()
     Yt = torch.from_numpy(yt).cuda()
     trainer = DistTrainer(net, rank, world, args.k)
+    grad_buf = torch.zeros_like(net.device_params()) if args.mode == "sync" else None
+
+    def step(Xs, Ys, lr_s):
+        if args.mode == "sync":
+            trainer.sync_epoch(Xs, Ys, lr_s, args.sync_batch, grad_buf)
+        else:
+            trainer.epoch(Xs, Ys, lr_s)
 
     def barrier():
         torch.cuda.synchronize()
@@ -198,7 +217,7 @@ def main():
 
     lr = w.lr0
     for s in range(args.warmup):
-        trainer.epoch(X, Y, lr * 0.9 ** s)
+        step(X, Y, lr * 0.9 ** s)
     net.sync()
     barrier()
     clk = ClockSampler(local)
@@ -211,7 +230,7 @@ def main():
     t0.record(stream)
     for s in range(args.steps):
         ev[s][0].record(stream)
-        trainer.epoch(X, Y, lr * 0.9 ** (args.warmup + s))
+        step(X, Y, lr * 0.9 ** (args.warmup + s))
         ev[s][1].record(stream)
     t1.record(stream)
     barrier()
@@ -225,7 +244,7 @@ def main():
     elapsed = float(tmax.item())
     total = PER_GPU * world * args.steps
     value = total / elapsed
-    train_loss = net.last_train_loss()
+    train_loss = net.last_train_loss() if args.mode == "hogwild" else None
 
     # a8: evaluation on the averaged model (timed separately)
     e0 = torch.cuda.Event(enable_timing=True)
@@ -236,21 +255,42 @@ def main():
     torch.cuda.synchronize()
     eval_ms = e0.elapsed_time(e1)
 
-    # e2e: the same metric through the public C-ABI host-buffer entry (H2D of every step's
-    # images + labels from pinned memory, D2H of the step's mean training loss)
+    # e2e: the same metric end to end with HOST buffers: every step copies its images + labels
+    # from pinned host memory (N=1 hogwild: inside the C-ABI call chaos_train_epoch_host; otherwise
+    # an explicit H2D copy on the training stream before the step) and reads a result back (the
+    # step's mean training loss / the updated parameters' first value), timed with barriers, max
+    # over ranks
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e:
         Xh = torch.from_numpy(xs).pin_memory()
         Yh = torch.from_numpy(ys).pin_memory()
-        net.train_epoch_host(Xh, Yh, lr * 0.5)  # warm the staging buffers
-        torch.cuda.synchronize()
+        host_entry = args.mode == "hogwild" and world == 1
+        out_h = torch.zeros(1, dtype=torch.float32).pin_memory()
+
+        def e2e_step(lr_s):
+            if host_entry:
+                net.train_epoch_host(Xh, Yh, lr_s)
+                net.last_train_loss()
+            else:
+                X.copy_(Xh, non_blocking=True)
+                Y.copy_(Yh, non_blocking=True)
+                step(X, Y, lr_s)
+                out_h.copy_(net.device_params()[:1], non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+        e2e_step(lr * 0.5)  # warm the staging buffers
+        barrier()
         t = time.perf_counter()
         for s in range(args.steps):
-            net.train_epoch_host(Xh, Yh, lr * 0.5)
-            net.last_train_loss()
-        dt = time.perf_counter() - t
-        e2e = {"value": PER_GPU * args.steps / dt, "unit": "samples/s",
-               "h2d_bytes_per_step": int(Xh.numel() * 4 + Yh.numel() * 4), "d2h_bytes_per_step": 8}
+            e2e_step(lr * 0.5)
+        barrier()
+        dt = torch.tensor([time.perf_counter() - t], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e = {"value": PER_GPU * world * args.steps / float(dt.item()), "unit": "samples/s",
+               "h2d_bytes_per_step": int(Xh.numel() * 4 + Yh.numel() * 4),
+               "d2h_bytes_per_step": 8 if host_entry else 4,
+               "path": "chaos_train_epoch_host (C ABI, host buffers)" if host_entry
+               else "pinned H2D copy + step on the training stream"}
 
     if rank != 0:
         dist.destroy_process_group()
@@ -270,15 +310,21 @@ def main():
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "configs[3] large net, hogwild (CHAOS), 60,000 images per GPU per step"
-                               + ("" if world == 1 else f"; configs[4] generator, NCCL average every {args.k}"),
-                   "arch": args.arch, "mode": "hogwild", "images_per_gpu_per_step": PER_GPU,
+        "config": {"workload": (f"configs[3] {args.arch} net, hogwild (CHAOS), 60,000 images per GPU per step"
+                                + ("" if world == 1 else f"; configs[4] generator, NCCL average every {args.k}"))
+                   if args.mode == "hogwild" else
+                   (f"configs[3] {args.arch} net, deterministic sync SGD, global batch {args.sync_batch}, "
+                    f"60,000 images per GPU per step" + ("" if world == 1 else
+                                                         "; one NCCL gradient all-reduce per batch")),
+                   "arch": args.arch, "mode": args.mode, "images_per_gpu_per_step": PER_GPU,
+                   "sync_batch": args.sync_batch if args.mode == "sync" else None,
                    "group_G": info["group"], "ctas": info["grid"], "threads_per_cta": info["block"],
                    "smem_bytes_per_cta": info["smem_bytes"], "sync_interval_K": args.k if world > 1 else None,
                    "l2": "inputs (202 MB/GPU) larger than the 126 MB L2", "parallelism": f"dp{world}"},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic,
-                     "kernel": "chaos_worker<LargeNet,G,512,kHogwild>",
+                     "kernel": f"chaos_worker<{args.arch.capitalize()}Net,{info['group']},{info['block']},"
+                               f"{'kHogwild' if args.mode == 'hogwild' else 'kSync'}>",
                      "flop_per_image": ALGO_FLOP[args.arch],
                      "peak_source": "148 SM x 128 FFMA/clk x 2 x 1.965 GHz (unit counts x max clock)"},
         "clocks": clocks,

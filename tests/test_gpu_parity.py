@@ -405,3 +405,26 @@ def test_two_rank_sync_emulated_matches_oracle(torch_cuda):
     np.testing.assert_array_equal(runs[0], runs[1])
     ref, _ = o.train_sync(p, d.x_train, d.y_train, 0.05, 64)
     assert_parity(runs[0], ref, o.blocks())
+
+
+@pytest.mark.parametrize("mode", ["hogwild", "sync"])
+def test_bench_line_contract(mode, torch_cuda):
+    # bench.py's JSON line on one GPU: contract keys, roofline + cpu_baseline objects, e2e with host bytes
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, os.path.join(root, "bench.py"), "--steps", "1", "--warmup", "1", "--mode", mode]
+    if mode == "sync":
+        cmd.append("--no-cpu-baseline")
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-3000:]
+    d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "clocks", "gpu_launches", "e2e"):
+        assert k in d, k
+    assert d["value"] > 0 and d["gpu_launches"] >= 1 and d["config"]["mode"] == mode
+    r = d["roofline"]
+    assert r["bound"] == "alu" and 0 < r["frac"] < 1 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert d["e2e"]["h2d_bytes_per_step"] == 60000 * (841 + 1) * 4
+    if mode == "hogwild":
+        assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
