@@ -654,7 +654,9 @@ __device__ __forceinline__ void conv_gw2(const KArgs& a, int slot, const float* 
 template <class L, int NT, int MODE, int NM, int W0, int NWARP>
 __device__ __forceinline__ void conv_gw_win(const KArgs& a, int slot, const float* __restrict__ in,
                                             const float* __restrict__ dp, const uint8_t* __restrict__ am, int woff,
-                                            int cnt, float sc) {
+                                            int cnt, float sc, const float4* __restrict__ dq4 = nullptr) {
+    // dq4 (optional): the phase-expanded delta, dq4[g][m][w] = d at component phase, 0 elsewhere
+    // (built once per iteration), replacing the per-thread (d, phase) selects
     constexpr int K = L::K, KP = L::KP, KK = L::KK, PW = L::PW, PH = L::PH, P = L::P, M = L::M, C = L::C;
     constexpr int W = L::W, HW = L::H * L::W, BS = KP + K - 1;
     constexpr int NG = (M + NM - 1) / NM, TILES = C * NG;
@@ -689,14 +691,26 @@ __device__ __forceinline__ void conv_gw_win(const KArgs& a, int slot, const floa
                 for (int q = 0; q < NM; ++q) {
                     const int m = m0 + q;
                     const bool vm = (NG * NM == M) || m < M;
-                    const float d = vm ? dpg[m * P + w] : 0.f;
-                    const int ph = vm ? amg[m * P + w] : 0;
-                    accb[q] += d;
+                    float dqv[4];
+                    if (dq4) {
+                        const float4 t4 = vm ? dq4[g * L::OUT_SZ + m * P + w] : make_float4(0.f, 0.f, 0.f, 0.f);
+                        dqv[0] = t4.x;
+                        dqv[1] = t4.y;
+                        dqv[2] = t4.z;
+                        dqv[3] = t4.w;
+                        accb[q] += (t4.x + t4.y) + (t4.z + t4.w);  // exactly d: three of them are 0
+                    } else {
+                        const float d = vm ? dpg[m * P + w] : 0.f;
+                        const int ph = vm ? amg[m * P + w] : 0;
+                        accb[q] += d;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) dqv[k] = (ph == k) ? d : 0.f;
+                    }
 #pragma unroll
                     for (int aa = 0; aa < KP; ++aa)
 #pragma unroll
                         for (int bb = 0; bb < KP; ++bb) {
-                            const float dq = (ph == aa * KP + bb) ? d : 0.f;
+                            const float dq = dqv[aa * KP + bb];
 #pragma unroll
                             for (int i = 0; i < K; ++i)
 #pragma unroll
@@ -1540,19 +1554,22 @@ __device__ __forceinline__ void conv_din3(const float* __restrict__ wsm, const f
 // registers; the phase selects d with a predicate-free select (4x the sparse MACs, no
 // branches, so the warp issues back to back).  Weights: 4 output maps per LDS.128.
 // ------------------------------------------------------------------------------------
-template <class L, int NT>
+template <class L, int NT, bool DEFER = false>
 __device__ __forceinline__ void conv_din_win(const float* __restrict__ wsm, const float* __restrict__ dp,
                                              const uint8_t* __restrict__ am, const float* __restrict__ in,
-                                             float* __restrict__ out, int cnt) {
+                                             float* __restrict__ out, int cnt, const float4* __restrict__ dq4 = nullptr) {
+    // dq4 (optional): phase-expanded delta as in conv_gw_win.  DEFER: one __syncthreads() between the
+    // accumulation and the writes of `out` (which may hold dq4, still read by other warps)
     constexpr int K = L::K, KP = L::KP, KK = L::KK, PW = L::PW, P = L::P, M = L::M, C = L::C;
     constexpr int H = L::H, W = L::W, HW = H * W, HR = L::HR, WR = L::WR;
     constexpr int NCW = (C + 31) / 32;
     static_assert(KP == 2 && M % 4 == 0 && L::MP == M, "2x2 pooling, 4 maps per vector load");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (warp >= cnt * NCW) return;
-    const int cw = warp % NCW, g = warp / NCW;
+    const bool has = warp < cnt * NCW;
+    if (!DEFER && !has) return;
+    const int cw = warp % NCW, g = has ? warp / NCW : 0;
     const int n = cw * 32 + lane;
-    const bool act = n < C;
+    const bool act = has && n < C;
     const float* wn = wsm + (act ? n : 0) * KK * L::MP;
     const float* dpg = dp + g * L::OUT_SZ;
     const uint8_t* amg = am + g * L::OUT_SZ;
@@ -1562,7 +1579,7 @@ __device__ __forceinline__ void conv_din_win(const float* __restrict__ wsm, cons
 #pragma unroll
         for (int x = 0; x < WR; ++x) acc[y][x] = 0.f;
 #pragma unroll 1
-    for (int m4 = 0; m4 < M; m4 += 4) {
+    for (int m4 = 0; m4 < (has ? M : 0); m4 += 4) {
         float4 w4[KK];
 #pragma unroll
         for (int tp = 0; tp < KK; ++tp) w4[tp] = *reinterpret_cast<const float4*>(wn + tp * L::MP + m4);
@@ -1572,13 +1589,24 @@ __device__ __forceinline__ void conv_din_win(const float* __restrict__ wsm, cons
 #pragma unroll
             for (int w = 0; w < P; ++w) {
                 const int pr = w / PW, pc = w % PW;
-                const float d = dpg[m * P + w];
-                const int ph = amg[m * P + w];
+                float dqv[4];
+                if (dq4) {
+                    const float4 t4 = dq4[g * L::OUT_SZ + m * P + w];
+                    dqv[0] = t4.x;
+                    dqv[1] = t4.y;
+                    dqv[2] = t4.z;
+                    dqv[3] = t4.w;
+                } else {
+                    const float d = dpg[m * P + w];
+                    const int ph = amg[m * P + w];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) dqv[k] = (ph == k) ? d : 0.f;
+                }
 #pragma unroll
                 for (int aa = 0; aa < KP; ++aa)
 #pragma unroll
                     for (int bb = 0; bb < KP; ++bb) {
-                        const float dq = (ph == aa * KP + bb) ? d : 0.f;
+                        const float dq = dqv[aa * KP + bb];
 #pragma unroll
                         for (int i = 0; i < K; ++i)
 #pragma unroll
@@ -1592,6 +1620,7 @@ __device__ __forceinline__ void conv_din_win(const float* __restrict__ wsm, cons
             }
         }
     }
+    if constexpr (DEFER) __syncthreads();
     if (act) {
         const float* ib = in + g * L::IN_SZ + n * HW;
         float* ob = out + g * L::IN_SZ + n * HW;
@@ -2267,13 +2296,31 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                     // weight gradient (issue-bound, published from registers) side by side
                     constexpr int DW = G * C3::NBAND * ((C3::C + 31) / 32);
                     static_assert(C3::PB > 0 && C3::NBAND == 1 && DW < NT / 32, "conv3 split");
-                    if (threadIdx.x < DW * 32) {
-                        if constexpr (C3::DWIN)
-                            conv_din_win<C3, NT>(wb, a3, am3, a2, sS, cnt);
-                        else
-                            conv_din2<C3, NT>(wb, a3, am3, a2, sS, nullptr, cnt);
+                    if constexpr (C3::DWIN && G * C3::OUT_SZ * 4 <= S::SFL) {
+                        // phase-expanded delta, once: dq4[g][m][w] = d at component phase (S is free here)
+                        float4* dq4 = reinterpret_cast<float4*>(sS);
+                        for (int e = threadIdx.x; e < cnt * C3::OUT_SZ; e += NT) {
+                            const float d = a3[e];
+                            const int ph = am3[e];
+                            dq4[e] = make_float4(ph == 0 ? d : 0.f, ph == 1 ? d : 0.f, ph == 2 ? d : 0.f, ph == 3 ? d : 0.f);
+                        }
+                        __syncthreads();
+                        if (threadIdx.x < DW * 32) {
+                            conv_din_win<C3, NT, true>(wb, a3, am3, a2, sS, cnt, dq4);  // output over dq4 after
+                        } else {
+                            conv_gw_win<C3, NT, MODE, C3::GWIN, DW, NT / 32 - DW>(a, slot, a2, a3, am3, O::c3w, cnt,
+                                                                                  sc, dq4);
+                            __syncthreads();  // pairs with conv_din_win's deferral barrier
+                        }
+                    } else {
+                        if (threadIdx.x < DW * 32) {
+                            if constexpr (C3::DWIN)
+                                conv_din_win<C3, NT>(wb, a3, am3, a2, sS, cnt);
+                            else
+                                conv_din2<C3, NT>(wb, a3, am3, a2, sS, nullptr, cnt);
+                        }
+                        conv_gw_win<C3, NT, MODE, C3::GWIN, DW, NT / 32 - DW>(a, slot, a2, a3, am3, O::c3w, cnt, sc);
                     }
-                    conv_gw_win<C3, NT, MODE, C3::GWIN, DW, NT / 32 - DW>(a, slot, a2, a3, am3, O::c3w, cnt, sc);
                     __syncthreads();
                     PTIME(9);
                 } else {

@@ -45,7 +45,7 @@ struct MediumNet {  // configs[2] = Table I medium
 struct LargeNet {  // configs[3], configs[4]
     // 20 warps (<= 96 registers): one warp per (image, window row) in conv2's delta_in and per
     // (3 maps, 32 input maps) in its weight gradient; see profiles/r1q (640-thread tile sweep)
-    static constexpr int NCONV = 3, NFULL = 2, GDEF = 4, GINIT = 4, INFLIGHT = 592, NT = 640, SFL = 6000;
+    static constexpr int NCONV = 3, NFULL = 2, GDEF = 4, GINIT = 4, INFLIGHT = 592, NT = 640, SFL = 6400;
 #ifndef C1MT
 #define C1MT 10
 #endif
