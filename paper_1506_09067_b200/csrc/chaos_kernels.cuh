@@ -48,8 +48,7 @@ __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 // Tuning knobs: MT maps per thread in the forward; TT taps per thread and GS split of the
 // (image, window) sum in the weight gradient; RB input rows per band in delta_in.
 template <int C_, int H_, int W_, int M_, int K_, int KP_, int MT_, int TT_, int GS_, int RB_, int PB_ = 0,
-          int NN_ = 0, int MS_ = 0, bool GWMMA_ = false, bool DIN3_ = false, int GWIN_ = 0,
-          bool DWIN_ = false, bool GW5_ = false, int NSPL_ = 1>
+          int MS_ = 0, bool GWMMA_ = false, bool DIN3_ = false, int GWIN_ = 0, bool DWIN_ = false, int NSPL_ = 1>
 struct Conv {
     static constexpr int C = C_, H = H_, W = W_, M = M_, K = K_, KP = KP_;
     static constexpr int OH = H - K + 1, OW = W - K + 1;
@@ -67,8 +66,6 @@ struct Conv {
     static constexpr int NBAND = PB > 0 ? (PH + PB - 1) / PB : 0;
     static constexpr int BR = PB * KP + K - 1;                        // input rows per band
     static constexpr int HAND = NBAND > 1 ? (NBAND - 1) * (K - 1) * WR * C : 0;  // hand-off floats per image
-    // weight gradient by (output map, group of NN input maps) items (conv_gw2) when NN > 0
-    static constexpr int NN = NN_;
     // weight gradient by (set of MS output maps, 32 input maps) warps (conv_gw3) when MS > 0
     static constexpr int MS = MS_;
     // weight gradient on the tensor cores (conv_gw_mma)
@@ -80,8 +77,6 @@ struct Conv {
     static constexpr int GWIN = GWIN_;
     // dense branch-free per-window delta_in, whole map per lane (conv_din_win)
     static constexpr bool DWIN = DWIN_;
-    // weight gradient with the compact sliding-block loop (conv_gw5, uses MS)
-    static constexpr bool GW5 = GW5_;
     // forward: the input maps of one item split over NSPL adjacent lanes (partial sums combined
     // with shfl_xor) -- more items for small layers
     static constexpr int NSPL = NSPL_;
@@ -580,66 +575,6 @@ __device__ __forceinline__ void conv_gw(const KArgs& a, int slot, const float* _
 }
 
 // ------------------------------------------------------------------------------------
-// PHASE(conv_gw2) conv weight gradient, one thread item = (output map m, NN input maps):
-//   gW[n][i][j][m] = sum_g sum_w dp[g][m][w] * in[g][n][argpos(g,m,w) + (i,j)],  gb[m] = sum dp
-// Consecutive lanes take consecutive n-groups of the same m, so the delta and argmax loads
-// are broadcasts; the windows of a pooled row are unrolled, so the only per-window address
-// arithmetic is the argmax phase offset and all NN*K*K gathers use immediate offsets.  Sums
-// are in a fixed (g, window) order per element (deterministic); the block, scaled by `sc`,
-// is assembled in the weight store's layout in `scr` and published with one bulk op.
-// ------------------------------------------------------------------------------------
-template <class L, int NT, int MODE>
-__device__ __forceinline__ void conv_gw2(const KArgs& a, int slot, const float* __restrict__ in,
-                                         const float* __restrict__ dp, const uint8_t* __restrict__ am,
-                                         float* __restrict__ scr, int woff, int cnt, float sc) {
-    constexpr int K = L::K, KP = L::KP, KK = L::KK, PW = L::PW, PH = L::PH, P = L::P, M = L::M, C = L::C;
-    constexpr int W = L::W, HW = L::H * L::W, NN = L::NN, NG = C / NN;
-    static_assert(NN > 0 && C % NN == 0, "NN must divide C");
-    for (int it = threadIdx.x; it < M * NG; it += NT) {
-        const int ng = it % NG;
-        const int m = it / NG;
-        float acc[NN][KK];
-#pragma unroll
-        for (int q = 0; q < NN; ++q)
-#pragma unroll
-            for (int t = 0; t < KK; ++t) acc[q][t] = 0.f;
-        float accb = 0.f;
-#pragma unroll 1
-        for (int g = 0; g < cnt; ++g) {
-            const float* ing = in + g * L::IN_SZ + ng * NN * HW;
-            const float* dpg = dp + g * L::OUT_SZ + m * P;
-            const uint8_t* amg = am + g * L::OUT_SZ + m * P;
-#pragma unroll 1
-            for (int pr = 0; pr < PH; ++pr) {
-                const float* inr = ing + pr * KP * W;
-#pragma unroll
-                for (int pc = 0; pc < PW; ++pc) {
-                    const float d = dpg[pr * PW + pc];
-                    const int arg = amg[pr * PW + pc];
-                    const float* base = inr + pc * KP + (arg / KP) * W + (arg % KP);
-#pragma unroll
-                    for (int q = 0; q < NN; ++q)
-#pragma unroll
-                        for (int t = 0; t < KK; ++t) acc[q][t] = fmaf(d, base[q * HW + (t / K) * W + (t % K)], acc[q][t]);
-                    accb += d;
-                }
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < NN; ++q)
-#pragma unroll
-            for (int t = 0; t < KK; ++t) scr[((ng * NN + q) * KK + t) * L::MP + m] = sc * acc[q][t];
-        if (ng == 0) scr[L::WFL + m] = sc * accb;
-    }
-    if constexpr (L::MP > M) {  // padding columns of the block publish zeros
-        for (int e = threadIdx.x; e < (L::ROWS + 1) * (L::MP - M); e += NT)
-            scr[(e / (L::MP - M)) * L::MP + M + e % (L::MP - M)] = 0.f;
-    }
-    sync_for_async();
-    publish_bulk<MODE>(a, slot, woff, scr, L::BLK);
-}
-
-// ------------------------------------------------------------------------------------
 // PHASE(conv_gw_win) conv weight gradient, dense per pooling window, branch-free (KP == 2):
 //   gW[n][i][j][m] = sum_g sum_w sum_{phase q} Dz_q[g][m][w] * in[g][n][2pr+a(q)+i][2pc+b(q)+j]
 // where Dz_q = d[g][m][w] if the argmax of (g, m, w) has phase q, else 0 (4x the argmax-sparse
@@ -915,117 +850,6 @@ __device__ __forceinline__ void conv_gw3(const KArgs& a, int slot, const float* 
                                 }
                             }
                         }
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < MS; ++q) {
-            if (act && (MS * NSET == M || m0 + q < M)) {
-#pragma unroll
-                for (int t = 0; t < KK; ++t) scr[(n * KK + t) * L::MP + m0 + q] = sc * acc[q][t];
-                if (n == 0) scr[L::WFL + m0 + q] = sc * accb[q];
-            }
-        }
-    }
-    if constexpr (L::MP > M) {  // padding columns of the block publish zeros
-        for (int e = threadIdx.x; e < (L::ROWS + 1) * (L::MP - M); e += NT)
-            scr[(e / (L::MP - M)) * L::MP + M + e % (L::MP - M)] = 0.f;
-    }
-    sync_for_async();
-    publish_bulk<MODE>(a, slot, woff, scr, L::BLK);
-}
-
-// ------------------------------------------------------------------------------------
-// PHASE(conv_gw5) conv_gw3 with a compact loop body (KP == 2): the windows of a pooled row
-// are a runtime loop over a (KP+K-1)^2 register block that slides KP columns per window
-// (KP new columns loaded per step), so the unrolled code is one window x MS maps x 4 phases
-// and stays in the instruction cache.  Same mapping, order and publish as conv_gw3.
-// ------------------------------------------------------------------------------------
-template <class L, int NT, int MODE>
-__device__ __forceinline__ void conv_gw5(const KArgs& a, int slot, const float* __restrict__ in,
-                                         const float* __restrict__ dp, const uint8_t* __restrict__ am,
-                                         float* __restrict__ scr, int woff, int cnt, float sc) {
-    constexpr int K = L::K, KP = L::KP, KK = L::KK, PW = L::PW, PH = L::PH, P = L::P, M = L::M, C = L::C;
-    constexpr int W = L::W, HW = L::H * L::W, MS = L::MS, NSET = (M + MS - 1) / MS;
-    constexpr int NCW = (C + 31) / 32, BS = KP + K - 1;
-    constexpr int NW = NT / 32;
-    static_assert(KP == 2, "2x2 pooling");
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int task = warp; task < NSET * NCW; task += NW) {
-        const int cw = task % NCW;
-        const int m0 = (task / NCW) * MS;
-        const int n = cw * 32 + lane;
-        const bool act = n < C;
-        float acc[MS][KK];
-        float accb[MS];
-#pragma unroll
-        for (int q = 0; q < MS; ++q) {
-            accb[q] = 0.f;
-#pragma unroll
-            for (int t = 0; t < KK; ++t) acc[q][t] = 0.f;
-        }
-#pragma unroll 1
-        for (int g = 0; g < cnt; ++g) {
-            const float* ing = in + g * L::IN_SZ + (act ? n : 0) * HW;
-            const float* dpg = dp + g * L::OUT_SZ;
-            const uint8_t* amg = am + g * L::OUT_SZ;
-#pragma unroll 1
-            for (int pr = 0; pr < PH; ++pr) {
-                const float* rowp = ing + pr * KP * W;
-                float blk[BS][BS];
-#pragma unroll
-                for (int r = 0; r < BS; ++r)
-#pragma unroll
-                    for (int c = 0; c < BS; ++c) blk[r][c] = rowp[r * W + c];
-#pragma unroll 1
-                for (int pc = 0; pc < PW; ++pc) {
-                    float dv[MS];
-                    int av[MS];
-#pragma unroll
-                    for (int q = 0; q < MS; ++q) {
-                        const bool vq = (MS * NSET == M) || m0 + q < M;
-                        const int o = (vq ? m0 + q : 0) * P + pr * PW + pc;
-                        dv[q] = vq ? dpg[o] : 0.f;
-                        av[q] = vq ? static_cast<int>(amg[o]) : -1;
-                    }
-                    // next block's new columns, loaded before the branches
-                    float nxt[BS][KP];
-                    const bool more = pc + 1 < PW;
-#pragma unroll
-                    for (int r = 0; r < BS; ++r)
-#pragma unroll
-                        for (int c = 0; c < KP; ++c) nxt[r][c] = more ? rowp[r * W + (pc + 1) * KP + (BS - KP) + c] : 0.f;
-#pragma unroll
-                    for (int q = 0; q < MS; ++q) {
-                        const float d = dv[q];
-                        const int arg = av[q];
-                        accb[q] += d;
-                        if (arg < 2) {  // warp-uniform two-level branch on the argmax phase
-                            if (arg == 0) {
-#pragma unroll
-                                for (int t = 0; t < KK; ++t) acc[q][t] = fmaf(d, blk[t / K][t % K], acc[q][t]);
-                            } else if (arg == 1) {
-#pragma unroll
-                                for (int t = 0; t < KK; ++t) acc[q][t] = fmaf(d, blk[t / K][1 + t % K], acc[q][t]);
-                            }
-                        } else {
-                            if (arg == 2) {
-#pragma unroll
-                                for (int t = 0; t < KK; ++t) acc[q][t] = fmaf(d, blk[1 + t / K][t % K], acc[q][t]);
-                            } else {
-#pragma unroll
-                                for (int t = 0; t < KK; ++t) acc[q][t] = fmaf(d, blk[1 + t / K][1 + t % K], acc[q][t]);
-                            }
-                        }
-                    }
-                    // slide KP columns
-#pragma unroll
-                    for (int r = 0; r < BS; ++r) {
-#pragma unroll
-                        for (int c = 0; c < BS - KP; ++c) blk[r][c] = blk[r][c + KP];
-#pragma unroll
-                        for (int c = 0; c < KP; ++c) blk[r][BS - KP + c] = nxt[r][c];
                     }
                 }
             }
@@ -2336,8 +2160,6 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                     conv_gw_mma<C3, NT, MODE>(a, slot, a2, a3, am3, wb, O::c3w, cnt, sc);
                 else if constexpr (C3::MS > 0)
                     conv_gw3<C3, NT, MODE>(a, slot, a2, a3, am3, wb, O::c3w, cnt, sc);
-                else if constexpr (C3::NN > 0)
-                    conv_gw2<C3, NT, MODE>(a, slot, a2, a3, am3, wb, O::c3w, cnt, sc);
                 else
                     conv_gw<C3, NT, MODE, true>(a, slot, a2, a3, am3, wb, O::c3w, cnt, sc);
                 }
@@ -2365,14 +2187,10 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                     PTIME(12);
                     PTIME(13);
                 } else {
-                if constexpr (C2::GW5)
-                    conv_gw5<C2, NT, MODE>(a, slot, a1, sS, am2, wb + C2::BLK, O::c2w, cnt, sc);
-                else if constexpr (C2::GWMMA)
+                if constexpr (C2::GWMMA)
                     conv_gw_mma<C2, NT, MODE>(a, slot, a1, sS, am2, wb + C2::BLK, O::c2w, cnt, sc);
                 else if constexpr (C2::MS > 0)
                     conv_gw3<C2, NT, MODE>(a, slot, a1, sS, am2, wb + C2::BLK, O::c2w, cnt, sc);
-                else if constexpr (C2::NN > 0)
-                    conv_gw2<C2, NT, MODE>(a, slot, a1, sS, am2, wb + C2::BLK, O::c2w, cnt, sc);
                 else
                     conv_gw<C2, NT, MODE, true>(a, slot, a1, sS, am2, wb + C2::BLK, O::c2w, cnt, sc);
                 __syncthreads();

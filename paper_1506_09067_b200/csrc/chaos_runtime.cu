@@ -44,19 +44,13 @@ struct MediumNet {  // configs[2] = Table I medium
 };
 struct LargeNet {  // configs[3], configs[4]
     // 20 warps (<= 96 registers): one warp per (image, window row) in conv2's delta_in and per
-    // (3 maps, 32 input maps) in its weight gradient; see profiles/r1q (640-thread tile sweep)
+    // (3 maps, 32 input maps) in its weight gradient; conv3's backward split over warps 0-7
+    // (delta_in) and 8-19 (weight gradient).  Tile sweeps: profiles/r1q.
     static constexpr int NCONV = 3, NFULL = 2, GDEF = 4, GINIT = 4, INFLIGHT = 592, NT = 640, SFL = 6400;
-#ifndef C1MT
-#define C1MT 10
-#endif
-#ifndef C1GS
-#define C1GS 16
-#endif
-    using C1 = Conv<1, 29, 29, 20, 4, 2, C1MT, 16, C1GS, 2>;
-    using C2 = Conv<20, 13, 13, 60, 3, 2, 10, 9, 1, 4, /*PB*/ 1, /*NN*/ 2, /*MS*/ 3, /*GWMMA*/ false, /*DIN3*/ true,
-                    /*GWIN*/ 0, /*DWIN*/ false, /*GW5*/ false>;
-    using C3 = Conv<60, 5, 5, 100, 2, 2, /*MT*/ 4, 4, 1, 5, /*PB*/ 2, /*NN*/ 4, /*MS*/ 13, /*GWMMA*/ false, /*DIN3*/ false,
-                    /*GWIN*/ 4, /*DWIN*/ true, /*GW5*/ false, /*NSPL*/ 1>;
+    //                C   H   W   M   K  KP  MT  TT  GS  RB  PB  MS  GWMMA  DIN3  GWIN  DWIN  NSPL
+    using C1 = Conv<1, 29, 29, 20, 4, 2, 10, 16, 16, 2>;
+    using C2 = Conv<20, 13, 13, 60, 3, 2, 10, 9, 1, 4, 1, 3, false, true, 0, false, 1>;
+    using C3 = Conv<60, 5, 5, 100, 2, 2, 4, 4, 1, 5, 2, 13, false, false, 4, true, 1>;
     using F1 = Full<400, 150, true>;
     using F2 = Full<150, 10, false>;
 };
