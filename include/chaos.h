@@ -106,9 +106,13 @@ int64_t chaos_net_device_params_len(const chaos_net* net); /* floats, incl. padd
  * net's stream.  lr is per call: the caller applies the x0.9/epoch schedule. */
 chaos_status chaos_train_epoch(chaos_net* net, const float* d_images, const int32_t* d_labels, int64_t n, float lr,
                                chaos_mode mode);
-/* Same, from HOST buffers: the images/labels are copied to net-owned device
- * staging buffers on the net's stream, chunk by chunk, overlapped with training
- * (hogwild) -- the end-to-end entry point.  Synchronizing on return. */
+/* Same, from HOST buffers -- the end-to-end entry point.  The images/labels are copied to
+ * net-owned device staging buffers in ~n/8 chunks on a net-owned copy stream; chunk c trains
+ * (on the net's stream) as soon as its own copy has landed, while chunk c+1 is in flight, so
+ * the H2D transfer overlaps training (pinned host memory required for the overlap).  Sync mode
+ * chunks on whole batches, so the result equals chaos_train_epoch(SYNC) bitwise; a hogwild
+ * epoch is the same hogwild run with a claim barrier at each chunk boundary.  The debug claim
+ * record (CHAOS_OPT_DEBUG_CLAIMS) then refers to the last chunk.  Synchronizing on return. */
 chaos_status chaos_train_epoch_host(chaos_net* net, const float* h_images, const int32_t* h_labels, int64_t n,
                                     float lr, chaos_mode mode);
 /* Mean training loss (double) of the last chaos_train_epoch call; synchronizing. */

@@ -227,6 +227,9 @@ struct chaos_net {
     int occ[2][4] = {};
     unsigned long long* ptime = nullptr;  // CHAOS_TIMING builds only
     int ptime_grid = 0;
+    cudaStream_t copy_stream = nullptr;    // chaos_train_epoch_host: H2D chunks overlap training
+    std::vector<cudaEvent_t> chunk_ev;
+    cudaEvent_t staging_free = nullptr;
 };
 
 namespace {
@@ -493,6 +496,9 @@ void chaos_net_destroy(chaos_net* net) {
     if (!net) return;
     if (net->stream) cudaStreamSynchronize(net->stream);
     cudaDeviceSynchronize();
+    if (net->copy_stream) cudaStreamDestroy(net->copy_stream);
+    if (net->staging_free) cudaEventDestroy(net->staging_free);
+    for (cudaEvent_t e : net->chunk_ev) cudaEventDestroy(e);
     void* ptrs[] = {net->params, net->latch,  net->counter, net->loss_sum, net->partial, net->grad_out, net->claims,
                     net->ev_loss, net->ev_wrong, net->ev_sum, net->ev_err, net->st_x, net->st_y, net->ptime};
     for (void* p : ptrs)
@@ -562,16 +568,13 @@ chaos_status chaos_net_set_params(chaos_net* net, const float* host_src, int64_t
     return CHAOS_OK;
 }
 
-chaos_status chaos_train_epoch(chaos_net* net, const float* d_images, const int32_t* d_labels, int64_t n, float lr,
-                               chaos_mode mode) {
-    if (!net) return fail(CHAOS_E_INVALID, "net is NULL");
-    if (n < 0) return fail(CHAOS_E_INVALID, "n < 0");
-    if (!std::isfinite(lr)) return fail(CHAOS_E_INVALID, "lr is not finite");
-    if (mode != CHAOS_HOGWILD && mode != CHAOS_SYNC) return fail(CHAOS_E_INVALID, "unknown mode %d", (int)mode);
-    CUDA_TRY(cudaMemsetAsync(net->loss_sum, 0, sizeof(double), net->stream));
-    net->last_train_n = n;
-    if (n == 0) return CHAOS_OK;
-    if (!d_images || !d_labels) return fail(CHAOS_E_INVALID, "NULL images/labels");
+}  // extern "C"
+
+namespace {
+// One Training phase launch over images [0, n) (n > 0, arguments validated), accumulating into
+// the net's training-loss sum; asynchronous on the net's stream.
+chaos_status train_range(chaos_net* net, const float* d_images, const int32_t* d_labels, int64_t n, float lr,
+                         chaos_mode mode) {
     const int G = net->group;
     if (mode == CHAOS_HOGWILD) {
         KArgs k = base_args(net);
@@ -616,6 +619,22 @@ chaos_status chaos_train_epoch(chaos_net* net, const float* d_images, const int3
     }
     return CHAOS_OK;
 }
+}  // namespace
+
+extern "C" {
+
+chaos_status chaos_train_epoch(chaos_net* net, const float* d_images, const int32_t* d_labels, int64_t n, float lr,
+                               chaos_mode mode) {
+    if (!net) return fail(CHAOS_E_INVALID, "net is NULL");
+    if (n < 0) return fail(CHAOS_E_INVALID, "n < 0");
+    if (!std::isfinite(lr)) return fail(CHAOS_E_INVALID, "lr is not finite");
+    if (mode != CHAOS_HOGWILD && mode != CHAOS_SYNC) return fail(CHAOS_E_INVALID, "unknown mode %d", (int)mode);
+    CUDA_TRY(cudaMemsetAsync(net->loss_sum, 0, sizeof(double), net->stream));
+    net->last_train_n = n;
+    if (n == 0) return CHAOS_OK;
+    if (!d_images || !d_labels) return fail(CHAOS_E_INVALID, "NULL images/labels");
+    return train_range(net, d_images, d_labels, n, lr, mode);
+}
 
 chaos_status chaos_train_epoch_host(chaos_net* net, const float* h_images, const int32_t* h_labels, int64_t n,
                                     float lr, chaos_mode mode) {
@@ -623,7 +642,10 @@ chaos_status chaos_train_epoch_host(chaos_net* net, const float* h_images, const
     if (n < 0) return fail(CHAOS_E_INVALID, "n < 0");
     if (n == 0) return chaos_train_epoch(net, nullptr, nullptr, 0, lr, mode);
     if (!h_images || !h_labels) return fail(CHAOS_E_INVALID, "NULL images/labels");
+    if (!std::isfinite(lr)) return fail(CHAOS_E_INVALID, "lr is not finite");
+    if (mode != CHAOS_HOGWILD && mode != CHAOS_SYNC) return fail(CHAOS_E_INVALID, "unknown mode %d", (int)mode);
     if (net->st_cap < n) {
+        CUDA_TRY(cudaStreamSynchronize(net->stream));
         if (net->st_x) cudaFree(net->st_x);
         if (net->st_y) cudaFree(net->st_y);
         net->st_x = nullptr;
@@ -632,10 +654,40 @@ chaos_status chaos_train_epoch_host(chaos_net* net, const float* h_images, const
         CUDA_TRY(cudaMalloc(&net->st_y, sizeof(int) * n));
         net->st_cap = n;
     }
-    CUDA_TRY(cudaMemcpyAsync(net->st_x, h_images, sizeof(float) * 841 * n, cudaMemcpyHostToDevice, net->stream));
-    CUDA_TRY(cudaMemcpyAsync(net->st_y, h_labels, sizeof(int) * n, cudaMemcpyHostToDevice, net->stream));
-    chaos_status s = chaos_train_epoch(net, net->st_x, net->st_y, n, lr, mode);
-    if (s) return s;
+    if (!net->copy_stream) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&net->copy_stream, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&net->staging_free, cudaEventDisableTiming));
+    }
+    // chunks of ~n/8 images (whole sync batches in sync mode; multiples of 16 images so every chunk
+    // start keeps the 16-B alignment of the TMA image copies): chunk c+1 is copied on the copy
+    // stream while chunk c trains on the net's stream
+    const long long unit = (mode == CHAOS_SYNC) ? net->sync_batch : 16;
+    long long chunk = (n + 7) / 8;
+    chunk = (chunk + unit - 1) / unit * unit;
+    if (chunk < 8192 && mode == CHAOS_HOGWILD) chunk = 8192;  // keep launches long enough to fill the GPU
+    const long long nch = (n + chunk - 1) / chunk;
+    while ((long long)net->chunk_ev.size() < nch) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        net->chunk_ev.push_back(e);
+    }
+    // the staging buffers may still be read by the previous call's kernels
+    CUDA_TRY(cudaEventRecord(net->staging_free, net->stream));
+    CUDA_TRY(cudaStreamWaitEvent(net->copy_stream, net->staging_free, 0));
+    CUDA_TRY(cudaMemsetAsync(net->loss_sum, 0, sizeof(double), net->stream));
+    net->last_train_n = n;
+    for (long long c = 0; c < nch; ++c) {
+        const long long off = c * chunk;
+        const long long len = (n - off) < chunk ? (n - off) : chunk;
+        CUDA_TRY(cudaMemcpyAsync(net->st_x + off * 841, h_images + off * 841, sizeof(float) * 841 * len,
+                                 cudaMemcpyHostToDevice, net->copy_stream));
+        CUDA_TRY(cudaMemcpyAsync(net->st_y + off, h_labels + off, sizeof(int) * len, cudaMemcpyHostToDevice,
+                                 net->copy_stream));
+        CUDA_TRY(cudaEventRecord(net->chunk_ev[c], net->copy_stream));
+        CUDA_TRY(cudaStreamWaitEvent(net->stream, net->chunk_ev[c], 0));
+        chaos_status st = train_range(net, net->st_x + off * 841, net->st_y + off, len, lr, mode);
+        if (st) return st;
+    }
     return chaos_net_sync(net);
 }
 

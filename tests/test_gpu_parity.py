@@ -428,3 +428,22 @@ def test_bench_line_contract(mode, torch_cuda):
     assert d["e2e"]["h2d_bytes_per_step"] == 60000 * (841 + 1) * 4
     if mode == "hogwild":
         assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
+
+
+def test_host_entry_hogwild_chunks_are_the_same_run(torch_cuda):
+    # chaos_train_epoch_host streams ~n/8-image chunks (>= 8192) through a copy stream; with one
+    # worker (1 CTA, G=1) hogwild is sequential SGD, so the chunked host run must equal the
+    # single-launch device run bit for bit across the chunk boundary
+    from paper_1506_09067_b200 import OPT_MAX_CTAS
+    import torch
+    n = 9000  # two chunks: 8192 + 808
+    d = sd.prototype_dataset(19, n, 0)
+    o, a, p = make("tiny", 19, torch_cuda, 1)
+    a.set_option(OPT_MAX_CTAS, 1)
+    a.train_epoch_host(torch.from_numpy(d.x_train).pin_memory(), torch.from_numpy(d.y_train).pin_memory(), 0.01)
+    _, b, _ = make("tiny", 19, torch_cuda, 1)
+    b.set_option(OPT_MAX_CTAS, 1)
+    X, Y = dev(torch_cuda, d.x_train, d.y_train)
+    b.train_epoch(X, Y, 0.01)
+    np.testing.assert_array_equal(a.get_params(), b.get_params())
+    assert abs(a.last_train_loss() - b.last_train_loss()) <= 1e-12 * abs(b.last_train_loss())
