@@ -42,6 +42,15 @@ struct MediumNet {  // configs[2] = Table I medium
     using F1 = Full<360, 150, true>;
     using F2 = Full<150, 10, false>;
 };
+struct PaperSmallNet {  // Table I small: conv5 4x4 -> pool2 -> conv10 5x5 -> pool3
+                        // -> FC 90->50 tanh -> FC 50->10; same generic kernels as the medium net
+    static constexpr int NCONV = 2, NFULL = 2, GDEF = 4, GINIT = 1, INFLIGHT = 148, NT = 256, SFL = 3364;
+    using C1 = Conv<1, 29, 29, 5, 4, 2, /*MT*/ 5, /*TT*/ 16, /*GS*/ 32, /*RB*/ 2>;
+    using C2 = Conv<5, 13, 13, 10, 5, 3, /*MT*/ 2, /*TT*/ 25, /*GS*/ 1, /*RB*/ 3>;
+    using C3 = C2;
+    using F1 = Full<90, 50, true>;
+    using F2 = Full<50, 10, false>;
+};
 struct LargeNet {  // configs[3], configs[4]
     // 20 warps (<= 96 registers): one warp per (image, window row) in conv2's delta_in and per
     // (3 maps, 32 input maps) in its weight gradient; conv3's backward split over warps 0-7
@@ -166,6 +175,10 @@ const std::vector<NetDesc>& registry() {
         v.push_back(make_desc<MediumNet>(
             "medium", {{CHAOS_CONV, 20, 4, CHAOS_TANH}, {CHAOS_MAXPOOL, 0, 2, 0}, {CHAOS_CONV, 40, 5, CHAOS_TANH},
                        {CHAOS_MAXPOOL, 0, 3, 0}, {CHAOS_FULL, 150, 0, CHAOS_TANH}, {CHAOS_FULL, 10, 0, CHAOS_IDENTITY}}));
+        v.push_back(make_desc<PaperSmallNet>(
+            "paper_small", {{CHAOS_CONV, 5, 4, CHAOS_TANH}, {CHAOS_MAXPOOL, 0, 2, 0}, {CHAOS_CONV, 10, 5, CHAOS_TANH},
+                            {CHAOS_MAXPOOL, 0, 3, 0}, {CHAOS_FULL, 50, 0, CHAOS_TANH},
+                            {CHAOS_FULL, 10, 0, CHAOS_IDENTITY}}));
         v.push_back(make_desc<LargeNet>(
             "large", {{CHAOS_CONV, 20, 4, CHAOS_TANH}, {CHAOS_MAXPOOL, 0, 2, 0}, {CHAOS_CONV, 60, 3, CHAOS_TANH},
                       {CHAOS_MAXPOOL, 0, 2, 0}, {CHAOS_CONV, 100, 2, CHAOS_TANH}, {CHAOS_MAXPOOL, 0, 2, 0},
@@ -441,7 +454,7 @@ chaos_net* chaos_net_create(const chaos_arch* arch) {
     if (validate(arch) != CHAOS_OK) return nullptr;
     const NetDesc* d = match(arch);
     if (!d) {
-        fail(CHAOS_E_UNSUPPORTED, "valid arch without a compiled sm_100a instantiation (compiled: tiny, medium, large)");
+        fail(CHAOS_E_UNSUPPORTED, "valid arch without a compiled sm_100a instantiation (compiled: tiny, medium, large, paper_small)");
         return nullptr;
     }
     chaos_net* net = new chaos_net();

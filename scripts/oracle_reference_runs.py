@@ -30,16 +30,19 @@ RUNS = {
     "config3_seq": ("config3", "seq", 1, 15),
     "config3_sync64_e1": ("config3", "sync", 64, 1),
     "config2_sync64_e1": ("config2", "sync", 64, 1),
+    # the paper's Table I small net (NEXT-1) on the configs[1] data
+    "paper_small_seq": ("config1", "seq", 1, 15, "paper_small"),
 }
 
 
 def run(name):
-    wname, mode, batch, epochs = RUNS[name]
+    wname, mode, batch, epochs = RUNS[name][:4]
     w = sd.WORKLOADS[wname]
+    arch = RUNS[name][4] if len(RUNS[name]) > 4 else w.arch
     d = sd.make_dataset(w)
-    o = Oracle(sd.ARCHS[w.arch])
+    o = Oracle(sd.ARCHS[arch])
     p = sd.init_params(w.seed, o.blocks()).astype(np.float64)
-    rec = {"run": name, "workload": wname, "arch": w.arch, "mode": mode, "batch": batch, "epochs": epochs,
+    rec = {"run": name, "workload": wname, "arch": arch, "mode": mode, "batch": batch, "epochs": epochs,
            "data_sha256": d.sha256(), "lr0": w.lr0, "per_epoch": []}
     t0 = time.time()
     ckpt = os.path.join(OUT, name + "_ckpt.npy")

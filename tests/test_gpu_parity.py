@@ -17,7 +17,7 @@ from helpers import assert_parity, parity_report, tie_free_prefix
 
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden", "oracle_runs")
-NETS = ["tiny", "medium", "large"]
+NETS = ["tiny", "medium", "large", "paper_small"]
 
 
 @pytest.fixture(scope="module")
@@ -340,7 +340,7 @@ def test_full_size_sampled_parity(torch_cuda):
     assert_parity(g, ref, o.blocks())
 
 
-@pytest.mark.parametrize("run", ["config1_seq", "config3_seq", "config2_seq"])
+@pytest.mark.parametrize("run", ["config1_seq", "config3_seq", "config2_seq", "paper_small_seq"])
 def test_hogwild_accuracy_gate(run, torch_cuda):
     # BASELINE.json north_star: hogwild test error within 0.5 pp of the oracle's sequential SGD
     import torch
@@ -353,7 +353,7 @@ def test_hogwild_accuracy_gate(run, torch_cuda):
     w = sd.WORKLOADS[rec["workload"]]
     d = sd.make_dataset(w)
     assert d.sha256() == rec["data_sha256"]
-    o, net, p = make(w.arch, w.seed, torch_cuda)
+    o, net, p = make(rec.get("arch", w.arch), w.seed, torch_cuda)
     X, Y, Xt, Yt = dev(torch, d.x_train, d.y_train, d.x_test, d.y_test)
     curve = []
     for e in range(w.epochs):
