@@ -170,6 +170,9 @@ def main():
                     help="hogwild (CHAOS, the headline) or the deterministic sync mode (multi-GPU: one "
                          "gradient all-reduce per global batch, SURVEY NEXT-4)")
     ap.add_argument("--sync-batch", type=int, default=64, help="global batch of --mode sync")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the multi-GPU leg (NCCL process group, configs[4] shards, averaging every K) "
+                         "even with one rank -- exercises the N>1 code path on one GPU")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -182,9 +185,10 @@ def main():
 
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
-    if world > 1:
+    distributed = world > 1 or args.force_dist
+    if distributed:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    if args.mode == "sync" and world > 1:
+    if args.mode == "sync" and distributed:
         # sync mode: every rank holds the global training set (60,000 per GPU, weak scaling) and
         # computes its contiguous part of every global batch
         wl = sd.WORKLOADS["config4"]
@@ -192,7 +196,7 @@ def main():
         xt, yt = sd.prototype_samples(wl.seed, wl.n_train, 10000)
         w = wl
     else:
-        w, xs, ys, xt, yt = make_data(world, rank)
+        w, xs, ys, xt, yt = make_data(world if not args.force_dist else max(world, 2), rank)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     net = Net(sd.ARCHS[args.arch], init_seed=w.seed, stream=stream)
@@ -201,7 +205,7 @@ def main():
     Y = torch.from_numpy(ys).cuda()
     Xt = torch.from_numpy(xt).cuda()
     Yt = torch.from_numpy(yt).cuda()
-    trainer = DistTrainer(net, rank, world, args.k)
+    trainer = DistTrainer(net, rank, world, args.k, force_collective=args.force_dist)
     grad_buf = torch.zeros_like(net.device_params()) if args.mode == "sync" else None
 
     def step(Xs, Ys, lr_s):
@@ -212,7 +216,7 @@ def main():
 
     def barrier():
         torch.cuda.synchronize()
-        if world > 1:
+        if distributed:
             dist.barrier(device_ids=[local])
 
     lr = w.lr0
@@ -239,7 +243,7 @@ def main():
     per_step_ms = [a.elapsed_time(b) for a, b in ev]
     launches = trainer.n_launches - launches0
     tmax = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
-    if world > 1:
+    if distributed:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     elapsed = float(tmax.item())
     total = PER_GPU * world * args.steps
@@ -264,7 +268,7 @@ def main():
     if not args.no_e2e:
         Xh = torch.from_numpy(xs).pin_memory()
         Yh = torch.from_numpy(ys).pin_memory()
-        host_entry = args.mode == "hogwild" and world == 1
+        host_entry = args.mode == "hogwild" and not distributed
         out_h = torch.zeros(1, dtype=torch.float32).pin_memory()
 
         def e2e_step(lr_s):
@@ -284,7 +288,7 @@ def main():
             e2e_step(lr * 0.5)
         barrier()
         dt = torch.tensor([time.perf_counter() - t], dtype=torch.float64, device="cuda")
-        if world > 1:
+        if distributed:
             dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         e2e = {"value": PER_GPU * world * args.steps / float(dt.item()), "unit": "samples/s",
                "h2d_bytes_per_step": int(Xh.numel() * 4 + Yh.numel() * 4),
@@ -293,10 +297,11 @@ def main():
                else "pinned H2D copy + step on the training stream"}
 
     if rank != 0:
-        dist.destroy_process_group()
+        if distributed:
+            dist.destroy_process_group()
         return
     # roofline of the dominant kernel: the persistent worker (one launch per step at N=1)
-    kern_s = statistics.median(per_step_ms) / 1e3 if world == 1 else elapsed / args.steps
+    kern_s = statistics.median(per_step_ms) / 1e3 if not distributed else elapsed / args.steps
     achieved = ALGO_FLOP[args.arch] * PER_GPU / kern_s / 1e12
     traffic = None
     tp = os.path.join(ROOT, "profiles", "latest_traffic.json")
@@ -311,15 +316,15 @@ def main():
         "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": (f"configs[3] {args.arch} net, hogwild (CHAOS), 60,000 images per GPU per step"
-                                + ("" if world == 1 else f"; configs[4] generator, NCCL average every {args.k}"))
+                                + ("" if not distributed else f"; configs[4] generator, NCCL average every {args.k}"))
                    if args.mode == "hogwild" else
                    (f"configs[3] {args.arch} net, deterministic sync SGD, global batch {args.sync_batch}, "
-                    f"60,000 images per GPU per step" + ("" if world == 1 else
+                    f"60,000 images per GPU per step" + ("" if not distributed else
                                                          "; one NCCL gradient all-reduce per batch")),
                    "arch": args.arch, "mode": args.mode, "images_per_gpu_per_step": PER_GPU,
                    "sync_batch": args.sync_batch if args.mode == "sync" else None,
                    "group_G": info["group"], "ctas": info["grid"], "threads_per_cta": info["block"],
-                   "smem_bytes_per_cta": info["smem_bytes"], "sync_interval_K": args.k if world > 1 else None,
+                   "smem_bytes_per_cta": info["smem_bytes"], "sync_interval_K": args.k if distributed else None,
                    "l2": "inputs (202 MB/GPU) larger than the 126 MB L2", "parallelism": f"dp{world}"},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic,
@@ -337,8 +342,11 @@ def main():
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.arch)
+    if args.force_dist:
+        line["config"]["force_dist"] = True
+        line["collectives"] = trainer.n_collectives
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
 
 

@@ -35,18 +35,18 @@ def batch_part(b0: int, nb: int, rank: int, world: int) -> tuple[int, int]:
     return b0 + nb * rank // world, b0 + nb * (rank + 1) // world
 
 
-def sum_(tensor, world: int, group=None):
+def sum_(tensor, world: int, group=None, force: bool = False):
     """In-place all-reduce sum (the sync-mode gradient exchange)."""
     import torch.distributed as dist
-    if world > 1:
+    if world > 1 or force:
         dist.all_reduce(tensor, op=dist.ReduceOp.SUM, group=group)
     return tensor
 
 
-def average_(tensor, world: int, group=None):
+def average_(tensor, world: int, group=None, force: bool = False):
     """In-place all-reduce average.  NCCL has ReduceOp.AVG; gloo does not (sum, then scale)."""
     import torch.distributed as dist
-    if world == 1:
+    if world == 1 and not force:
         return tensor
     if dist.get_backend(group) == "nccl":
         dist.all_reduce(tensor, op=dist.ReduceOp.AVG, group=group)
@@ -64,8 +64,11 @@ class DistTrainer:
     API) -- plus ``batch_gradient`` / ``apply_gradient`` for the sync mode; tests substitute a
     CPU stand-in with the same methods."""
 
-    def __init__(self, net, rank: int, world: int, k: int, group=None):
+    def __init__(self, net, rank: int, world: int, k: int, group=None, force_collective: bool = False):
+        """force_collective: run the K-interval schedule and the collectives even with one rank
+        (exercises the multi-GPU code path on one GPU)."""
         self.net, self.rank, self.world, self.k, self.group = net, rank, world, k, group
+        self.force = force_collective
         self.n_collectives = 0
         self.n_launches = 0
 
@@ -73,11 +76,12 @@ class DistTrainer:
         """One Training phase over this rank's images[lo:hi) (already sharded by the caller)."""
         hi = int(labels.shape[0]) if hi is None else hi
         params = self.net.device_params()
-        for s, e in intervals(lo, hi, self.k if self.world > 1 else 0):
+        multi = self.world > 1 or self.force
+        for s, e in intervals(lo, hi, self.k if multi else 0):
             self.net.train_epoch(images[s:e], labels[s:e], lr)
             self.n_launches += 1
-            if self.world > 1:
-                average_(params, self.world, self.group)
+            if multi:
+                average_(params, self.world, self.group, force=self.force)
                 self.n_collectives += 1
 
     def sync_epoch(self, images, labels, lr: float, batch: int, grad=None):
@@ -97,8 +101,8 @@ class DistTrainer:
             s, e = batch_part(b0, nb, self.rank, self.world)
             self.net.batch_gradient(images[s:e], labels[s:e], grad)
             self.n_launches += 2
-            if self.world > 1:
-                sum_(grad, self.world, self.group)
+            if self.world > 1 or self.force:
+                sum_(grad, self.world, self.group, force=self.force)
                 self.n_collectives += 1
             self.net.apply_gradient(grad, lr)
         return grad
