@@ -1949,6 +1949,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
     (void)L5;
 
     long long iter = 0;
+    long long next_claim = -1;  // hogwild: thread 0 claims the next group during the backward pass
     long long t_last = clock64();
     (void)t_last;
     for (;;) {
@@ -1956,7 +1957,8 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
         if (threadIdx.x == 0) {
             long long base;
             if constexpr (MODE == kHogwild)
-                base = static_cast<long long>(atomicAdd(a.counter, static_cast<unsigned long long>(G)));
+                base = next_claim >= 0 ? next_claim
+                                       : static_cast<long long>(atomicAdd(a.counter, static_cast<unsigned long long>(G)));
             else
                 base = (static_cast<long long>(blockIdx.x) + iter * gridDim.x) * G;
             *s_base = base < a.n ? static_cast<int>(base) : -1;
@@ -2075,6 +2077,9 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
         if constexpr (TRAIN) {
             __syncthreads();
             PTIME(6);
+            if constexpr (MODE == kHogwild)  // the claim's round trip overlaps the backward pass
+                if (threadIdx.x == 0)
+                    next_claim = static_cast<long long>(atomicAdd(a.counter, static_cast<unsigned long long>(G)));
             if (threadIdx.x == 0 && a.loss_sum) {
                 double ls = 0.0;
                 for (int g = 0; g < cnt; ++g) ls += s_loss[g];
