@@ -173,6 +173,11 @@ def main():
     ap.add_argument("--force-dist", action="store_true",
                     help="run the multi-GPU leg (NCCL process group, configs[4] shards, averaging every K) "
                          "even with one rank -- exercises the N>1 code path on one GPU")
+    ap.add_argument("--avg", default="async", choices=["interval", "async"],
+                    help="multi-GPU hogwild averaging: 'interval' = one launch per K images, then a blocking "
+                         "NCCL average; 'async' = one launch per shard with in-flight averages every K images on "
+                         "a second stream (SURVEY NEXT-2)")
+    ap.add_argument("--reserve-sms", type=int, default=4, help="--avg async: SMs left to the comm kernels")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -180,13 +185,20 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_1506_09067_b200 import HOGWILD, Net
+    from paper_1506_09067_b200 import HOGWILD, OPT_RESERVE_SMS, Net
     from paper_1506_09067_b200.dist import DistTrainer
 
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
     distributed = world > 1 or args.force_dist
     if distributed:
+        if "RANK" not in os.environ:  # --force-dist without a launcher: a one-rank group
+            import socket
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
+                              MASTER_PORT=str(sk.getsockname()[1]))
+            sk.close()
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if args.mode == "sync" and distributed:
         # sync mode: every rank holds the global training set (60,000 per GPU, weak scaling) and
@@ -200,6 +212,9 @@ def main():
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     net = Net(sd.ARCHS[args.arch], init_seed=w.seed, stream=stream)
+    use_async = distributed and args.mode == "hogwild" and args.avg == "async"
+    if use_async:
+        net.set_option(OPT_RESERVE_SMS, args.reserve_sms)
     info = net.launch_info()
     X = torch.from_numpy(xs).cuda()
     Y = torch.from_numpy(ys).cuda()
@@ -211,6 +226,8 @@ def main():
     def step(Xs, Ys, lr_s):
         if args.mode == "sync":
             trainer.sync_epoch(Xs, Ys, lr_s, args.sync_batch, grad_buf)
+        elif use_async:
+            trainer.epoch_async(Xs, Ys, lr_s)
         else:
             trainer.epoch(Xs, Ys, lr_s)
 
@@ -227,7 +244,7 @@ def main():
     clk = ClockSampler(local)
     clk.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    launches0 = trainer.n_launches
+    launches0 = trainer.n_launches + trainer.n_aux_launches
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     barrier()
@@ -241,7 +258,7 @@ def main():
     clocks = clk.stop()
     elapsed = t0.elapsed_time(t1) / 1e3
     per_step_ms = [a.elapsed_time(b) for a, b in ev]
-    launches = trainer.n_launches - launches0
+    launches = trainer.n_launches + trainer.n_aux_launches - launches0
     tmax = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
     if distributed:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
@@ -275,6 +292,10 @@ def main():
             if host_entry:
                 net.train_epoch_host(Xh, Yh, lr_s)
                 net.last_train_loss()
+            elif use_async:
+                trainer.epoch_async(X, Y, lr_s, host=(Xh, Yh))
+                out_h.copy_(net.device_params()[:1], non_blocking=True)
+                torch.cuda.current_stream().synchronize()
             else:
                 X.copy_(Xh, non_blocking=True)
                 Y.copy_(Yh, non_blocking=True)
@@ -294,6 +315,8 @@ def main():
                "h2d_bytes_per_step": int(Xh.numel() * 4 + Yh.numel() * 4),
                "d2h_bytes_per_step": 8 if host_entry else 4,
                "path": "chaos_train_epoch_host (C ABI, host buffers)" if host_entry
+               else "DistTrainer.epoch_async(host=...): pinned H2D chunks on a copy stream overlap the "
+                    "chunk launches" if use_async
                else "pinned H2D copy + step on the training stream"}
 
     if rank != 0:
@@ -316,7 +339,9 @@ def main():
         "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": (f"configs[3] {args.arch} net, hogwild (CHAOS), 60,000 images per GPU per step"
-                                + ("" if not distributed else f"; configs[4] generator, NCCL average every {args.k}"))
+                                + ("" if not distributed else f"; configs[4] generator, NCCL average every {args.k}"
+                                   + (f" images in flight (async, {args.reserve_sms} SMs reserved)" if use_async
+                                      else " images (blocking)")))
                    if args.mode == "hogwild" else
                    (f"configs[3] {args.arch} net, deterministic sync SGD, global batch {args.sync_batch}, "
                     f"60,000 images per GPU per step" + ("" if not distributed else
@@ -325,6 +350,7 @@ def main():
                    "sync_batch": args.sync_batch if args.mode == "sync" else None,
                    "group_G": info["group"], "ctas": info["grid"], "threads_per_cta": info["block"],
                    "smem_bytes_per_cta": info["smem_bytes"], "sync_interval_K": args.k if distributed else None,
+                   "averaging": (args.avg if distributed and args.mode == "hogwild" else None),
                    "l2": "inputs (202 MB/GPU) larger than the 126 MB L2", "parallelism": f"dp{world}"},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic,

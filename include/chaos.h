@@ -82,7 +82,9 @@ typedef enum {
     CHAOS_OPT_SYNC_BATCH = 1,    /* B >= 1, default 64 */
     CHAOS_OPT_GROUP = 2,         /* G, images per CTA per claim: compiled values 1 and the net's default */
     CHAOS_OPT_MAX_CTAS = 3,      /* cap on resident CTAs (1 => a single worker = sequential SGD when G=1) */
-    CHAOS_OPT_DEBUG_CLAIMS = 4   /* 1 => count claims per image into a device buffer (exactly-once test) */
+    CHAOS_OPT_DEBUG_CLAIMS = 4,  /* 1 => count claims per image into a device buffer (exactly-once test) */
+    CHAOS_OPT_RESERVE_SMS = 5    /* hogwild: leave this many SMs free of training CTAs (room for concurrent
+                                    averaging / NCCL kernels, chaos_progress_wait), in [0, #SMs), default 0 */
 } chaos_option;
 
 typedef struct chaos_net chaos_net;
@@ -142,6 +144,26 @@ chaos_status chaos_compute_gradients(chaos_net* net, const float* d_images, cons
 chaos_status chaos_batch_gradient(chaos_net* net, const float* d_images, const int32_t* d_labels, int64_t n,
                                   float* d_grad);
 chaos_status chaos_apply_gradient(chaos_net* net, const float* d_grad, float lr);
+
+/* Asynchronous cross-GPU averaging (the paper's "arbitrary order of
+ * synchronization" carried across GPUs).  While one hogwild
+ * launch trains on the net's stream, a caller-owned second stream (cast to int64_t) repeatedly
+ * waits for K more images of progress, snapshots the weights, all-reduces the snapshot (NCCL AVG,
+ * caller side) and adds (avg - snapshot) to the live weights, so the local updates made during the
+ * collective are kept.  None of these calls delays the training kernel.
+ * chaos_progress_enqueued: images enqueued to this net's hogwild launches since creation (host
+ *   counter, not synchronizing).  The device progress counter -- bumped by each CTA once a group's
+ *   updates are published -- reaches it when those launches complete.
+ * chaos_progress_wait: enqueue on `stream` one single-thread kernel that returns once the device
+ *   progress counter >= target.  target > chaos_progress_enqueued() is CHAOS_E_INVALID (it could
+ *   never return).  Runs beside the training kernel on a free SM (CHAOS_OPT_RESERVE_SMS).
+ * chaos_avg_snapshot: d_snap[0..chaos_net_device_params_len) = params (device copy on `stream`).
+ * chaos_avg_apply: params[j] += d_avg[j] - d_snap[j] over the internal layout with atomic adds on
+ *   `stream`, safe beside a running hogwild launch; d_avg/d_snap caller-owned, 16-B aligned. */
+uint64_t chaos_progress_enqueued(const chaos_net* net);
+chaos_status chaos_progress_wait(chaos_net* net, uint64_t target, int64_t stream);
+chaos_status chaos_avg_snapshot(chaos_net* net, float* d_snap, int64_t stream);
+chaos_status chaos_avg_apply(chaos_net* net, const float* d_avg, const float* d_snap, int64_t stream);
 
 /* Debug: copies the per-image claim counts of the last hogwild epoch (needs
  * CHAOS_OPT_DEBUG_CLAIMS=1 before the epoch) into host_counts[n]. */

@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("CHAOS_LIB") or os.path.join(HERE, "libchaos.so")
 CHAOS_CONV, CHAOS_MAXPOOL, CHAOS_FULL = 1, 2, 3
 CHAOS_TANH, CHAOS_IDENTITY = 0, 1
 HOGWILD, SYNC = 0, 1
-OPT_STREAM, OPT_SYNC_BATCH, OPT_GROUP, OPT_MAX_CTAS, OPT_DEBUG_CLAIMS = 0, 1, 2, 3, 4
+OPT_STREAM, OPT_SYNC_BATCH, OPT_GROUP, OPT_MAX_CTAS, OPT_DEBUG_CLAIMS, OPT_RESERVE_SMS = 0, 1, 2, 3, 4, 5
 STATUS = {0: "CHAOS_OK", -1: "CHAOS_E_INVALID", -2: "CHAOS_E_ARCH", -3: "CHAOS_E_UNSUPPORTED",
           -4: "CHAOS_E_LABEL", -5: "CHAOS_E_NONFINITE", -6: "CHAOS_E_CUDA", -7: "CHAOS_E_NCCL"}
 
@@ -29,7 +29,8 @@ EXPORTS = ["chaos_net_create", "chaos_net_destroy", "chaos_net_set_option", "cha
            "chaos_net_device_params_len", "chaos_train_epoch", "chaos_train_epoch_host", "chaos_last_train_loss",
            "chaos_evaluate", "chaos_forward", "chaos_compute_gradients", "chaos_debug_claims", "chaos_net_sync",
            "chaos_net_launch_info", "chaos_last_error", "chaos_last_status", "chaos_debug_phase_times",
-           "chaos_batch_gradient", "chaos_apply_gradient"]
+           "chaos_batch_gradient", "chaos_apply_gradient", "chaos_progress_enqueued", "chaos_progress_wait",
+           "chaos_avg_snapshot", "chaos_avg_apply"]
 
 
 class ChaosError(RuntimeError):
@@ -82,9 +83,13 @@ def lib():
             "chaos_last_error": ([], C.c_char_p),
             "chaos_last_status": ([], C.c_int),
             "chaos_debug_phase_times": ([vp, C.POINTER(C.c_uint64), C.c_int32], C.c_int),
+            "chaos_progress_enqueued": ([vp], C.c_uint64),
+            "chaos_progress_wait": ([vp, C.c_uint64, C.c_int64], C.c_int),
+            "chaos_avg_snapshot": ([vp, vp, C.c_int64], C.c_int),
+            "chaos_avg_apply": ([vp, vp, vp, C.c_int64], C.c_int),
         }
         for name, (args, res) in sig.items():
-            if name == "chaos_debug_phase_times" and os.environ.get("CHAOS_LIB") and not hasattr(L, name):
+            if os.environ.get("CHAOS_LIB") and not hasattr(L, name):
                 continue  # an older library picked for an A/B experiment
             f = getattr(L, name)
             f.argtypes = args
@@ -250,6 +255,21 @@ class Net:
     def apply_gradient(self, grad, lr):
         """chaos_apply_gradient: params -= lr * grad (internal layout); asynchronous."""
         _check(lib().chaos_apply_gradient(self._h, _ptr(grad), float(lr)))
+
+    def progress_enqueued(self) -> int:
+        """chaos_progress_enqueued: images enqueued to this net's hogwild launches so far."""
+        return int(lib().chaos_progress_enqueued(self._h))
+
+    def progress_wait(self, target, stream):
+        """chaos_progress_wait on a torch.cuda.Stream other than the net's."""
+        _check(lib().chaos_progress_wait(self._h, int(target), stream.cuda_stream))
+
+    def avg_snapshot(self, snap, stream):
+        _check(lib().chaos_avg_snapshot(self._h, _ptr(snap), stream.cuda_stream))
+
+    def avg_apply(self, avg, snap, stream):
+        """chaos_avg_apply: params += avg - snap (atomic, beside a running hogwild launch)."""
+        _check(lib().chaos_avg_apply(self._h, _ptr(avg), _ptr(snap), stream.cuda_stream))
 
     def debug_claims(self, n):
         out = np.zeros(n, np.int32)

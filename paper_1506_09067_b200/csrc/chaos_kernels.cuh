@@ -167,6 +167,7 @@ struct KArgs {
     unsigned char* out_wrong;    // eval: per-image error flag
     float* out_logits;           // forward: [n][kClasses]
     unsigned long long* ptime;   // CHAOS_TIMING builds: per-CTA clock64 cycles per phase [grid][kPhases]
+    unsigned long long* progress; // hogwild: monotonic count of images whose updates are published
 };
 
 // Phase timing (instrumented build only, -DCHAOS_TIMING): thread 0 adds the clock64 cycles
@@ -2236,6 +2237,8 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
 #ifndef CHAOS_NO_ITER_FENCE
             if constexpr (MODE == kHogwild) __threadfence();  // this worker's REDs precede its next reads
 #endif
+            if constexpr (MODE == kHogwild)  // progress for the asynchronous cross-GPU averaging
+                if (threadIdx.x == 0 && a.progress) atomicAdd(a.progress, static_cast<unsigned long long>(cnt));
         }
         __syncthreads();
         PTIME(15);
@@ -2263,6 +2266,27 @@ __global__ void chaos_apply_gradient_kernel(float* __restrict__ params, const fl
                                             long long np) {
     const long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j < np) params[j] = fmaf(-lr, grad[j], params[j]);
+}
+
+// Asynchronous cross-GPU averaging: w[j] += avg[j] - snap[j]
+// with vector REDs, so the local updates a running hogwild launch adds meanwhile are kept.
+__global__ void chaos_avg_apply_kernel(float* __restrict__ params, const float* __restrict__ avg,
+                                       const float* __restrict__ snap, long long np) {
+    const long long nq = np / 4;
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; q < nq; q += stride) {
+        const float4 x = reinterpret_cast<const float4*>(avg)[q], y = reinterpret_cast<const float4*>(snap)[q];
+        red_add4(params + 4 * q, make_float4(x.x - y.x, x.y - y.y, x.z - y.z, x.w - y.w));
+    }
+    for (long long j = 4 * nq + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; j < np; j += stride)
+        red_add(params + j, avg[j] - snap[j]);
+}
+
+// Returns once the hogwild progress counter reaches target (one thread; polls L2).  The training
+// kernel never waits on it, so it cannot deadlock: at worst it runs after the training launch.
+__global__ void chaos_progress_wait_kernel(const unsigned long long* progress, unsigned long long target) {
+    if (threadIdx.x != 0) return;
+    while (*reinterpret_cast<const volatile unsigned long long*>(progress) < target) __nanosleep(2000);
 }
 
 // Fixed-order evaluation reduction: one CTA of 1024 threads.

@@ -237,6 +237,9 @@ struct chaos_net {
     int group = 1;
     int max_ctas = 0;
     int debug_claims = 0;
+    int reserve_sms = 0;                   // hogwild: SMs left free of training CTAs
+    unsigned long long* progress = nullptr;  // device: images published by hogwild launches (monotonic)
+    unsigned long long progress_enqueued = 0; // host: images enqueued to hogwild launches
     int occ[2][4] = {};
     unsigned long long* ptime = nullptr;  // CHAOS_TIMING builds only
     int ptime_grid = 0;
@@ -264,7 +267,7 @@ chaos_status ensure_kernel_attrs(chaos_net* net) {
 }
 
 int grid_for(const chaos_net* net, int mode, long long work_groups) {
-    long long g = (long long)net->sms * net->occ[gidx(net)][mode];
+    long long g = (long long)(mode == kHogwild ? net->sms - net->reserve_sms : net->sms) * net->occ[gidx(net)][mode];
     if (mode == kHogwild && g * net->group > net->d->max_inflight) g = net->d->max_inflight / net->group;
     if (net->max_ctas > 0 && g > net->max_ctas) g = net->max_ctas;
     if (g > work_groups) g = work_groups;
@@ -482,6 +485,7 @@ chaos_net* chaos_net_create(const chaos_arch* arch) {
     if (cudaMalloc(&net->params, sizeof(float) * d->pint) != cudaSuccess ||
         cudaMalloc(&net->latch, sizeof(int)) != cudaSuccess ||
         cudaMalloc(&net->counter, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&net->progress, sizeof(unsigned long long)) != cudaSuccess ||
         cudaMalloc(&net->loss_sum, sizeof(double)) != cudaSuccess ||
         cudaMalloc(&net->ev_sum, sizeof(double)) != cudaSuccess ||
         cudaMalloc(&net->ev_err, sizeof(long long)) != cudaSuccess) {
@@ -489,6 +493,7 @@ chaos_net* chaos_net_create(const chaos_arch* arch) {
         return bail(CHAOS_E_CUDA);
     }
     cudaMemset(net->latch, 0, sizeof(int));
+    cudaMemset(net->progress, 0, sizeof(unsigned long long));
     cudaMemset(net->loss_sum, 0, sizeof(double));
     // parameters: U(-1/sqrt(fan_in), +1/sqrt(fan_in)), W then b per layer, splitmix64(seed ^ 0x5EED)
     std::vector<float> norm((size_t)d->nparams);
@@ -513,7 +518,8 @@ void chaos_net_destroy(chaos_net* net) {
     if (net->staging_free) cudaEventDestroy(net->staging_free);
     for (cudaEvent_t e : net->chunk_ev) cudaEventDestroy(e);
     void* ptrs[] = {net->params, net->latch,  net->counter, net->loss_sum, net->partial, net->grad_out, net->claims,
-                    net->ev_loss, net->ev_wrong, net->ev_sum, net->ev_err, net->st_x, net->st_y, net->ptime};
+                    net->ev_loss, net->ev_wrong, net->ev_sum, net->ev_err, net->st_x, net->st_y, net->ptime,
+                    net->progress};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     delete net;
@@ -541,6 +547,10 @@ chaos_status chaos_net_set_option(chaos_net* net, chaos_option opt, int64_t valu
         case CHAOS_OPT_DEBUG_CLAIMS:
             net->debug_claims = value ? 1 : 0;
             return CHAOS_OK;
+        case CHAOS_OPT_RESERVE_SMS:
+            if (value < 0 || value >= net->sms) return fail(CHAOS_E_INVALID, "reserve_sms must be in [0, %d)", net->sms);
+            net->reserve_sms = (int)value;
+            return CHAOS_OK;
     }
     return fail(CHAOS_E_INVALID, "unknown option %d", (int)opt);
 }
@@ -553,6 +563,7 @@ int64_t chaos_net_get_option(const chaos_net* net, chaos_option opt) {
         case CHAOS_OPT_GROUP: return net->group;
         case CHAOS_OPT_MAX_CTAS: return net->max_ctas;
         case CHAOS_OPT_DEBUG_CLAIMS: return net->debug_claims;
+        case CHAOS_OPT_RESERVE_SMS: return net->reserve_sms;
     }
     return -1;
 }
@@ -618,6 +629,8 @@ chaos_status train_range(chaos_net* net, const float* d_images, const int32_t* d
         CUDA_TRY(cudaMemsetAsync(net->ptime, 0, sizeof(unsigned long long) * kPhases * net->ptime_grid, net->stream));
         k.ptime = net->ptime;
 #endif
+        k.progress = net->progress;
+        net->progress_enqueued += (unsigned long long)n;
         net->d->fn[gidx(net)][kHogwild]<<<grid, net->d->nt, net->d->smem[gidx(net)], net->stream>>>(k);
         CUDA_TRY(cudaGetLastError());
         return CHAOS_OK;
@@ -799,6 +812,37 @@ chaos_status chaos_apply_gradient(chaos_net* net, const float* d_grad, float lr)
     if (!std::isfinite(lr)) return fail(CHAOS_E_INVALID, "lr is not finite");
     const long long np = net->d->pint;
     chaos_apply_gradient_kernel<<<(unsigned)((np + 255) / 256), 256, 0, net->stream>>>(net->params, d_grad, lr, np);
+    CUDA_TRY(cudaGetLastError());
+    return CHAOS_OK;
+}
+
+uint64_t chaos_progress_enqueued(const chaos_net* net) { return net ? net->progress_enqueued : 0; }
+
+chaos_status chaos_progress_wait(chaos_net* net, uint64_t target, int64_t stream) {
+    if (!net) return fail(CHAOS_E_INVALID, "net is NULL");
+    if (target > net->progress_enqueued)
+        return fail(CHAOS_E_INVALID, "progress target %llu beyond the %llu images enqueued (would never return)",
+                    (unsigned long long)target, net->progress_enqueued);
+    chaos_progress_wait_kernel<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(net->progress, target);
+    CUDA_TRY(cudaGetLastError());
+    return CHAOS_OK;
+}
+
+chaos_status chaos_avg_snapshot(chaos_net* net, float* d_snap, int64_t stream) {
+    if (!net || !d_snap) return fail(CHAOS_E_INVALID, "NULL argument");
+    CUDA_TRY(cudaMemcpyAsync(d_snap, net->params, sizeof(float) * net->d->pint, cudaMemcpyDeviceToDevice,
+                             reinterpret_cast<cudaStream_t>(stream)));
+    return CHAOS_OK;
+}
+
+chaos_status chaos_avg_apply(chaos_net* net, const float* d_avg, const float* d_snap, int64_t stream) {
+    if (!net || !d_avg || !d_snap) return fail(CHAOS_E_INVALID, "NULL argument");
+    if ((reinterpret_cast<uintptr_t>(d_avg) | reinterpret_cast<uintptr_t>(d_snap)) & 15)
+        return fail(CHAOS_E_INVALID, "avg/snap must be 16-byte aligned");
+    const long long np = net->d->pint;
+    const long long blocks = std::min<long long>((np / 4 + 255) / 256 + 1, 64);
+    chaos_avg_apply_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(net->params, d_avg,
+                                                                                                  d_snap, np);
     CUDA_TRY(cudaGetLastError());
     return CHAOS_OK;
 }

@@ -30,6 +30,12 @@ def n_averages(n_local: int, k: int) -> int:
     return len(intervals(0, n_local, k))
 
 
+def async_targets(n_local: int, k: int) -> list[int]:
+    """Progress points (images into the shard) of the in-flight averages of ``epoch_async``:
+    k, 2k, ... strictly inside the shard; the end of the shard gets the final, exact average."""
+    return list(range(k, n_local, k)) if k > 0 else []
+
+
 def batch_part(b0: int, nb: int, rank: int, world: int) -> tuple[int, int]:
     """Rank r's contiguous part [s, e) of the global sync batch [b0, b0 + nb) (fixed split)."""
     return b0 + nb * rank // world, b0 + nb * (rank + 1) // world
@@ -71,18 +77,129 @@ class DistTrainer:
         self.force = force_collective
         self.n_collectives = 0
         self.n_launches = 0
+        self.n_aux_launches = 0  # epoch_async: progress-wait + apply kernels
+        self._agreed_cache = {}
+
+    def _agreed(self, n_local: int, op: str) -> int:
+        """MIN / MAX of the shard length over ranks (cached per length): the number of
+        collectives per epoch must be the same on every rank even when shard sizes differ."""
+        key = (n_local, op)
+        if key not in self._agreed_cache:
+            import torch
+            import torch.distributed as dist
+            on_gpu = dist.get_backend(self.group) == "nccl"
+            t = torch.tensor([n_local], dtype=torch.int64, device="cuda" if on_gpu else "cpu")
+            dist.all_reduce(t, op=dist.ReduceOp.MIN if op == "min" else dist.ReduceOp.MAX, group=self.group)
+            self._agreed_cache[key] = int(t.item())
+        return self._agreed_cache[key]
 
     def epoch(self, images, labels, lr: float, lo: int = 0, hi: int | None = None):
-        """One Training phase over this rank's images[lo:hi) (already sharded by the caller)."""
+        """One Training phase over this rank's images[lo:hi) (already sharded by the caller):
+        one launch per interval of K images, each followed by a blocking average.  Every rank runs
+        ceil(max shard / K) intervals (a shorter shard ends with empty ones) so the collectives
+        match."""
         hi = int(labels.shape[0]) if hi is None else hi
         params = self.net.device_params()
         multi = self.world > 1 or self.force
-        for s, e in intervals(lo, hi, self.k if multi else 0):
-            self.net.train_epoch(images[s:e], labels[s:e], lr)
-            self.n_launches += 1
+        if not multi or self.k <= 0:
+            if hi > lo:
+                self.net.train_epoch(images[lo:hi], labels[lo:hi], lr)
+                self.n_launches += 1
             if multi:
                 average_(params, self.world, self.group, force=self.force)
                 self.n_collectives += 1
+            return
+        count = max(1, -(-self._agreed(hi - lo, "max") // self.k))
+        for i in range(count):
+            s, e = lo + i * self.k, min(lo + (i + 1) * self.k, hi)
+            if e > s:
+                self.net.train_epoch(images[s:e], labels[s:e], lr)
+                self.n_launches += 1
+            average_(params, self.world, self.group, force=self.force)
+            self.n_collectives += 1
+
+    def _launch(self, images, labels, lr, lo, hi, host, chunks):
+        """Training launch(es) over [lo, hi) on the net's stream.  host = pinned CPU (images,
+        labels) of the same rows: the rows are copied into images/labels in `chunks` pieces on a
+        copy stream and each piece trains as soon as its own copy has landed (the H2D transfer
+        overlaps training -- the end-to-end path; one launch per piece)."""
+        if hi <= lo:
+            return
+        if host is None:
+            self.net.train_epoch(images[lo:hi], labels[lo:hi], lr)
+            self.n_launches += 1
+            return
+        import torch
+        ts = self.net.stream
+        if getattr(self, "_copy_stream", None) is None:
+            self._copy_stream = torch.cuda.Stream()
+        cps = self._copy_stream
+        cps.wait_stream(ts)  # earlier launches no longer read the buffers being overwritten
+        step = max(4, -(-(hi - lo) // chunks) // 4 * 4)
+        for s in range(lo, hi, step):
+            e = min(s + step, hi)
+            with torch.cuda.stream(cps):
+                images[s:e].copy_(host[0][s:e], non_blocking=True)
+                labels[s:e].copy_(host[1][s:e], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cps)
+            ts.wait_event(ev)
+            self.net.train_epoch(images[s:e], labels[s:e], lr)
+            self.n_launches += 1
+
+    def epoch_async(self, images, labels, lr: float, lo: int = 0, hi: int | None = None, host=None,
+                    chunks: int = 8):
+        """One Training phase with asynchronous averaging:
+        ONE hogwild launch over the whole shard on the net's stream (run with
+        CHAOS_OPT_RESERVE_SMS > 0 so the comm kernels find free SMs), and on a second stream, for
+        every target t in ``async_targets`` of the shortest shard (the collective count must match on
+        every rank): wait until the device progress counter has passed t
+        images, snapshot the weights, all-reduce the snapshot (average), add (avg - snapshot) to
+        the live weights -- local updates made during the collective are kept (the CHAOS
+        "arbitrary order of synchronization", across replicas).  After the launch
+        completes, one exact in-place average leaves every rank with identical weights.  Sum over
+        ranks of the weights is preserved by every in-flight average (each adds P*avg - sum snap
+        = 0), so with additive updates the final weights equal the mean of the replicas' total
+        progress, whatever the timing.  No K-interval tail: the kernel never drains mid-shard.
+        ``host``/``chunks``: see ``_launch`` (the progress counter spans the chunk launches)."""
+        import contextlib
+
+        import torch
+        hi = int(labels.shape[0]) if hi is None else hi
+        net = self.net
+        params = net.device_params()
+        if not (self.world > 1 or self.force):
+            self._launch(images, labels, lr, lo, hi, host, chunks)
+            return
+        cuda = params.is_cuda
+        if getattr(self, "_async_bufs", None) is None:
+            self._async_bufs = (torch.empty_like(params), torch.empty_like(params),
+                                torch.cuda.Stream() if cuda else None)
+        snap, avg, cs = self._async_bufs
+        ts = net.stream if cuda else None
+        scope = torch.cuda.stream(cs) if cuda else contextlib.nullcontext()
+        if cuda:
+            cs.wait_stream(ts)  # earlier work on the weights precedes this epoch's snapshots
+        n_min = self._agreed(hi - lo, "min")  # before the launch: its host sync must not stall the comm stream
+        base = net.progress_enqueued()
+        self._launch(images, labels, lr, lo, hi, host, chunks)
+        with scope:
+            for t in async_targets(n_min, self.k):
+                net.progress_wait(base + t, cs)
+                net.avg_snapshot(snap, cs)
+                avg.copy_(snap)
+                average_(avg, self.world, self.group, force=self.force)
+                net.avg_apply(avg, snap, cs)
+                self.n_collectives += 1
+                self.n_aux_launches += 2
+            if cuda:
+                cs.wait_stream(ts)  # the launch has completed
+            else:
+                net.sync()
+            average_(params, self.world, self.group, force=self.force)
+            self.n_collectives += 1
+        if cuda:
+            ts.wait_stream(cs)
 
     def sync_epoch(self, images, labels, lr: float, batch: int, grad=None):
         """Deterministic multi-GPU sync SGD: for every consecutive global

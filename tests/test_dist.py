@@ -15,7 +15,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1506_09067_b200.dist import DistTrainer, batch_part, intervals, n_averages, shard_range
+from paper_1506_09067_b200.dist import DistTrainer, async_targets, batch_part, intervals, n_averages, shard_range
 
 
 def test_shard_range_partitions_and_aligns():
@@ -197,3 +197,147 @@ def test_gloo_world2_sync_epoch_equals_single_process():
         assert ncoll == 5  # one all-reduce per batch (37 = 4*8 + 5)
         np.testing.assert_allclose(wr, w.numpy(), rtol=1e-12)
     np.testing.assert_array_equal(out[0][1], out[1][1])  # replicas stay bitwise identical
+
+
+def test_async_targets():
+    assert async_targets(10, 4) == [4, 8]
+    assert async_targets(8, 4) == [4]          # the shard end gets the final exact average
+    assert async_targets(3, 4) == [] and async_targets(10, 0) == []
+    assert len(async_targets(7500, 1024)) + 1 == n_averages(7500, 1024)
+
+
+class FakeAsyncNet(FakeNet):
+    """Stand-in for the asynchronous-averaging API: train_epoch only enqueues (as the real launch
+    is asynchronous); progress_wait(t) lets the 'device' train up to image t; avg_apply first lets
+    `lag` more images train -- local progress made while the collective ran -- then adds
+    avg - snap.  Every image adds lr*(rank+1)*3 to every weight (all-ones rows of 3 features)."""
+
+    stream = None
+
+    def __init__(self, n, rank, lag):
+        super().__init__(n, rank)
+        self.lag, self.enq, self.done, self.lr = lag, 0, 0, 0.0
+        self.residual = []
+
+    def progress_enqueued(self):
+        return self.enq
+
+    def train_epoch(self, images, labels, lr):
+        assert self.done == self.enq  # the previous epoch completed (final average waited for it)
+        self.calls.append(int(labels.shape[0]))
+        self.enq += int(labels.shape[0])
+        self.lr = lr
+
+    def _advance(self, t):
+        t = min(t, self.enq)
+        self.w += (t - self.done) * self.lr * (self.rank + 1) * 3
+        self.done = max(self.done, t)
+
+    def progress_wait(self, target, stream):
+        assert target <= self.enq
+        self._advance(target)
+
+    def avg_snapshot(self, snap, stream):
+        snap.copy_(self.w)
+
+    def avg_apply(self, avg, snap, stream):
+        d0 = self.done
+        self._advance(self.done + self.lag)
+        self.w += avg - snap
+        # weights after the apply minus the average: exactly the local progress since the snapshot
+        self.residual.append((self.w - avg).max().item() - (self.done - d0) * self.lr * (self.rank + 1) * 3)
+
+    def sync(self):
+        self._advance(self.enq)
+
+
+def _async_worker(rank, world, port, k, lr, lag, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = 1000
+        lo, hi = shard_range(n, rank, world)
+        X = torch.ones(n, 3)
+        Y = torch.zeros(n, dtype=torch.int32)
+        net = FakeAsyncNet(16, rank, lag)
+        net.w = net.w.double()
+        w0 = net.w.clone()
+        tr = DistTrainer(net, rank, world, k)
+        for _ in range(2):
+            tr.epoch_async(X, Y, lr, lo, hi)
+        gathered = [torch.zeros_like(net.w) for _ in range(world)]
+        dist.all_gather(gathered, net.w)
+        q.put((rank, net.calls, tr.n_collectives, w0.numpy(), [g.numpy() for g in gathered], net.residual))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("lag", [0, 37])
+def test_gloo_world2_async_average(lag):
+    """NEXT-2: in-flight averages keep the local progress made during the collective (the
+    sum over ranks is preserved), the final average leaves identical replicas, and the result is
+    the mean of the replicas' total progress whatever the timing (additive updates)."""
+    world, k, lr = 2, 128, 0.01
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_async_worker, args=(r, world, port, k, lr, lag, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=120) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    sizes = [shard_range(1000, r, world) for r in range(world)]
+    for rank, calls, ncoll, w0, gathered, residual in out:
+        lo, hi = sizes[rank]
+        assert len(residual) == 2 * len(async_targets(hi - lo, k)) and max(map(abs, residual)) < 1e-9
+        assert calls == [hi - lo, hi - lo]  # one launch per epoch, no K-interval split
+        assert ncoll == 2 * (len(async_targets(hi - lo, k)) + 1)
+        np.testing.assert_array_equal(gathered[1], gathered[0])
+    expect = out[0][3] + 2 * np.mean([(hi - lo) * lr * (r + 1) * 3 for r, (lo, hi) in enumerate(sizes)])
+    np.testing.assert_allclose(out[0][4][0], expect, rtol=1e-12)
+
+
+def _uneven_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # shards of 1025 and 1021 images: ceil(n/K) differs per rank at K = 1024
+        edges = [(0, 1025), (1025, 2046)]
+        lo, hi = edges[rank]
+        X = torch.ones(2046, 3)
+        Y = torch.zeros(2046, dtype=torch.int32)
+        out = []
+        for kind in ("interval", "async"):
+            net = FakeAsyncNet(8, rank, 5) if kind == "async" else FakeNet(8, rank)
+            net.w = net.w.double()
+            tr = DistTrainer(net, rank, world, 1024)
+            (tr.epoch_async if kind == "async" else tr.epoch)(X, Y, 0.01, lo, hi)
+            gathered = [torch.zeros_like(net.w) for _ in range(world)]
+            dist.all_gather(gathered, net.w)
+            out.append((kind, tr.n_collectives, sum(net.calls), [g.numpy() for g in gathered]))
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_uneven_shards_agree_on_collective_count():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_uneven_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(2)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for (_, a), (_, b) in [(res[0], res[1])]:
+        for (kind, nc0, n0, g0), (_, nc1, n1, _) in zip(a, b):
+            assert nc0 == nc1, kind  # 2 intervals on both ranks; async: no in-flight average
+            assert (n0, n1) == (1025, 1021)
+            np.testing.assert_array_equal(g0[0], g0[1])
+    assert [o[1] for o in res[0][1]] == [2, 1]

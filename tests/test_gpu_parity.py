@@ -414,27 +414,33 @@ def test_two_rank_sync_emulated_matches_oracle(torch_cuda):
     assert_parity(runs[0], ref, o.blocks())
 
 
-@pytest.mark.parametrize("mode", ["hogwild", "sync"])
+@pytest.mark.parametrize("mode", ["hogwild", "sync", "hogwild_dist"])
 def test_bench_line_contract(mode, torch_cuda):
     # bench.py's JSON line on one GPU: contract keys, roofline + cpu_baseline objects, e2e with host bytes
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    cmd = [sys.executable, os.path.join(root, "bench.py"), "--steps", "1", "--warmup", "1", "--mode", mode]
-    if mode == "sync":
+    cmd = [sys.executable, os.path.join(root, "bench.py"), "--steps", "1", "--warmup", "1",
+           "--mode", mode.split("_")[0]]
+    if mode != "hogwild":
         cmd.append("--no-cpu-baseline")
+    if mode == "hogwild_dist":  # the N>1 code path on one GPU: one-rank NCCL group, async averaging
+        cmd.append("--force-dist")
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
     assert out.returncode == 0, out.stderr[-3000:]
     d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
               "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "clocks", "gpu_launches", "e2e"):
         assert k in d, k
-    assert d["value"] > 0 and d["gpu_launches"] >= 1 and d["config"]["mode"] == mode
+    assert d["value"] > 0 and d["gpu_launches"] >= 1 and d["config"]["mode"] == mode.split("_")[0]
     r = d["roofline"]
     assert r["bound"] == "alu" and 0 < r["frac"] < 1 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
     assert d["e2e"]["h2d_bytes_per_step"] == 60000 * (841 + 1) * 4
     if mode == "hogwild":
         assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
+    if mode == "hogwild_dist":
+        assert d["config"]["averaging"] == "async" and d["collectives"] >= 2
+        assert d["eval"]["test_errors"] < 0.05 * d["eval"]["images"]
 
 
 def test_host_entry_hogwild_chunks_are_the_same_run(torch_cuda):
@@ -475,3 +481,87 @@ def test_staleness_cap(torch_cuda):
             info = net.launch_info()
             assert info["grid"] * info["group"] <= cap, (name, g, info)
             net.close()
+
+
+def test_avg_apply_snapshot_and_progress_abi(torch_cuda):
+    # NEXT-2 building blocks (include/chaos.h): snapshot = params; apply adds avg - snap with the
+    # same fp32 roundings as torch; the progress counter counts every enqueued image; waits up to
+    # it return (on a side stream, beside the training launch), beyond it are refused
+    import torch
+    from paper_1506_09067_b200 import OPT_RESERVE_SMS, ChaosError
+    _, net, _ = make("large", 3, torch_cuda)
+    side = torch.cuda.Stream()
+    params = net.device_params()
+    snap = torch.empty_like(params)
+    net.avg_snapshot(snap, side)
+    side.synchronize()
+    assert torch.equal(snap, params)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    avg = snap + 1e-3 * torch.randn(snap.shape, generator=g, device="cuda")
+    expect = params + (avg - snap)
+    net.avg_apply(avg, snap, side)
+    side.synchronize()
+    assert torch.equal(params, expect)
+    w = sd.WORKLOADS["config3"]
+    xs, ys = sd.prototype_samples(w.seed, 0, 6001)
+    X, Y = dev(torch, xs, ys)
+    assert net.progress_enqueued() == 0
+    net.train_epoch(X, Y, 0.001)
+    net.train_epoch(X[:5], Y[:5], 0.001)
+    assert net.progress_enqueued() == 6006
+    net.progress_wait(6006, side)
+    side.synchronize()  # returned: every image's updates are published
+    with pytest.raises(ChaosError):
+        net.progress_wait(6007, side)
+    net.set_option(OPT_RESERVE_SMS, 4)
+    assert net.launch_info()["grid"] == torch.cuda.get_device_properties(0).multi_processor_count - 4
+    with pytest.raises(ChaosError):
+        net.set_option(OPT_RESERVE_SMS, 100000)
+    net.close()
+
+
+def test_async_averaging_runs_in_flight(torch_cuda):
+    # NEXT-2: with 4 SMs reserved, the progress waits on the comm stream return while the one
+    # training launch runs (spread over it, not bunched at its end), and snapshot + zero-delta
+    # apply in flight leave hogwild training intact (the config3 accuracy gate still holds)
+    import torch
+    from paper_1506_09067_b200 import OPT_RESERVE_SMS
+    path = os.path.join(GOLD, "config3_seq.json")
+    if not os.path.exists(path):
+        pytest.skip("oracle reference run config3_seq not recorded")
+    rec = json.load(open(path))
+    w = sd.WORKLOADS[rec["workload"]]
+    d = sd.make_dataset(w)
+    _, net, _ = make(rec.get("arch", w.arch), w.seed, torch_cuda)
+    net.set_option(OPT_RESERVE_SMS, 4)
+    X, Y, Xt, Yt = dev(torch, d.x_train, d.y_train, d.x_test, d.y_test)
+    side = torch.cuda.Stream()
+    params = net.device_params()
+    snap = torch.empty_like(params)
+    n, k = int(Y.shape[0]), 1024
+    spreads = []
+    for e in range(w.epochs):
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        side.wait_stream(net.stream)
+        base = net.progress_enqueued()
+        t0.record(net.stream)
+        net.train_epoch(X, Y, w.lr0 * 0.9 ** e)
+        t1.record(net.stream)
+        marks = []
+        for t in range(k, n, k):
+            net.progress_wait(base + t, side)
+            m = torch.cuda.Event(enable_timing=True)
+            m.record(side)
+            marks.append(m)
+            net.avg_snapshot(snap, side)
+            net.avg_apply(snap, snap, side)  # zero delta
+        net.stream.wait_stream(side)
+        torch.cuda.synchronize()
+        total = t0.elapsed_time(t1)
+        spreads.append(marks[0].elapsed_time(marks[-1]) / total)
+    assert min(spreads) > 0.5, spreads
+    ml, ne = net.evaluate(Xt, Yt)
+    ref = rec["per_epoch"][-1]
+    assert abs(ne - ref["test_errors"]) / len(d.y_test) * 100 <= 0.5, (ne, ref)
+    net.close()
