@@ -37,7 +37,10 @@ N_SM = 148
 FP32_PEAK_TFLOPS = N_SM * 128 * 2 * 1.965e9 / 1e12
 # algorithmic FLOP per training image: forward of the conv outputs
 # the pools use, argmax-only backward (gW and delta_in), 2 FLOP per parameter for the update
-ALGO_FLOP = {"tiny": 202_990, "medium": 4_985_880, "large": 5_495_720}
+ALGO_FLOP = {"tiny": 202_990, "medium": 4_985_880, "large": 5_495_720,
+             # Table I large (NEXT-1): 34,286,140 MAC (fwd 22,648,820; bwd 11,637,320) + 2 x 383,160
+             "paper_large": 69_338_600}
+KERNEL_NET = {"tiny": "TinyNet", "medium": "MediumNet", "large": "LargeNet", "paper_large": "PaperLargeNet"}
 
 
 def env_rank():
@@ -161,7 +164,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--arch", default="large", choices=["tiny", "medium", "large"])
+    ap.add_argument("--arch", default="large", choices=["tiny", "medium", "large", "paper_large"])
     ap.add_argument("--k", type=int, default=K_AVG)
     ap.add_argument("--ref-images", type=int, default=400)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -354,7 +357,7 @@ def main():
                    "l2": "inputs (202 MB/GPU) larger than the 126 MB L2", "parallelism": f"dp{world}"},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic,
-                     "kernel": f"chaos_worker<{args.arch.capitalize()}Net,{info['group']},{info['block']},"
+                     "kernel": f"chaos_worker<{KERNEL_NET[args.arch]},{info['group']},{info['block']},"
                                f"{'kHogwild' if args.mode == 'hogwild' else 'kSync'}>",
                      "flop_per_image": ALGO_FLOP[args.arch],
                      "peak_source": "148 SM x 128 FFMA/clk x 2 x 1.965 GHz (unit counts x max clock)"},

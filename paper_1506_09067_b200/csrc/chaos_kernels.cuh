@@ -29,6 +29,7 @@
 //          tanh-fed inputs multiply by (1 - a^2); pool routes delta to the argmax only.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace chaos {
@@ -42,6 +43,18 @@ enum Mode : int { kHogwild = 0, kSync = 1, kEval = 2, kForward = 3 };
 enum Latch : int { kLatchLabel = 1, kLatchNonfinite = 2 };
 
 __host__ __device__ constexpr int round4(int x) { return (x + 3) / 4 * 4; }
+
+// Nets whose conv3 / FC1 weights are too large to stage in shared memory (Table I large net,
+// SURVEY NEXT-1) declare BIGW = true: W1 + W2 are staged once per iteration and kept; conv3
+// and FC1 weights are read from L2 on demand.
+template <class N, class = void>
+struct BigW {
+    static constexpr bool value = false;
+};
+template <class N>
+struct BigW<N, std::void_t<decltype(N::BIGW)>> {
+    static constexpr bool value = N::BIGW;
+};
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 
 // Convolution block: conv (valid, stride 1, C->M maps, KxK) -> tanh -> KPxKP max-pool (floor).
@@ -129,12 +142,13 @@ struct SLayout {
     using C2 = typename Net::C2;
     using C3 = typename Net::C3;
     using F1 = typename Net::F1;
-    static constexpr int WBUF = round4(cmax(
-        cmax(cmax(C1::BLK + (Net::NCONV >= 2 ? C2::BLK : 0), C1::GW_SCRATCH),
-             Net::NCONV >= 3 ? 2 * C2::BLK : 0),
-        Net::NCONV >= 3 ? C3::BLK : 0));
+    static constexpr bool BIG = BigW<Net>::value;
+    static constexpr int WBUF = BIG ? round4(cmax(round4(C1::BLK) + C2::BLK, C1::GW_SCRATCH))
+                                    : round4(cmax(cmax(cmax(C1::BLK + (Net::NCONV >= 2 ? C2::BLK : 0), C1::GW_SCRATCH),
+                                                       Net::NCONV >= 3 ? 2 * C2::BLK : 0),
+                                                  Net::NCONV >= 3 ? C3::BLK : 0));
     static constexpr int SFL = round4(cmax(cmax(G * C1::IN_SZ, Net::SFL),
-                                           Net::NCONV >= 3 ? G * C2::OUT_SZ : 0));
+                                           (Net::NCONV >= 3 && !BIG) ? G * C2::OUT_SZ : 0));
     static constexpr int S = 0;
     static constexpr int A1 = S + SFL;
     static constexpr int A2 = A1 + round4(G * C1::OUT_SZ);
@@ -145,7 +159,7 @@ struct SLayout {
     static constexpr int WB = BS + kBiasScratch;
     static constexpr int FLOATS = WB + WBUF;
     static constexpr int AM1 = 0;  // argmax bytes
-    static constexpr int AM2 = AM1 + (G * C1::OUT_SZ + 15) / 16 * 16;
+    static constexpr int AM2 = AM1 + (C1::KP > 1 ? (G * C1::OUT_SZ + 15) / 16 * 16 : 0);  // pool 1x1: no argmax
     static constexpr int AM3 = AM2 + (Net::NCONV >= 2 ? (G * C2::OUT_SZ + 15) / 16 * 16 : 0);
     static constexpr int AMB = AM3 + (Net::NCONV >= 3 ? (G * C3::OUT_SZ + 15) / 16 * 16 : 0);
     static constexpr int BYTES = kHdrBytes + FLOATS * 4 + AMB;
@@ -463,7 +477,7 @@ __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const flo
                 }
             const int o = g * L::OUT_SZ + (mg * MT + mt) * P + p;
             out[o] = tanhf(best);
-            am[o] = static_cast<uint8_t>(arg);
+            if constexpr (KP > 1) am[o] = static_cast<uint8_t>(arg);
         }
     }
 }
@@ -491,10 +505,13 @@ __device__ __forceinline__ void conv_gw(const KArgs& a, int slot, const float* _
     const int span = cnt * P;
     const int total = C * M * TG * GS;
     for (int it = threadIdx.x; it < total; it += NT) {
-        const int n = it % C;
-        int r = it / C;
-        const int m = r % M;
-        r /= M;
+        // SCRATCH: n fastest (gathers from different maps, conflict-free); direct publish: m
+        // fastest, so a warp's reductions hit consecutive weights (coalesced) and its gathers
+        // come from one map (at most KP*KP distinct addresses per load)
+        const int n = SCRATCH ? it % C : (it / M) % C;
+        int r = SCRATCH ? it / C : it / (M * C);
+        const int m = SCRATCH ? r % M : it % M;
+        if constexpr (SCRATCH) r /= M;
         const int tg = r % TG;
         const int s = r / TG;
         const int q0 = (GS == 1) ? 0 : (span * s) / GS;
@@ -511,7 +528,8 @@ __device__ __forceinline__ void conv_gw(const KArgs& a, int slot, const float* _
 #pragma unroll 4
         for (int q = q0; q < q1; ++q) {
             const float d = dpg[pp];
-            const int arg = amg[pp];
+            int arg = 0;
+            if constexpr (KP > 1) arg = amg[pp];
             const int pr = pp / PW, pc = pp - (pp / PW) * PW;
             const float* base = ing + (pr * KP + arg / KP) * L::W + pc * KP + arg % KP;
 #pragma unroll
@@ -965,6 +983,91 @@ __device__ __forceinline__ void conv_din(const float* __restrict__ wsm, const fl
                 }
             }
         }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// PHASE(conv_din_gm) partial derivatives of the previous layer with the weights read from
+// global memory (a layer too large to stage: the Table I large net's conv3, 864 KB; with
+// GLOBALW = false the same loop over a staged block -- its conv2, whose 20 input maps would
+// leave lanes idle and give too few warp tasks in conv_din):
+//   dout[g][n][y][x] = (1 - in^2) * sum_m sum_pp [tap in range] W[n][y-r][x-c][m] dp[g][m][pp]
+// One warp per (image g, input map n, band of RB input rows); lanes over output maps m, so
+// each weight load is one coalesced row segment W[n][tap][m..m+31] (__ldcg: L2, coherent with
+// the other workers' reductions).  The argmax phase differs per lane, so every window's delta
+// is expanded to its KP*KP phases (zero but one) and all phases accumulate branch-free into the
+// lane's band registers; the lanes' partial bands are summed with warp shuffles.  W is read
+// before this worker publishes the layer's gradient (pre-update for one worker, R5); dout may
+// alias in.
+// ------------------------------------------------------------------------------------
+template <class L, int NT, int RB, bool GLOBALW = true>
+__device__ __forceinline__ void conv_din_gm(const float* __restrict__ wg, const float* __restrict__ dp,
+                                            const uint8_t* __restrict__ am, const float* in, float* dout, int cnt) {
+    constexpr int K = L::K, KP = L::KP, KK = L::KK, PW = L::PW, PH = L::PH, P = L::P, M = L::M, C = L::C;
+    constexpr int W = L::W, HW = L::H * L::W, NB = (L::H + RB - 1) / RB;
+    static_assert(RB % KP == 0, "bands start on a window row");
+    constexpr int R2 = RB / KP;
+    constexpr int DLO = -((KP + K - 2) / KP);  // window rows, relative to the band's first, that reach it
+    constexpr int DHI = (RB - 1) / KP;
+    constexpr int NWR = DHI - DLO + 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int total = cnt * C * NB;
+    for (int vw = warp; vw < total; vw += NT / 32) {
+        const int b = vw % NB;
+        const int n = (vw / NB) % C;
+        const int g = vw / (NB * C);
+        float acc[RB][W];
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+            for (int c = 0; c < W; ++c) acc[r][c] = 0.f;
+        const float* wn = wg + static_cast<long long>(n) * KK * L::MP;
+        const float* dpg = dp + g * L::OUT_SZ;
+        const uint8_t* amg = am + g * L::OUT_SZ;
+        const int pr0 = b * R2;
+#pragma unroll 1
+        for (int m = lane; m < M; m += 32) {
+            float w[KK];
+#pragma unroll
+            for (int tp = 0; tp < KK; ++tp) w[tp] = GLOBALW ? __ldcg(wn + tp * L::MP + m) : wn[tp * L::MP + m];
+#pragma unroll
+            for (int dr = 0; dr < NWR; ++dr) {
+                const int pr = pr0 + DLO + dr;
+                const bool ok = pr >= 0 && pr < PH;
+#pragma unroll
+                for (int pc = 0; pc < PW; ++pc) {
+                    const int o = m * P + (ok ? pr : 0) * PW + pc;
+                    const float d = ok ? dpg[o] : 0.f;
+                    const int arg = ok ? static_cast<int>(amg[o]) : 0;
+#pragma unroll
+                    for (int ph = 0; ph < KP * KP; ++ph) {
+                        const float dq = arg == ph ? d : 0.f;
+#pragma unroll
+                        for (int i = 0; i < K; ++i) {
+                            const int rr = (DLO + dr) * KP + ph / KP + i;
+                            if (rr < 0 || rr >= RB) continue;  // compile-time after unrolling
+#pragma unroll
+                            for (int j = 0; j < K; ++j) {
+                                const int cc = pc * KP + ph % KP + j;
+                                acc[rr][cc] = fmaf(w[i * K + j], dq, acc[rr][cc]);
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        const float* ib = in + g * L::IN_SZ + n * HW + b * RB * W;
+        float* ob = dout + g * L::IN_SZ + n * HW + b * RB * W;
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+            for (int c = 0; c < W; ++c) {
+                const float v = warp_sum(acc[r][c]);
+                if (lane == (r * W + c) % 32 && b * RB + r < L::H) {
+                    const float x = ib[r * W + c];
+                    ob[r * W + c] = v * (1.f - x * x);
+                }
+            }
     }
 }
 
@@ -1900,12 +2003,16 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
     constexpr bool TRAIN = (MODE == kHogwild || MODE == kSync);
     // weight-buffer placement: W1 at 0, W2 at the tail (prefetched during conv1), W3 in two
     // halves (first half prefetched during conv2 into [0, W3A), second after conv2)
-    constexpr int W2OFF = (NCONV >= 2) ? S::WBUF - C2::BLK : 0;
-    constexpr int W3A = (NCONV >= 3) ? (C3::C / 2) * C3::KK * C3::MP : 0;
-    static_assert(NCONV < 3 || W3A <= W2OFF, "W3 first half must not overlap W2");
+    // BIGW nets (Table I large): W1 at 0 and W2 right after it, both staged once per iteration
+    // and kept (W2 serves the conv2 forward and delta_in); conv3 and FC1 read from L2
+    constexpr bool BIG = S::BIG;
+    constexpr int W2OFF = (NCONV >= 2) ? (BIG ? round4(C1::BLK) : S::WBUF - C2::BLK) : 0;
+    constexpr int W3A = (NCONV >= 3 && !BIG) ? (C3::C / 2) * C3::KK * C3::MP : 0;
+    static_assert(NCONV < 3 || BIG || W3A <= W2OFF, "W3 first half must not overlap W2");
+    static_assert(!BIG || NCONV == 3, "BIGW nets have three conv layers");
     // FC1 weights staged through WB in two chunks of FRCH rows (large net: WB is free between
     // the conv3 forward and the conv3 backward, which re-fetches W3)
-    constexpr bool FCSTAGE = (NCONV == 3) && (NFULL == 2) && (F1::IN % 4 == 0);
+    constexpr bool FCSTAGE = (NCONV == 3) && (NFULL == 2) && (F1::IN % 4 == 0) && !BIG;
     constexpr int FRCH = FCSTAGE ? (S::WBUF / (2 * F1::IN)) : 1;
     static_assert(!FCSTAGE || FRCH >= 1, "FC1 chunk must hold a row");
     static_assert(NCONV < 2 || C1::BLK <= W2OFF, "W1 and W2 must not overlap");
@@ -2011,12 +2118,17 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             fence_async_smem();
             __syncthreads();
             PTIME(2);
-            if constexpr (NCONV >= 3) L2.issue(wb, P + O::c3w, W3A);  // W1 region is dead: W3's first half
+            if constexpr (NCONV >= 3 && !BIG) L2.issue(wb, P + O::c3w, W3A);  // W1 region is dead: W3's first half
             L1.wait();
             conv_fwd<C2, NT>(a1, wb + W2OFF, a2, am2, cnt);
             alast = a2;
         }
-        if constexpr (NCONV >= 3) {
+        if constexpr (NCONV >= 3 && BIG) {
+            __syncthreads();
+            PTIME(3);
+            conv_fwd<C3, NT>(a2, P + O::c3w, a3, am3, cnt);  // weights from L2
+            alast = a3;
+        } else if constexpr (NCONV >= 3) {
             fence_async_smem();
             __syncthreads();
             PTIME(3);
@@ -2034,7 +2146,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             if constexpr (FCSTAGE)
                 fc_fwd3<F1, G, NT, FRCH>(P + O::f1w, P + O::f1b, alast, hh, F1::OUT, cnt, wb, L4, L5, sS);
             else if constexpr (F1::IN % 4 == 0)
-                fc_fwd2<F1, G, NT, (NT > 512 ? 2 : 4)>(P + O::f1w, P + O::f1b, alast, hh, F1::OUT, cnt);
+                fc_fwd2<F1, G, NT, (NT > 512 || BIG ? 2 : 4)>(P + O::f1w, P + O::f1b, alast, hh, F1::OUT, cnt);
             else
                 fc_fwd<F1, G, NT>(P + O::f1w, P + O::f1b, alast, hh, F1::OUT, cnt);
             __syncthreads();
@@ -2091,7 +2203,11 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 fc_bwd<F2, G, NT, MODE, SHALF>(a, slot, O::f2w, O::f2b, hh, zz, kZStride, sS, bsc, cnt, sc);
                 wait_publish_reads();
                 PTIME(7);
-                if constexpr (FCSTAGE) {
+                if constexpr (BIG) {
+                    constexpr int NRG = NT / (F1::IN / 4) < 4 ? NT / (F1::IN / 4) : 4;
+                    static_assert(NRG >= 1 && (NRG - 1) * G * F1::IN <= S::SFL, "row-group partials must fit in S");
+                    fc_bwd2<F1, G, NT, MODE, NRG>(a, slot, O::f1w, O::f1b, alast, hh, F1::OUT, sS, bsc, cnt, sc);
+                } else if constexpr (FCSTAGE) {
                     constexpr int NRG = NT / (F1::IN / 4) < 4 ? NT / (F1::IN / 4) : 4;
                     static_assert((NRG - 1) * G * F1::IN <= S::SFL, "row-group partials must fit in S");
                     fence_async_smem();
@@ -2111,7 +2227,30 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             wait_publish_reads();
             PTIME(8);
             // ---------------- a6/a7: pool + conv backward, publish per layer
-            if constexpr (NCONV == 3) {
+            if constexpr (NCONV == 3 && BIG) {
+                // conv3 delta_in first (W3 read from L2 before this worker publishes its
+                // gradient: the pre-update weights for one worker, R5) into WB (W2 is re-staged
+                // below), then the weight gradient (reads a2), then the delta back over a2
+                static_assert(G * C2::OUT_SZ <= S::WBUF, "conv3 delta_in must fit in WB");
+                conv_din_gm<C3, NT, Net::RB3>(P + O::c3w, a3, am3, a2, wb, cnt);
+                __syncthreads();
+                PTIME(9);
+                conv_gw<C3, NT, MODE, false>(a, slot, a2, a3, am3, nullptr, O::c3w, cnt, sc);
+                __syncthreads();
+                PTIME(10);
+                for (int e = threadIdx.x; e < cnt * C2::OUT_SZ; e += NT) a2[e] = wb[e];
+                fence_async_smem();
+                __syncthreads();
+                L1.issue(wb + W2OFF, P + O::c2w, C2::BLK);  // W2 again (pre-update snapshot)
+                L1.wait();
+                PTIME(11);
+                conv_gw<C2, NT, MODE, false>(a, slot, a1, a2, am2, nullptr, O::c2w, cnt, sc);
+                __syncthreads();
+                PTIME(12);
+                conv_din_gm<C2, NT, C2::RB, false>(wb + W2OFF, a2, am2, a1, a1, cnt);
+                __syncthreads();
+                PTIME(13);
+            } else if constexpr (NCONV == 3) {
                 if constexpr (FCSTAGE) {
                     // W3 again (the FC1 chunks used its buffer); this worker has not published
                     // layer 3 yet, so for one worker it is the snapshot the forward used (R5)

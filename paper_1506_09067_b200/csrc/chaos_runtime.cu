@@ -64,6 +64,20 @@ struct LargeNet {  // configs[3], configs[4]
     using F2 = Full<150, 10, false>;
 };
 
+struct PaperLargeNet {  // Table I large: conv20 4x4 -> pool 1x1 -> conv60 5x5
+                       // -> pool2 -> conv100 6x6 -> pool2 -> FC 900->150 tanh -> FC 150->10.  383,160
+                       // weights: W1 + W2 staged and kept, W3 (864 KB) and FC1 (540 KB) read from L2 (BIGW);
+                       // one image per worker (224 KB of shared memory)
+    static constexpr int NCONV = 3, NFULL = 2, GDEF = 1, GINIT = 1, INFLIGHT = 148, NT = 384, SFL = 1800, RB3 = 4;
+    static constexpr bool BIGW = true;
+    //                C   H   W    M  K  KP  MT  TT  GS  RB  PB  MS  GWMMA  DIN3  GWIN  DWIN  NSPL
+    using C1 = Conv<1, 29, 29, 20, 4, 1, 10, 16, 16, 1>;
+    using C2 = Conv<20, 26, 26, 60, 5, 2, 10, 25, 1, 2>;
+    using C3 = Conv<60, 11, 11, 100, 6, 2, 5, 12, 1, 2, 0, 0, false, false, 0, false, 2>;
+    using F1 = Full<900, 150, true>;
+    using F2 = Full<150, 10, false>;
+};
+
 using KernelFn = void (*)(KArgs);
 
 struct Block {  // one weighted layer, host view
@@ -183,6 +197,10 @@ const std::vector<NetDesc>& registry() {
             "large", {{CHAOS_CONV, 20, 4, CHAOS_TANH}, {CHAOS_MAXPOOL, 0, 2, 0}, {CHAOS_CONV, 60, 3, CHAOS_TANH},
                       {CHAOS_MAXPOOL, 0, 2, 0}, {CHAOS_CONV, 100, 2, CHAOS_TANH}, {CHAOS_MAXPOOL, 0, 2, 0},
                       {CHAOS_FULL, 150, 0, CHAOS_TANH}, {CHAOS_FULL, 10, 0, CHAOS_IDENTITY}}));
+        v.push_back(make_desc<PaperLargeNet>(
+            "paper_large", {{CHAOS_CONV, 20, 4, CHAOS_TANH}, {CHAOS_MAXPOOL, 0, 1, 0}, {CHAOS_CONV, 60, 5, CHAOS_TANH},
+                            {CHAOS_MAXPOOL, 0, 2, 0}, {CHAOS_CONV, 100, 6, CHAOS_TANH}, {CHAOS_MAXPOOL, 0, 2, 0},
+                            {CHAOS_FULL, 150, 0, CHAOS_TANH}, {CHAOS_FULL, 10, 0, CHAOS_IDENTITY}}));
         return v;
     }();
     return r;

@@ -17,7 +17,11 @@ from helpers import assert_parity, parity_report, tie_free_prefix
 
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden", "oracle_runs")
-NETS = ["tiny", "medium", "large", "paper_small"]
+NETS = ["tiny", "medium", "large", "paper_small", "paper_large"]
+# Element-wise tolerance of multi-step weight comparisons (R9 / R15): BASELINE.json's
+# rel 1e-4 for its nets; the Table I large net (not a BASELINE config) sums up to 2,160 fp32
+# products per output (9x the large net's 240), so its bound scales by sqrt(9): 3e-4
+REL = {"paper_large": 3e-4}
 
 
 @pytest.fixture(scope="module")
@@ -33,6 +37,9 @@ def make(name, seed, torch_cuda, group=None):
     o = Oracle(sd.ARCHS[name])
     net = Net(sd.ARCHS[name], init_seed=seed)
     if group is not None:
+        if group != 1 and name == "paper_large":
+            net.close()
+            pytest.skip("paper_large is compiled for G = 1 only (one image per worker)")
         net.set_option(OPT_GROUP, group)
     p = sd.init_params(seed, o.blocks())
     net.set_params(p)
@@ -113,7 +120,7 @@ def test_sync_steps(name, torch_cuda):
     got = net.get_params()
     ref, _ = o.train_sync(p, d.x_train, d.y_train, lr, 64)
     # the weights move by lr*g: compare the step (ref - p) as well as the weights
-    assert_parity(got, ref, o.blocks())
+    assert_parity(got, ref, o.blocks(), rel=REL.get(name, 1e-4))
     step_ok, w, wn, _ = parity_report(got.astype(np.float64) - p, ref - p, o.blocks(), rel=1e-3, floor=1e-2,
                                       norm_rel=1e-4)
     assert step_ok, (w, wn)
@@ -192,7 +199,7 @@ def test_hogwild_single_worker_is_sequential_sgd(name, seed, torch_cuda):
     net.train_epoch(X, Y, 0.05)
     got = net.get_params()
     ref, _ = o.train_sgd(p, d.x_train[:n], d.y_train[:n], 0.05)
-    assert_parity(got, ref, o.blocks())
+    assert_parity(got, ref, o.blocks(), rel=REL.get(name, 1e-4))
 
 
 @pytest.mark.parametrize("name", NETS)
@@ -475,8 +482,8 @@ def test_phase_timing_is_not_in_the_product_build(torch_cuda):
 def test_staleness_cap(torch_cuda):
     # R14: images in flight (CTAs x G) never exceed the per-net cap
     from paper_1506_09067_b200 import OPT_GROUP
-    for name, cap in [("tiny", 148), ("medium", 592), ("large", 592), ("paper_small", 148)]:
-        for g in (1, 4):
+    for name, cap in [("tiny", 148), ("medium", 592), ("large", 592), ("paper_small", 148), ("paper_large", 148)]:
+        for g in ((1,) if name == "paper_large" else (1, 4)):
             _, net, _ = make(name, 1, torch_cuda, g)
             info = net.launch_info()
             assert info["grid"] * info["group"] <= cap, (name, g, info)
