@@ -396,6 +396,21 @@ __device__ __forceinline__ void mma3(float (&d)[4], const uint32_t (&ah)[4], con
     mma_tf32(d, ah, bh0, bh1);
 }
 
+// Sums 32 values across the warp's lanes at once (v[k] of every lane -> lane k): 16+8+4+2+1
+// shuffles; at each step a lane keeps the half of its values its lane bit selects.
+__device__ __forceinline__ float warp_transpose_sum(float (&v)[32], int lane) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int k = 0; k < o; ++k) {
+            const float send = up ? v[k] : v[k + o];
+            const float keep = up ? v[k + o] : v[k];
+            v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    return v[0];
+}
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -407,9 +422,11 @@ __device__ __forceinline__ float warp_sum(float v) {
 // one pooled window x one image; the KP*KP conv outputs of the window stay in registers,
 // the weights of the MT maps are warp-uniform vector loads from the staged block.
 // ------------------------------------------------------------------------------------
-template <class L, int NT>
+template <class L, int NT, bool PFW = false>
 __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const float* __restrict__ wsm,
                                          float* __restrict__ out, uint8_t* __restrict__ am, int cnt) {
+    // PFW: the weights are in global memory (BIGW conv3): each thread prefetches one tap row of
+    // the next input map's weights into L1, so the block's loads of map n+1 hit L1
     constexpr int MT = L::MT, KP = L::KP, K = L::K, PW = L::PW, P = L::P, MG = L::M / MT;
     constexpr int PS = KP + K - 1;
     constexpr bool A4 = (MT % 4 == 0) || (MG == 1);
@@ -437,6 +454,10 @@ __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const flo
         const float* wb = wsm + mg * MT;
 #pragma unroll 1
         for (int n = half * CH; n < (half + 1) * CH; ++n) {
+            if constexpr (PFW) {
+                if (n + 1 < (half + 1) * CH)
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(wb + ((n + 1) * L::KK + threadIdx.x % L::KK) * L::MP));
+            }
             float patch[PS][PS];
 #pragma unroll
             for (int u = 0; u < PS; ++u)
@@ -1025,20 +1046,30 @@ __device__ __forceinline__ void conv_din_gm(const float* __restrict__ wg, const 
         const float* dpg = dp + g * L::OUT_SZ;
         const uint8_t* amg = am + g * L::OUT_SZ;
         const int pr0 = b * R2;
+        // weights of the lane's next map are loaded one round ahead (global: hides the L2 latency)
+        float wnx[KK];
+#pragma unroll
+        for (int tp = 0; tp < KK; ++tp)
+            wnx[tp] = lane < M ? (GLOBALW ? __ldcg(wn + tp * L::MP + lane) : wn[tp * L::MP + lane]) : 0.f;
 #pragma unroll 1
         for (int m = lane; m < M; m += 32) {
             float w[KK];
 #pragma unroll
-            for (int tp = 0; tp < KK; ++tp) w[tp] = GLOBALW ? __ldcg(wn + tp * L::MP + m) : wn[tp * L::MP + m];
+            for (int tp = 0; tp < KK; ++tp) w[tp] = wnx[tp];
+            if (m + 32 < M) {
+#pragma unroll
+                for (int tp = 0; tp < KK; ++tp)
+                    wnx[tp] = GLOBALW ? __ldcg(wn + tp * L::MP + m + 32) : wn[tp * L::MP + m + 32];
+            }
 #pragma unroll
             for (int dr = 0; dr < NWR; ++dr) {
                 const int pr = pr0 + DLO + dr;
-                const bool ok = pr >= 0 && pr < PH;
+                if (pr < 0 || pr >= PH) continue;  // warp-uniform (the band is the warp's)
 #pragma unroll
                 for (int pc = 0; pc < PW; ++pc) {
-                    const int o = m * P + (ok ? pr : 0) * PW + pc;
-                    const float d = ok ? dpg[o] : 0.f;
-                    const int arg = ok ? static_cast<int>(amg[o]) : 0;
+                    const int o = m * P + pr * PW + pc;
+                    const float d = dpg[o];
+                    const int arg = static_cast<int>(amg[o]);
 #pragma unroll
                     for (int ph = 0; ph < KP * KP; ++ph) {
                         const float dq = arg == ph ? d : 0.f;
@@ -1056,18 +1087,23 @@ __device__ __forceinline__ void conv_din_gm(const float* __restrict__ wg, const 
                 }
             }
         }
+        // transpose reduction: 32 band values per pass, 31 shuffles; lane l ends with value l
         const float* ib = in + g * L::IN_SZ + n * HW + b * RB * W;
         float* ob = dout + g * L::IN_SZ + n * HW + b * RB * W;
+        const int nval = (b * RB + RB <= L::H ? RB : L::H - b * RB) * W;
+        constexpr int NV = RB * W, NPASS = (NV + 31) / 32;
 #pragma unroll
-        for (int r = 0; r < RB; ++r)
+        for (int ps = 0; ps < NPASS; ++ps) {
+            float v[32];
 #pragma unroll
-            for (int c = 0; c < W; ++c) {
-                const float v = warp_sum(acc[r][c]);
-                if (lane == (r * W + c) % 32 && b * RB + r < L::H) {
-                    const float x = ib[r * W + c];
-                    ob[r * W + c] = v * (1.f - x * x);
-                }
+            for (int k = 0; k < 32; ++k) v[k] = (ps * 32 + k < NV) ? acc[(ps * 32 + k) / W][(ps * 32 + k) % W] : 0.f;
+            const float s = warp_transpose_sum(v, lane);
+            const int idx = ps * 32 + lane;
+            if (idx < nval) {
+                const float x = ib[idx];
+                ob[idx] = s * (1.f - x * x);
             }
+        }
     }
 }
 
@@ -2126,7 +2162,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
         if constexpr (NCONV >= 3 && BIG) {
             __syncthreads();
             PTIME(3);
-            conv_fwd<C3, NT>(a2, P + O::c3w, a3, am3, cnt);  // weights from L2
+            conv_fwd<C3, NT, true>(a2, P + O::c3w, a3, am3, cnt);  // weights from L2 (prefetched to L1)
             alast = a3;
         } else if constexpr (NCONV >= 3) {
             fence_async_smem();

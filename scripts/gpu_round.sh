@@ -18,7 +18,7 @@ fi
 timeout 600 python bench.py --arch $ARCH > ${O}_bench.json 2> ${O}_bench.err; echo "bench rc=$?"; cat ${O}_bench.json; tail -3 ${O}_bench.err
 if [ -z "$SKIP_NCU" ]; then
   CMD="python bench.py --arch $ARCH --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
-  case $ARCH in large) KN="LargeNetELi4ELi[0-9]+ELi0E";; medium) KN="MediumNetELi4ELi[0-9]+ELi0E";; tiny) KN="TinyNetELi1ELi[0-9]+ELi0E";; esac
+  case $ARCH in paper_large) KN="PaperLargeNetELi1ELi[0-9]+ELi0E";; large) KN="LargeNetELi4ELi[0-9]+ELi0E";; medium) KN="MediumNetELi4ELi[0-9]+ELi0E";; tiny) KN="TinyNetELi1ELi[0-9]+ELi0E";; esac
   timeout 600 $CMD > ${O}_plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file ${O}_launches.csv $CMD > ${O}_ncu_launch.log 2>&1
   echo "launch-list rc=$?"
