@@ -715,6 +715,82 @@ __device__ __forceinline__ void conv_gw_win(const KArgs& a, int slot, const floa
 }
 
 // ------------------------------------------------------------------------------------
+// PHASE(conv_gw_wt) conv_gw_win for large kernels (KP == 2): the K*K taps are split into
+// groups of KR tap rows so a thread's accumulators (NM maps x KR*K taps) and input block
+// ((KR+1) x (K+1)) fit in registers.  Tile = (map group of NM, input map n, tap-row group), map
+// group fastest: a warp's lanes share n (input-block loads are broadcasts) and publish
+// consecutive 16-B weight groups (coalesced vector reductions).  Dense per window (4 phases,
+// one of them the argmax), fixed order (deterministic).  Bias gradient: tiles with n == 0, tr == 0.
+// ------------------------------------------------------------------------------------
+template <class L, int NT, int MODE, int NM, int KR>
+__device__ __forceinline__ void conv_gw_wt(const KArgs& a, int slot, const float* __restrict__ in,
+                                           const float* __restrict__ dp, const uint8_t* __restrict__ am, int woff,
+                                           int cnt, float sc) {
+    constexpr int K = L::K, KP = L::KP, KK = L::KK, PW = L::PW, P = L::P, M = L::M, C = L::C;
+    constexpr int W = L::W, HW = L::H * L::W, BR = KP + KR - 1, BC = KP + K - 1;
+    constexpr int NG = M / NM, NTR = K / KR, TILES = NG * C * NTR;
+    static_assert(KP == 2 && NM % 4 == 0 && M % NM == 0 && K % KR == 0, "2x2 pooling, vector publish");
+    for (int tile = threadIdx.x; tile < TILES; tile += NT) {
+        const int mg = tile % NG;
+        const int n = (tile / NG) % C;
+        const int tr = tile / (NG * C);
+        const int m0 = mg * NM;
+        float acc[NM][KR * K];
+        float accb[NM];
+#pragma unroll
+        for (int q = 0; q < NM; ++q) {
+            accb[q] = 0.f;
+#pragma unroll
+            for (int t = 0; t < KR * K; ++t) acc[q][t] = 0.f;
+        }
+#pragma unroll 1
+        for (int g = 0; g < cnt; ++g) {
+            const float* ing = in + g * L::IN_SZ + n * HW + tr * KR * W;
+            const float* dpg = dp + g * L::OUT_SZ + m0 * P;
+            const uint8_t* amg = am + g * L::OUT_SZ + m0 * P;
+#pragma unroll 1
+            for (int w = 0; w < P; ++w) {
+                const int pr = w / PW, pc = w - (w / PW) * PW;
+                float blk[BR][BC];
+#pragma unroll
+                for (int u = 0; u < BR; ++u)
+#pragma unroll
+                    for (int v = 0; v < BC; ++v) blk[u][v] = ing[(pr * KP + u) * W + pc * KP + v];
+#pragma unroll
+                for (int q = 0; q < NM; ++q) {
+                    const float d = dpg[q * P + w];
+                    const int ph = amg[q * P + w];
+                    accb[q] += d;
+#pragma unroll
+                    for (int aa = 0; aa < KP; ++aa)
+#pragma unroll
+                        for (int bb = 0; bb < KP; ++bb) {
+                            const float dq = (ph == aa * KP + bb) ? d : 0.f;
+#pragma unroll
+                            for (int i = 0; i < KR; ++i)
+#pragma unroll
+                                for (int j = 0; j < K; ++j)
+                                    acc[q][i * K + j] = fmaf(dq, blk[aa + i][bb + j], acc[q][i * K + j]);
+                        }
+                }
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < KR * K; ++t)
+#pragma unroll
+            for (int q4 = 0; q4 < NM; q4 += 4)
+                publish_vec4<MODE>(a, slot, woff + (n * KK + tr * KR * K + t) * L::MP + m0 + q4,
+                                   make_float4(sc * acc[q4][t], sc * acc[q4 + 1][t], sc * acc[q4 + 2][t],
+                                               sc * acc[q4 + 3][t]));
+        if (n == 0 && tr == 0)
+#pragma unroll
+            for (int q4 = 0; q4 < NM; q4 += 4)
+                publish_vec4<MODE>(a, slot, woff + L::WFL + m0 + q4,
+                                   make_float4(sc * accb[q4], sc * accb[q4 + 1], sc * accb[q4 + 2], sc * accb[q4 + 3]));
+    }
+}
+
+// ------------------------------------------------------------------------------------
 // PHASE(conv_gw_mma) conv weight gradient on the tensor cores (KP == 2), as the dense GEMM
 //   gW[k][m] = sum_g sum_p in[g][n(k)][r(p)+i(k)][c(p)+j(k)] * Dz[g][m][p]
 // over the conv positions p that lie in a pooling window (k = n*K*K + i*K + j, the row of the
@@ -2271,7 +2347,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 conv_din_gm<C3, NT, Net::RB3>(P + O::c3w, a3, am3, a2, wb, cnt);
                 __syncthreads();
                 PTIME(9);
-                conv_gw<C3, NT, MODE, false>(a, slot, a2, a3, am3, nullptr, O::c3w, cnt, sc);
+                conv_gw_wt<C3, NT, MODE, 4, 2>(a, slot, a2, a3, am3, O::c3w, cnt, sc);
                 __syncthreads();
                 PTIME(10);
                 for (int e = threadIdx.x; e < cnt * C2::OUT_SZ; e += NT) a2[e] = wb[e];
