@@ -504,6 +504,89 @@ __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const flo
 }
 
 // ------------------------------------------------------------------------------------
+// PHASE(conv_fwd_slab) conv -> tanh -> max-pool forward with the weights streamed through
+// shared memory one input map at a time (a layer too large to stage whole: the Table I large
+// net's conv3, 864 KB).  W[n][*][*] (K*K*MP floats, contiguous in the internal layout) is TMA
+// bulk-copied into a ring of 3 buffers, two maps ahead; all threads walk the input maps in
+// lockstep (one barrier per map).  Item = MT maps x one pooled window (G = 1 images), its KP*KP
+// conv outputs in registers, as in conv_fwd.  ring: 3 * K*K*MP floats of dead shared memory.
+// ------------------------------------------------------------------------------------
+template <class L, int NT>
+__device__ __forceinline__ void conv_fwd_slab(const float* __restrict__ in, const float* __restrict__ wg,
+                                              float* __restrict__ out, uint8_t* __restrict__ am, float* ring,
+                                              Loader& R0, Loader& R1, Loader& R2) {
+    constexpr int MT = L::MT, KP = L::KP, K = L::K, KK = L::KK, PW = L::PW, P = L::P, MG = L::M / MT;
+    constexpr int PS = KP + K - 1, SLAB = KK * L::MP, ITEMS = MG * P;
+    static_assert(ITEMS <= NT, "one item per thread");
+    static_assert((SLAB * 4) % 16 == 0 && MT % 4 == 0, "16-B slabs, vector weight loads");
+    Loader* R[3] = {&R0, &R1, &R2};
+    R0.issue(ring, wg, SLAB);
+    R1.issue(ring + SLAB, wg + SLAB, SLAB);
+    R2.issue(ring + 2 * SLAB, wg + 2 * SLAB, SLAB);
+    const int it = threadIdx.x;
+    const bool act = it < ITEMS;
+    const int p = act ? it % P : 0;
+    const int mg = act ? it / P : 0;
+    const int pr = p / PW, pc = p - (p / PW) * PW;
+    float acc[MT][KP * KP];
+    {
+        float b[MT];
+        load_vec<MT, true>(b, wg + L::WFL + mg * MT);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int q = 0; q < KP * KP; ++q) acc[mt][q] = b[mt];
+    }
+    const float* ib = in + (pr * KP) * L::W + pc * KP;
+#pragma unroll 1
+    for (int n = 0; n < L::C; ++n) {
+        R[n % 3]->wait();
+        const float* wb = ring + (n % 3) * SLAB + mg * MT;
+        if (act) {
+            float patch[PS][PS];
+#pragma unroll
+            for (int u = 0; u < PS; ++u)
+#pragma unroll
+                for (int v = 0; v < PS; ++v) patch[u][v] = ib[n * (L::H * L::W) + u * L::W + v];
+#pragma unroll
+            for (int i = 0; i < K; ++i)
+#pragma unroll
+                for (int j = 0; j < K; ++j) {
+                    float wv[MT];
+                    load_vec<MT, true>(wv, wb + (i * K + j) * L::MP);
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                        for (int u = 0; u < KP; ++u)
+#pragma unroll
+                            for (int v = 0; v < KP; ++v)
+                                acc[mt][u * KP + v] = fmaf(wv[mt], patch[u + i][v + j], acc[mt][u * KP + v]);
+                }
+        }
+        if (n + 3 < L::C) {
+            sync_for_async();  // every thread is done with this buffer
+            R[n % 3]->issue(ring + (n % 3) * SLAB, wg + static_cast<long long>(n + 3) * SLAB, SLAB);
+        }
+    }
+    if (act) {
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            float best = acc[mt][0];
+            int arg = 0;
+#pragma unroll
+            for (int q = 1; q < KP * KP; ++q)
+                if (acc[mt][q] > best) {  // first strict maximum wins (R4)
+                    best = acc[mt][q];
+                    arg = q;
+                }
+            const int o = (mg * MT + mt) * P + p;
+            out[o] = tanhf(best);
+            am[o] = static_cast<uint8_t>(arg);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
 // PHASE(conv_gw) conv weight gradient.  dp[g][m][pp] = dL/dz at the argmax of pooled
 // output pp (the pool routes the delta there and nowhere else):
 //   gW[n][i][j][m] = sum_g sum_pp dp[g][m][pp] * in[g][n][r(pp)+i][c(pp)+j],  gb[m] = sum dp
@@ -2236,9 +2319,10 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             alast = a2;
         }
         if constexpr (NCONV >= 3 && BIG) {
-            __syncthreads();
+            static_assert(3 * C3::KK * C3::MP <= G * C1::OUT_SZ, "conv3 weight ring must fit in A1");
+            sync_for_async();  // A1 (read by the conv2 forward) becomes the conv3 weight ring
             PTIME(3);
-            conv_fwd<C3, NT, true>(a2, P + O::c3w, a3, am3, cnt);  // weights from L2 (prefetched to L1)
+            conv_fwd_slab<C3, NT>(a2, P + O::c3w, a3, am3, a1, L2, L3, L4);
             alast = a3;
         } else if constexpr (NCONV >= 3) {
             fence_async_smem();
@@ -2341,20 +2425,29 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             // ---------------- a6/a7: pool + conv backward, publish per layer
             if constexpr (NCONV == 3 && BIG) {
                 // conv3 delta_in first (W3 read from L2 before this worker publishes its
-                // gradient: the pre-update weights for one worker, R5) into WB (W2 is re-staged
-                // below), then the weight gradient (reads a2), then the delta back over a2
-                static_assert(G * C2::OUT_SZ <= S::WBUF, "conv3 delta_in must fit in WB");
-                conv_din_gm<C3, NT, Net::RB3>(P + O::c3w, a3, am3, a2, wb, cnt);
+                // gradient: the pre-update weights for one worker, R5) into the dead A1 region,
+                // then the weight gradient (reads a2), then the delta back over a2; A1 is then
+                // recomputed (conv1 forward again, same image and staged W1) for conv2's backward.
+                // W1 and W2 stay staged from the forward pass (the snapshot it used).
+                static_assert(G * C2::OUT_SZ <= G * C1::OUT_SZ, "conv3 delta_in must fit in A1");
+                conv_din_gm<C3, NT, Net::RB3>(P + O::c3w, a3, am3, a2, a1, cnt);
                 __syncthreads();
                 PTIME(9);
                 conv_gw_wt<C3, NT, MODE, 4, 2>(a, slot, a2, a3, am3, O::c3w, cnt, sc);
                 __syncthreads();
                 PTIME(10);
-                for (int e = threadIdx.x; e < cnt * C2::OUT_SZ; e += NT) a2[e] = wb[e];
+                for (int e = threadIdx.x; e < cnt * C2::OUT_SZ; e += NT) a2[e] = a1[e];
                 fence_async_smem();
+                wait_publish_reads();  // S (FC scratch, bulk-published) takes the image again
+                if (x_bulk) {
+                    L0.issue(sS, xsrc, cnt * IMG);
+                    L0.wait();
+                } else {
+                    for (int i = threadIdx.x; i < cnt * IMG; i += NT) sS[i] = __ldg(xsrc + i);
+                    __syncthreads();
+                }
+                conv_fwd<C1, NT>(sS, wb, a1, am1, cnt);
                 __syncthreads();
-                L1.issue(wb + W2OFF, P + O::c2w, C2::BLK);  // W2 again (pre-update snapshot)
-                L1.wait();
                 PTIME(11);
                 conv_gw<C2, NT, MODE, false>(a, slot, a1, a2, am2, nullptr, O::c2w, cnt, sc);
                 __syncthreads();

@@ -73,7 +73,7 @@ struct PaperLargeNet {  // Table I large: conv
     //                C   H   W    M  K  KP  MT  TT  GS  RB  PB  MS  GWMMA  DIN3  GWIN  DWIN  NSPL
     using C1 = Conv<1, 29, 29, 20, 4, 1, 10, 16, 16, 1>;
     using C2 = Conv<20, 26, 26, 60, 5, 2, 10, 25, 1, 2>;
-    using C3 = Conv<60, 11, 11, 100, 6, 2, 5, 12, 1, 2, 0, 0, false, false, 0, false, 2>;
+    using C3 = Conv<60, 11, 11, 100, 6, 2, 4, 12, 1, 2>;
     using F1 = Full<900, 150, true>;
     using F2 = Full<150, 10, false>;
 };

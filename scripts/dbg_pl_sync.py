@@ -17,12 +17,15 @@ o = Oracle(sd.ARCHS[name])
 net = Net(sd.ARCHS[name], init_seed=7)
 p = sd.init_params(7, o.blocks())
 net.set_params(p)
+nimg = int(sys.argv[2]) if len(sys.argv) > 2 else 150
 net.set_option(OPT_SYNC_BATCH, 64)
 d = sd.prototype_dataset(7, 150, 0)
-X, Y = torch.from_numpy(d.x_train).cuda(), torch.from_numpy(d.y_train).cuda()
-net.train_epoch(X, Y, 0.05, SYNC)
+X, Y = torch.from_numpy(d.x_train[:nimg]).cuda(), torch.from_numpy(d.y_train[:nimg]).cuda()
+LR = float(sys.argv[3]) if len(sys.argv) > 3 else 0.05
+net.train_epoch(X, Y, LR, SYNC)
 got = net.get_params().astype(np.float64)
-ref, _ = o.train_sync(p, d.x_train, d.y_train, 0.05, 64)
+ref, _ = o.train_sync(p, d.x_train[:nimg], d.y_train[:nimg], LR, 64)
+print("images", nimg)
 for k, (g, r, p0) in enumerate(zip(split_blocks(got, o.blocks()), split_blocks(ref, o.blocks()),
                                    split_blocks(p.astype(np.float64), o.blocks()))):
     tol = 1e-4 * np.maximum(np.abs(r), 1e-2 * np.abs(r).max())

@@ -32,6 +32,9 @@ RUNS = {
     "config2_sync64_e1": ("config2", "sync", 64, 1),
     # the paper's Table I small net (NEXT-1) on the configs[1] data
     "paper_small_seq": ("config1", "seq", 1, 15, "paper_small"),
+    # the Table I large net (NEXT-1): 69 MFLOP per image, so a bounded slice of the configs[1]
+    # data (the first 3,000 training / 1,000 test images), 3 epochs (~10 min of oracle time)
+    "paper_large_seq": ("config1", "seq", 1, 3, "paper_large", 3000, 1000),
 }
 
 
@@ -39,11 +42,13 @@ def run(name):
     wname, mode, batch, epochs = RUNS[name][:4]
     w = sd.WORKLOADS[wname]
     arch = RUNS[name][4] if len(RUNS[name]) > 4 else w.arch
-    d = sd.make_dataset(w)
+    ntr, nte = (RUNS[name][5], RUNS[name][6]) if len(RUNS[name]) > 6 else (None, None)
+    d = sd.make_dataset(w, ntr, nte)
     o = Oracle(sd.ARCHS[arch])
     p = sd.init_params(w.seed, o.blocks()).astype(np.float64)
     rec = {"run": name, "workload": wname, "arch": arch, "mode": mode, "batch": batch, "epochs": epochs,
-           "data_sha256": d.sha256(), "lr0": w.lr0, "per_epoch": []}
+           "data_sha256": d.sha256(), "lr0": w.lr0, "n_train": len(d.y_train), "n_test": len(d.y_test),
+           "per_epoch": []}
     t0 = time.time()
     ckpt = os.path.join(OUT, name + "_ckpt.npy")
     start = 0
