@@ -18,7 +18,7 @@ from helpers import assert_parity, parity_report, tie_free_prefix
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden", "oracle_runs")
 NETS = ["tiny", "medium", "large", "paper_small", "paper_large"]
-# Element-wise tolerance of multi-step weight comparisons (R9 / R15): BASELINE.json's
+# Element-wise tolerance of multi-step weight comparisons (R9 / R16): BASELINE.json's
 # rel 1e-4 for its nets; the Table I large net (not a BASELINE config) sums up to 2,160 fp32
 # products per output (9x the large net's 240), so its bound scales by sqrt(9): 3e-4
 REL = {"paper_large": 3e-4}
