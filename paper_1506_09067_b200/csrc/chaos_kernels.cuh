@@ -2253,6 +2253,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
 
     long long iter = 0;
     long long next_claim = -1;  // hogwild: thread 0 claims the next group during the backward pass
+    int pending_progress = 0;   // hogwild: images of the previous iteration not yet counted in a.progress
     long long t_last = clock64();
     (void)t_last;
     for (;;) {
@@ -2387,8 +2388,12 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             __syncthreads();
             PTIME(6);
             if constexpr (MODE == kHogwild)  // the claim's round trip overlaps the backward pass
-                if (threadIdx.x == 0)
+                if (threadIdx.x == 0) {
                     next_claim = static_cast<long long>(atomicAdd(a.counter, static_cast<unsigned long long>(G)));
+                    if (pending_progress && a.progress)
+                        atomicAdd(a.progress, static_cast<unsigned long long>(pending_progress));
+                    pending_progress = 0;
+                }
             if (threadIdx.x == 0 && a.loss_sum) {
                 double ls = 0.0;
                 for (int g = 0; g < cnt; ++g) ls += s_loss[g];
@@ -2581,13 +2586,16 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
 #ifndef CHAOS_NO_ITER_FENCE
             if constexpr (MODE == kHogwild) __threadfence();  // this worker's REDs precede its next reads
 #endif
-            if constexpr (MODE == kHogwild)  // progress for the asynchronous cross-GPU averaging
-                if (threadIdx.x == 0 && a.progress) atomicAdd(a.progress, static_cast<unsigned long long>(cnt));
+            if constexpr (MODE == kHogwild)  // progress for the asynchronous cross-GPU averaging: the
+                pending_progress = cnt;     // reduction is issued during the next iteration (off the fences)
         }
         __syncthreads();
         PTIME(15);
     }
     if (threadIdx.x == 0) bulk_wait_all<0>();
+    if constexpr (MODE == kHogwild)
+        if (threadIdx.x == 0 && pending_progress && a.progress)
+            atomicAdd(a.progress, static_cast<unsigned long long>(pending_progress));
 }
 
 // w[j] -= lr * sum_{s < nslots} partial[s][j]  (fixed order: the sync-mode update)
