@@ -2000,7 +2000,10 @@ __device__ __forceinline__ void fc_fwd3(const float* __restrict__ Wg, const floa
 // every NRG-th row.  W is the pre-update snapshot: this CTA publishes gW[o][4c..] only after
 // its thread read W[o][4c..] from the chunk (the chunk was copied before any publish of it).
 // ------------------------------------------------------------------------------------
-template <class F, int G, int NT, int MODE, int NRG, int RCH>
+// RESIDENT: the forward's last two chunks are still in `buf` (nothing touched it since
+// fc_fwd3): the chunks are processed in reverse order, the first two without a copy -- the
+// forward's snapshot, which precedes this worker's publish of the layer (R5).
+template <class F, int G, int NT, int MODE, int NRG, int RCH, bool RESIDENT = false>
 __device__ __forceinline__ void fc_bwd3(const KArgs& a, int slot, int woff, int boff, float* __restrict__ in,
                                         const float* __restrict__ dz, int dstride, float* __restrict__ scr,
                                         float* __restrict__ bsc, int cnt, float sc, float* __restrict__ buf,
@@ -2009,10 +2012,13 @@ __device__ __forceinline__ void fc_bwd3(const KArgs& a, int slot, int woff, int 
     constexpr int IN4 = F::IN / 4;
     constexpr int NCH = (F::OUT + RCH - 1) / RCH;
     static_assert(IN4 * NRG <= NT, "one thread per (column quad, row group)");
+    static_assert(!RESIDENT || NCH >= 2, "two resident chunks");
     const float* Wg = a.params + woff;
     auto rows = [](int c) { return (c + 1) * RCH <= F::OUT ? RCH : F::OUT - c * RCH; };
-    LA.issue(buf, Wg, rows(0) * F::IN);
-    if (NCH > 1) LB.issue(buf + RCH * F::IN, Wg + RCH * F::IN, rows(1) * F::IN);
+    if constexpr (!RESIDENT) {
+        LA.issue(buf, Wg, rows(0) * F::IN);
+        if (NCH > 1) LB.issue(buf + RCH * F::IN, Wg + RCH * F::IN, rows(1) * F::IN);
+    }
     const int c4 = threadIdx.x % IN4;
     const int rg = threadIdx.x / IN4;
     const bool act = threadIdx.x < IN4 * NRG;
@@ -2022,12 +2028,15 @@ __device__ __forceinline__ void fc_bwd3(const KArgs& a, int slot, int woff, int 
         av[g] = (act && g < cnt) ? reinterpret_cast<const float4*>(in + g * F::IN)[c4] : make_float4(0.f, 0.f, 0.f, 0.f);
         din[g] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    for (int c = 0; c < NCH; ++c) {
+    for (int i = 0; i < NCH; ++i) {
+        const int c = RESIDENT ? NCH - 1 - i : i;
         const float* cb = buf + (c & 1) * RCH * F::IN;
-        if (c & 1)
-            LB.wait();
-        else
-            LA.wait();
+        if (!RESIDENT || i >= 2) {
+            if (c & 1)
+                LB.wait();
+            else
+                LA.wait();
+        }
         if (act) {
             for (int r = rg; r < rows(c); r += NRG) {
                 const int o = c * RCH + r;
@@ -2051,12 +2060,13 @@ __device__ __forceinline__ void fc_bwd3(const KArgs& a, int slot, int woff, int 
                                    make_float4(sc * gw.x, sc * gw.y, sc * gw.z, sc * gw.w));
             }
         }
-        if (c + 2 < NCH) {
+        const int nx = RESIDENT ? c - 2 : c + 2;
+        if (RESIDENT ? nx >= 0 : nx < NCH) {
             sync_for_async();
             if (c & 1)
-                LB.issue(buf + RCH * F::IN, Wg + (c + 2) * RCH * F::IN, rows(c + 2) * F::IN);
+                LB.issue(buf + RCH * F::IN, Wg + nx * RCH * F::IN, rows(nx) * F::IN);
             else
-                LA.issue(buf, Wg + (c + 2) * RCH * F::IN, rows(c + 2) * F::IN);
+                LA.issue(buf, Wg + nx * RCH * F::IN, rows(nx) * F::IN);
         }
     }
     if (act && rg > 0)
@@ -2413,8 +2423,8 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                     static_assert((NRG - 1) * G * F1::IN <= S::SFL, "row-group partials must fit in S");
                     fence_async_smem();
                     wait_publish_reads();  // the FC2 publish has read its buffers; WB is free
-                    fc_bwd3<F1, G, NT, MODE, NRG, FRCH>(a, slot, O::f1w, O::f1b, alast, hh, F1::OUT, sS, bsc, cnt,
-                                                         sc, wb, L4, L5);
+                    fc_bwd3<F1, G, NT, MODE, NRG, FRCH, true>(a, slot, O::f1w, O::f1b, alast, hh, F1::OUT, sS, bsc,
+                                                               cnt, sc, wb, L4, L5);
                 } else if constexpr (F1::IN % 4 == 0 && (F1::IN / 4) * 4 <= NT) {
                     constexpr int NRG = NT / (F1::IN / 4) < 4 ? NT / (F1::IN / 4) : 4;
                     static_assert((NRG - 1) * G * F1::IN <= S::SFL, "row-group partials must fit in S");
