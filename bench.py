@@ -194,6 +194,13 @@ def main():
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
     distributed = world > 1 or args.force_dist
+    if distributed and args.mode == "hogwild" and args.avg == "async":
+        # the averaging collectives run beside a persistent kernel that holds every other SM:
+        # NCCL's blocks must all be co-resident on the reserved SMs (a channel block waiting for
+        # a peer whose matching block cannot be scheduled would never finish), so cap them, and
+        # leave NVLS (which wants many channels) off for this small-message path
+        os.environ.setdefault("NCCL_MAX_CTAS", str(max(1, args.reserve_sms)))
+        os.environ.setdefault("NCCL_NVLS_ENABLE", "0")
     if distributed:
         if "RANK" not in os.environ:  # --force-dist without a launcher: a one-rank group
             import socket
@@ -354,6 +361,7 @@ def main():
                    "group_G": info["group"], "ctas": info["grid"], "threads_per_cta": info["block"],
                    "smem_bytes_per_cta": info["smem_bytes"], "sync_interval_K": args.k if distributed else None,
                    "averaging": (args.avg if distributed and args.mode == "hogwild" else None),
+                   "nccl_max_ctas": os.environ.get("NCCL_MAX_CTAS") if use_async else None,
                    "l2": "inputs (202 MB/GPU) larger than the 126 MB L2", "parallelism": f"dp{world}"},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic,

@@ -161,7 +161,10 @@ class DistTrainer:
         ranks of the weights is preserved by every in-flight average (each adds P*avg - sum snap
         = 0), so with additive updates the final weights equal the mean of the replicas' total
         progress, whatever the timing.  No K-interval tail: the kernel never drains mid-shard.
-        ``host``/``chunks``: see ``_launch`` (the progress counter spans the chunk launches)."""
+        ``host``/``chunks``: see ``_launch`` (the progress counter spans the chunk launches).
+        NCCL's blocks must fit the reserved SMs all at once (set NCCL_MAX_CTAS <= reserved SMs
+        before the process group is created; bench.py does), else a collective could wait for a
+        block that cannot be scheduled beside the persistent training kernel."""
         import contextlib
 
         import torch
