@@ -358,7 +358,7 @@ def main():
                                                          "; one NCCL gradient all-reduce per batch")),
                    "arch": args.arch, "mode": args.mode, "images_per_gpu_per_step": PER_GPU,
                    "sync_batch": args.sync_batch if args.mode == "sync" else None,
-                   "group_G": info["group"], "ctas": info["grid"], "threads_per_cta": info["block"],
+                   "group_G": info["group"], "publish_group": info["group"], "ctas": info["grid"], "threads_per_cta": info["block"],
                    "smem_bytes_per_cta": info["smem_bytes"], "sync_interval_K": args.k if distributed else None,
                    "averaging": (args.avg if distributed and args.mode == "hogwild" else None),
                    "nccl_max_ctas": os.environ.get("NCCL_MAX_CTAS") if use_async else None,
