@@ -181,6 +181,9 @@ def main():
                          "NCCL average; 'async' = one launch per shard with in-flight averages every K images on "
                          "a second stream (SURVEY NEXT-2)")
     ap.add_argument("--reserve-sms", type=int, default=4, help="--avg async: SMs left to the comm kernels")
+    ap.add_argument("--comm", default="torch", choices=["torch", "chaos"],
+                    help="hogwild averaging collectives: torch.distributed or the library's own NCCL "
+                         "communicator (chaos_dist_*)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -230,7 +233,8 @@ def main():
     Y = torch.from_numpy(ys).cuda()
     Xt = torch.from_numpy(xt).cuda()
     Yt = torch.from_numpy(yt).cuda()
-    trainer = DistTrainer(net, rank, world, args.k, force_collective=args.force_dist)
+    trainer = DistTrainer(net, rank, world, args.k, force_collective=args.force_dist,
+                          comm=args.comm if args.mode == "hogwild" else "torch")
     grad_buf = torch.zeros_like(net.device_params()) if args.mode == "sync" else None
 
     def step(Xs, Ys, lr_s):
@@ -362,6 +366,7 @@ def main():
                    "smem_bytes_per_cta": info["smem_bytes"], "sync_interval_K": args.k if distributed else None,
                    "averaging": (args.avg if distributed and args.mode == "hogwild" else None),
                    "nccl_max_ctas": os.environ.get("NCCL_MAX_CTAS") if use_async else None,
+                   "comm": (args.comm if distributed and args.mode == "hogwild" else None),
                    "l2": "inputs (202 MB/GPU) larger than the 126 MB L2", "parallelism": f"dp{world}"},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic,

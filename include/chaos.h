@@ -47,7 +47,7 @@ typedef enum {
     CHAOS_E_LABEL = -4,       /* device latch: a label outside [0, n_classes) */
     CHAOS_E_NONFINITE = -5,   /* device latch: non-finite loss */
     CHAOS_E_CUDA = -6,        /* CUDA runtime error (message has cudaGetErrorString) */
-    CHAOS_E_NCCL = -7         /* reserved */
+    CHAOS_E_NCCL = -7         /* chaos_dist_*: libnccl.so.2 not loadable or an NCCL error */
 } chaos_status;
 
 typedef enum { CHAOS_CONV = 1, CHAOS_MAXPOOL = 2, CHAOS_FULL = 3 } chaos_layer_kind;
@@ -164,6 +164,24 @@ uint64_t chaos_progress_enqueued(const chaos_net* net);
 chaos_status chaos_progress_wait(chaos_net* net, uint64_t target, int64_t stream);
 chaos_status chaos_avg_snapshot(chaos_net* net, float* d_snap, int64_t stream);
 chaos_status chaos_avg_apply(chaos_net* net, const float* d_avg, const float* d_snap, int64_t stream);
+
+/* Library-owned NCCL communicator (optional: dist.py's torch.distributed path
+ * needs none of this).  The averaging is R11: w <- (1/P) sum_r w_r (ncclAvg, in place).
+ * libnccl.so.2 is loaded at run time (the copy the process already holds, else the system one);
+ * if it cannot be loaded the calls return CHAOS_E_NCCL, as do NCCL errors (message in
+ * chaos_last_error()).
+ * chaos_dist_unique_id: writes an NCCL unique id (CHAOS_DIST_ID_BYTES bytes) to host_id; call on
+ *   rank 0 and send the bytes to every rank (e.g. a torch.distributed broadcast).
+ * chaos_dist_init: creates the net's communicator, rank in [0, world); collective (every rank
+ *   calls it) and synchronizing.  Destroyed with the net.
+ * chaos_dist_average: params <- average over the ranks, on the net's stream, asynchronous.
+ * chaos_dist_average_buffer: the same on n floats of caller-owned device memory on `stream`
+ *   (cast cudaStream_t; the in-flight averaging of the asynchronous schedule). */
+#define CHAOS_DIST_ID_BYTES 128
+chaos_status chaos_dist_unique_id(void* host_id);
+chaos_status chaos_dist_init(chaos_net* net, const void* host_id, int32_t rank, int32_t world);
+chaos_status chaos_dist_average(chaos_net* net);
+chaos_status chaos_dist_average_buffer(chaos_net* net, float* d_buf, int64_t n, int64_t stream);
 
 /* Debug: copies the per-image claim counts of the last hogwild epoch (needs
  * CHAOS_OPT_DEBUG_CLAIMS=1 before the epoch) into host_counts[n]. */

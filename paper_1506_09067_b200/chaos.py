@@ -30,7 +30,8 @@ EXPORTS = ["chaos_net_create", "chaos_net_destroy", "chaos_net_set_option", "cha
            "chaos_evaluate", "chaos_forward", "chaos_compute_gradients", "chaos_debug_claims", "chaos_net_sync",
            "chaos_net_launch_info", "chaos_last_error", "chaos_last_status", "chaos_debug_phase_times",
            "chaos_batch_gradient", "chaos_apply_gradient", "chaos_progress_enqueued", "chaos_progress_wait",
-           "chaos_avg_snapshot", "chaos_avg_apply"]
+           "chaos_avg_snapshot", "chaos_avg_apply", "chaos_dist_unique_id", "chaos_dist_init",
+           "chaos_dist_average", "chaos_dist_average_buffer"]
 
 
 class ChaosError(RuntimeError):
@@ -87,6 +88,10 @@ def lib():
             "chaos_progress_wait": ([vp, C.c_uint64, C.c_int64], C.c_int),
             "chaos_avg_snapshot": ([vp, vp, C.c_int64], C.c_int),
             "chaos_avg_apply": ([vp, vp, vp, C.c_int64], C.c_int),
+            "chaos_dist_unique_id": ([vp], C.c_int),
+            "chaos_dist_init": ([vp, vp, C.c_int32, C.c_int32], C.c_int),
+            "chaos_dist_average": ([vp], C.c_int),
+            "chaos_dist_average_buffer": ([vp, vp, C.c_int64, C.c_int64], C.c_int),
         }
         for name, (args, res) in sig.items():
             if os.environ.get("CHAOS_LIB") and not hasattr(L, name):
@@ -270,6 +275,27 @@ class Net:
     def avg_apply(self, avg, snap, stream):
         """chaos_avg_apply: params += avg - snap (atomic, beside a running hogwild launch)."""
         _check(lib().chaos_avg_apply(self._h, _ptr(avg), _ptr(snap), stream.cuda_stream))
+
+    @staticmethod
+    def dist_unique_id() -> bytes:
+        """chaos_dist_unique_id: 128 bytes to send from rank 0 to every rank."""
+        buf = C.create_string_buffer(128)
+        _check(lib().chaos_dist_unique_id(buf))
+        return buf.raw
+
+    def dist_init(self, uid: bytes, rank: int, world: int):
+        """chaos_dist_init: the net's own NCCL communicator (collective)."""
+        if len(uid) != 128:
+            raise ValueError("expected the 128-byte id of dist_unique_id()")
+        _check(lib().chaos_dist_init(self._h, C.create_string_buffer(uid, 128), int(rank), int(world)))
+
+    def dist_average(self):
+        """chaos_dist_average: params <- mean over the ranks, on the net's stream."""
+        _check(lib().chaos_dist_average(self._h))
+
+    def dist_average_buffer(self, buf, stream):
+        """chaos_dist_average_buffer: in-place average of a CUDA float32 tensor on `stream`."""
+        _check(lib().chaos_dist_average_buffer(self._h, _ptr(buf), int(buf.numel()), stream.cuda_stream))
 
     def debug_claims(self, n):
         out = np.zeros(n, np.int32)

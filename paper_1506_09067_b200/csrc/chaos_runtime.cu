@@ -5,6 +5,9 @@
 // device allocations, the documented parameter initialiser, launches of the worker
 // kernel in its four modes, the deterministic sync-mode update, the fixed-order
 // evaluation reduction, and the device error latch.
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -228,6 +231,39 @@ chaos_status fail(chaos_status s, const char* fmt, ...) {
 
 }  // namespace
 
+// NCCL, loaded at run time (no link-time dependency): the copy a torch process already holds
+// (RTLD_NOLOAD) if any, else the system libnccl.so.2.  Only chaos_dist_* use it.
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    ncclResult_t (*destroy)(ncclComm_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+};
+const NcclApi& nccl_api() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+        if (!h) {
+            a.why = std::string("libnccl.so.2 not loadable: ") + dlerror();
+            return a;
+        }
+        a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+        a.init_rank = reinterpret_cast<decltype(a.init_rank)>(dlsym(h, "ncclCommInitRank"));
+        a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+        a.destroy = reinterpret_cast<decltype(a.destroy)>(dlsym(h, "ncclCommDestroy"));
+        a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+        a.ok = a.get_unique_id && a.init_rank && a.all_reduce && a.destroy && a.error_string;
+        if (!a.ok) a.why = "libnccl.so.2 lacks an expected symbol";
+        return a;
+    }();
+    return api;
+}
+
 struct chaos_net {
     const NetDesc* d = nullptr;
     int dev = 0;
@@ -261,6 +297,8 @@ struct chaos_net {
     int occ[2][4] = {};
     unsigned long long* ptime = nullptr;  // CHAOS_TIMING builds only
     int ptime_grid = 0;
+    ncclComm_t comm = nullptr;             // chaos_dist_init (library-owned communicator)
+    int comm_world = 0;
     cudaStream_t copy_stream = nullptr;    // chaos_train_epoch_host: H2D chunks overlap training
     std::vector<cudaEvent_t> chunk_ev;
     cudaEvent_t staging_free = nullptr;
@@ -532,6 +570,7 @@ void chaos_net_destroy(chaos_net* net) {
     if (!net) return;
     if (net->stream) cudaStreamSynchronize(net->stream);
     cudaDeviceSynchronize();
+    if (net->comm) nccl_api().destroy(net->comm);
     if (net->copy_stream) cudaStreamDestroy(net->copy_stream);
     if (net->staging_free) cudaEventDestroy(net->staging_free);
     for (cudaEvent_t e : net->chunk_ev) cudaEventDestroy(e);
@@ -863,6 +902,52 @@ chaos_status chaos_avg_apply(chaos_net* net, const float* d_avg, const float* d_
                                                                                                   d_snap, np);
     CUDA_TRY(cudaGetLastError());
     return CHAOS_OK;
+}
+
+chaos_status chaos_dist_unique_id(void* host_id) {
+    if (!host_id) return fail(CHAOS_E_INVALID, "host_id is NULL");
+    const NcclApi& n = nccl_api();
+    if (!n.ok) return fail(CHAOS_E_NCCL, "%s", n.why.c_str());
+    ncclUniqueId id;
+    const ncclResult_t r = n.get_unique_id(&id);
+    if (r != ncclSuccess) return fail(CHAOS_E_NCCL, "ncclGetUniqueId: %s", n.error_string(r));
+    static_assert(sizeof(ncclUniqueId) == CHAOS_DIST_ID_BYTES, "NCCL unique id size");
+    std::memcpy(host_id, &id, sizeof id);
+    return CHAOS_OK;
+}
+
+chaos_status chaos_dist_init(chaos_net* net, const void* host_id, int32_t rank, int32_t world) {
+    if (!net || !host_id) return fail(CHAOS_E_INVALID, "NULL argument");
+    if (world < 1 || rank < 0 || rank >= world) return fail(CHAOS_E_INVALID, "rank %d / world %d", rank, world);
+    if (net->comm) return fail(CHAOS_E_INVALID, "communicator already initialised");
+    const NcclApi& n = nccl_api();
+    if (!n.ok) return fail(CHAOS_E_NCCL, "%s", n.why.c_str());
+    CUDA_TRY(cudaSetDevice(net->dev));
+    ncclUniqueId id;
+    std::memcpy(&id, host_id, sizeof id);
+    const ncclResult_t r = n.init_rank(&net->comm, world, id, rank);
+    if (r != ncclSuccess) {
+        net->comm = nullptr;
+        return fail(CHAOS_E_NCCL, "ncclCommInitRank: %s", n.error_string(r));
+    }
+    net->comm_world = world;
+    return CHAOS_OK;
+}
+
+chaos_status chaos_dist_average_buffer(chaos_net* net, float* d_buf, int64_t n, int64_t stream) {
+    if (!net || (!d_buf && n > 0) || n < 0) return fail(CHAOS_E_INVALID, "NULL buffer or n < 0");
+    if (!net->comm) return fail(CHAOS_E_INVALID, "chaos_dist_init has not been called");
+    if (n == 0) return CHAOS_OK;
+    const NcclApi& a = nccl_api();
+    const ncclResult_t r = a.all_reduce(d_buf, d_buf, static_cast<size_t>(n), ncclFloat32, ncclAvg, net->comm,
+                                        reinterpret_cast<cudaStream_t>(stream));
+    if (r != ncclSuccess) return fail(CHAOS_E_NCCL, "ncclAllReduce: %s", a.error_string(r));
+    return CHAOS_OK;
+}
+
+chaos_status chaos_dist_average(chaos_net* net) {
+    if (!net) return fail(CHAOS_E_INVALID, "net is NULL");
+    return chaos_dist_average_buffer(net, net->params, net->d->pint, reinterpret_cast<int64_t>(net->stream));
 }
 
 chaos_status chaos_debug_claims(chaos_net* net, int32_t* host_counts, int64_t n) {

@@ -70,15 +70,40 @@ class DistTrainer:
     API) -- plus ``batch_gradient`` / ``apply_gradient`` for the sync mode; tests substitute a
     CPU stand-in with the same methods."""
 
-    def __init__(self, net, rank: int, world: int, k: int, group=None, force_collective: bool = False):
+    def __init__(self, net, rank: int, world: int, k: int, group=None, force_collective: bool = False,
+                 comm: str = "torch"):
         """force_collective: run the K-interval schedule and the collectives even with one rank
-        (exercises the multi-GPU code path on one GPU)."""
+        (exercises the multi-GPU code path on one GPU).  comm: "torch" = torch.distributed
+        all-reduces; "chaos" = the library's own NCCL communicator (chaos_dist_*; its unique id
+        travels over the torch process group once, here)."""
         self.net, self.rank, self.world, self.k, self.group = net, rank, world, k, group
         self.force = force_collective
+        self.comm = comm
+        if comm == "chaos" and (world > 1 or force_collective):
+            import torch
+            import torch.distributed as dist
+            uid = net.dist_unique_id() if rank == 0 else bytes(128)
+            t = torch.tensor(list(uid), dtype=torch.uint8,
+                             device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
+            dist.broadcast(t, src=0, group=group)
+            net.dist_init(bytes(t.cpu().tolist()), rank, world)
+        elif comm not in ("torch", "chaos"):
+            raise ValueError(f"comm must be 'torch' or 'chaos', not {comm!r}")
         self.n_collectives = 0
         self.n_launches = 0
         self.n_aux_launches = 0  # epoch_async: progress-wait + apply kernels
         self._agreed_cache = {}
+
+    def _average(self, tensor, stream=None):
+        """In-place average over the ranks: torch.distributed (current stream) or chaos_dist_*."""
+        if self.comm == "chaos":
+            import torch
+            if tensor.data_ptr() == self.net.device_params().data_ptr() and stream is None:
+                self.net.dist_average()  # the net's stream
+            else:
+                self.net.dist_average_buffer(tensor, stream if stream is not None else torch.cuda.current_stream())
+        else:
+            average_(tensor, self.world, self.group, force=self.force)
 
     def _agreed(self, n_local: int, op: str) -> int:
         """MIN / MAX of the shard length over ranks (cached per length): the number of
@@ -106,7 +131,7 @@ class DistTrainer:
                 self.net.train_epoch(images[lo:hi], labels[lo:hi], lr)
                 self.n_launches += 1
             if multi:
-                average_(params, self.world, self.group, force=self.force)
+                self._average(params)
                 self.n_collectives += 1
             return
         count = max(1, -(-self._agreed(hi - lo, "max") // self.k))
@@ -115,7 +140,7 @@ class DistTrainer:
             if e > s:
                 self.net.train_epoch(images[s:e], labels[s:e], lr)
                 self.n_launches += 1
-            average_(params, self.world, self.group, force=self.force)
+            self._average(params)
             self.n_collectives += 1
 
     def _launch(self, images, labels, lr, lo, hi, host, chunks):
@@ -191,7 +216,7 @@ class DistTrainer:
                 net.progress_wait(base + t, cs)
                 net.avg_snapshot(snap, cs)
                 avg.copy_(snap)
-                average_(avg, self.world, self.group, force=self.force)
+                self._average(avg, cs)
                 net.avg_apply(avg, snap, cs)
                 self.n_collectives += 1
                 self.n_aux_launches += 2
@@ -199,7 +224,7 @@ class DistTrainer:
                 cs.wait_stream(ts)  # the launch has completed
             else:
                 net.sync()
-            average_(params, self.world, self.group, force=self.force)
+            self._average(params, cs)
             self.n_collectives += 1
         if cuda:
             ts.wait_stream(cs)

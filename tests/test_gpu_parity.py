@@ -425,7 +425,7 @@ def test_two_rank_sync_emulated_matches_oracle(torch_cuda):
     assert_parity(runs[0], ref, o.blocks())
 
 
-@pytest.mark.parametrize("mode", ["hogwild", "sync", "hogwild_dist"])
+@pytest.mark.parametrize("mode", ["hogwild", "sync", "hogwild_dist", "hogwild_dist_chaoscomm"])
 def test_bench_line_contract(mode, torch_cuda):
     # bench.py's JSON line on one GPU: contract keys, roofline + cpu_baseline objects, e2e with host bytes
     import subprocess
@@ -435,8 +435,10 @@ def test_bench_line_contract(mode, torch_cuda):
            "--mode", mode.split("_")[0]]
     if mode != "hogwild":
         cmd.append("--no-cpu-baseline")
-    if mode == "hogwild_dist":  # the N>1 code path on one GPU: one-rank NCCL group, async averaging
+    if mode.startswith("hogwild_dist"):  # the N>1 code path on one GPU: one-rank NCCL group, async averaging
         cmd.append("--force-dist")
+    if mode == "hogwild_dist_chaoscomm":  # ... with the library's own communicator
+        cmd += ["--comm", "chaos"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
     assert out.returncode == 0, out.stderr[-3000:]
     d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
@@ -449,7 +451,7 @@ def test_bench_line_contract(mode, torch_cuda):
     assert d["e2e"]["h2d_bytes_per_step"] == 60000 * (841 + 1) * 4
     if mode == "hogwild":
         assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
-    if mode == "hogwild_dist":
+    if mode.startswith("hogwild_dist"):
         assert d["config"]["averaging"] == "async" and d["collectives"] >= 2
         assert d["eval"]["test_errors"] < 0.05 * d["eval"]["images"]
 
@@ -575,4 +577,30 @@ def test_async_averaging_runs_in_flight(torch_cuda):
     ml, ne = net.evaluate(Xt, Yt)
     ref = rec["per_epoch"][-1]
     assert abs(ne - ref["test_errors"]) / len(d.y_test) * 100 <= 0.5, (ne, ref)
+    net.close()
+
+
+def test_library_nccl_communicator_one_rank(torch_cuda):
+    # chaos_dist_* (include/chaos.h): with one rank the average is the identity, bitwise, for the
+    # parameters (net's stream) and for a caller buffer (caller stream); uninitialised -> error
+    import torch
+    from paper_1506_09067_b200 import ChaosError
+    _, net, _ = make("tiny", 3, torch_cuda)
+    with pytest.raises(ChaosError):
+        net.dist_average()
+    uid = net.dist_unique_id()
+    assert len(uid) == 128
+    net.dist_init(uid, 0, 1)
+    before = net.get_params()
+    net.dist_average()
+    net.sync()
+    np.testing.assert_array_equal(net.get_params(), before)
+    side = torch.cuda.Stream()
+    buf = torch.randn(1003, device="cuda")
+    ref = buf.clone()
+    net.dist_average_buffer(buf, side)
+    side.synchronize()
+    assert torch.equal(buf, ref)
+    with pytest.raises(ChaosError):
+        net.dist_init(uid, 0, 1)  # already initialised
     net.close()
