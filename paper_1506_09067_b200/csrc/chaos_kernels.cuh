@@ -2577,8 +2577,10 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 // W2 is still staged from the forward pass at W2OFF
                 conv_gw<C2, NT, MODE, false>(a, slot, a1, a2, am2, nullptr, O::c2w, cnt, sc);
                 __syncthreads();
+                PTIME(12);
                 conv_din<C2, NT>(wb + W2OFF, a2, am2, a1, a1, cnt);
                 __syncthreads();
+                PTIME(13);
             }
             // conv1: the images again (S was reused as scratch), then its gradient
             fence_async_smem();
