@@ -95,7 +95,7 @@ def test_appendix_a_closed_form_values():
 # --------------------------------------------------------------------------------------
 # Closed forms: zero-weight net
 # --------------------------------------------------------------------------------------
-@pytest.mark.parametrize("name", ["tiny", "medium", "large"])
+@pytest.mark.parametrize("name", ["tiny", "medium", "large", "paper_large"])
 def test_zero_weights(name):
     o = Oracle(sd.ARCHS[name])
     x = sd.uniform_dataset(5, 1, 0).x_train[0]
@@ -154,7 +154,7 @@ def torch_grad(arch, params, X, Y):
     return loss.item(), P.grad.numpy().copy(), h.detach().numpy()
 
 
-@pytest.mark.parametrize("name", ["tiny", "medium", "large", "paper_small"])
+@pytest.mark.parametrize("name", ["tiny", "medium", "large", "paper_small", "paper_large"])
 def test_against_torch_f64(name):
     arch = sd.ARCHS[name]
     o = Oracle(arch)
