@@ -109,12 +109,13 @@ int64_t chaos_net_device_params_len(const chaos_net* net); /* floats, incl. padd
 chaos_status chaos_train_epoch(chaos_net* net, const float* d_images, const int32_t* d_labels, int64_t n, float lr,
                                chaos_mode mode);
 /* Same, from HOST buffers -- the end-to-end entry point.  The images/labels are copied to
- * net-owned device staging buffers in ~n/8 chunks on a net-owned copy stream; chunk c trains
- * (on the net's stream) as soon as its own copy has landed, while chunk c+1 is in flight, so
- * the H2D transfer overlaps training (pinned host memory required for the overlap).  Sync mode
- * chunks on whole batches, so the result equals chaos_train_epoch(SYNC) bitwise; a hogwild
- * epoch is the same hogwild run with a claim barrier at each chunk boundary.  The debug claim
- * record (CHAOS_OPT_DEBUG_CLAIMS) then refers to the last chunk.  Synchronizing on return. */
+ * net-owned device staging buffers on a net-owned copy stream, overlapping training (pinned host
+ * memory required for the overlap).  Hogwild: ONE launch over [0, n); the copy stream lands
+ * ~n/16-image chunks and after each advances a device counter of landed images, and a worker that
+ * claims a group waits in its claim until the group has landed (so only the first chunk's copy
+ * is exposed; the debug claim record covers the whole epoch).  Sync: chunks of whole batches,
+ * chunk c+1 copied while chunk c trains, so the result equals chaos_train_epoch(SYNC) bitwise.
+ * Synchronizing on return. */
 chaos_status chaos_train_epoch_host(chaos_net* net, const float* h_images, const int32_t* h_labels, int64_t n,
                                     float lr, chaos_mode mode);
 /* Mean training loss (double) of the last chaos_train_epoch call; synchronizing. */

@@ -182,6 +182,7 @@ struct KArgs {
     float* out_logits;           // forward: [n][kClasses]
     unsigned long long* ptime;   // CHAOS_TIMING builds: per-CTA clock64 cycles per phase [grid][kPhases]
     unsigned long long* progress; // hogwild: monotonic count of images whose updates are published
+    const unsigned long long* ready;  // hogwild from host buffers: images [0, *ready) have landed
 };
 
 // Phase timing (instrumented build only, -DCHAOS_TIMING): thread 0 adds the clock64 cycles
@@ -2191,9 +2192,16 @@ __device__ __forceinline__ void fc_bwd(const KArgs& a, int slot, int woff, int b
 }
 
 // ------------------------------------------------------------------------------------
+// Host entry point: spin until the copy stream has landed images [0, need).
+__device__ __forceinline__ void wait_landed(const unsigned long long* ready, unsigned long long need) {
+    while (*reinterpret_cast<const volatile unsigned long long*>(ready) < need) __nanosleep(256);
+}
+
+// ------------------------------------------------------------------------------------
 // PHASE(worker) The worker kernel: hogwild training, sync-batch gradients, evaluation, forward.
 // ------------------------------------------------------------------------------------
-template <class Net, int G, int NT, int MODE>
+// GATED (hogwild from host buffers only): claims wait for the copy stream's landed-images counter.
+template <class Net, int G, int NT, int MODE, bool GATED = false>
 __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
     using C1 = typename Net::C1;
     using C2 = typename Net::C2;
@@ -2270,11 +2278,14 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
         // ---------------- a1: claim the next unprocessed images
         if (threadIdx.x == 0) {
             long long base;
-            if constexpr (MODE == kHogwild)
+            if constexpr (MODE == kHogwild) {
                 base = next_claim >= 0 ? next_claim
                                        : static_cast<long long>(atomicAdd(a.counter, static_cast<unsigned long long>(G)));
-            else
+                if constexpr (GATED)  // host entry: the copy stream advances *ready after each chunk
+                    if (base < a.n) wait_landed(a.ready, static_cast<unsigned long long>(min(base + G, a.n)));
+            } else {
                 base = (static_cast<long long>(blockIdx.x) + iter * gridDim.x) * G;
+            }
             *s_base = base < a.n ? static_cast<int>(base) : -1;
         }
         fence_proxy_async();  // earlier generic smem / global accesses precede the async proxy

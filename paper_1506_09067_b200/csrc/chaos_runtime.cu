@@ -106,6 +106,7 @@ struct NetDesc {
     int max_inflight = 1 << 30;  // hogwild staleness cap: #CTAs x G
     // [gi][mode]: gi 0 -> G=1, gi 1 -> G=gdef
     KernelFn fn[2][4] = {};
+    KernelFn fn_gated[2] = {};  // hogwild from host buffers (claims gated by the landed counter)
     int smem[2] = {0, 0};
     double flops_per_sample = 0;  // algorithmic
 };
@@ -151,6 +152,7 @@ void fill_kernels(NetDesc& d, int gi) {
     d.fn[gi][kSync] = chaos_worker<Net, G, Net::NT, kSync>;
     d.fn[gi][kEval] = chaos_worker<Net, G, Net::NT, kEval>;
     d.fn[gi][kForward] = chaos_worker<Net, G, Net::NT, kForward>;
+    d.fn_gated[gi] = chaos_worker<Net, G, Net::NT, kHogwild, true>;
     d.smem[gi] = SLayout<Net, G>::BYTES;
 }
 
@@ -300,6 +302,10 @@ struct chaos_net {
     ncclComm_t comm = nullptr;             // chaos_dist_init (library-owned communicator)
     int comm_world = 0;
     cudaStream_t copy_stream = nullptr;    // chaos_train_epoch_host: H2D chunks overlap training
+    unsigned long long* ready = nullptr;       // device: images landed (hogwild host entry)
+    unsigned long long* ready_host = nullptr;  // pinned: the per-chunk values the copy stream writes
+    long long ready_cap = 0;
+    const unsigned long long* launch_ready = nullptr;  // set around the host entry's single launch
     std::vector<cudaEvent_t> chunk_ev;
     cudaEvent_t staging_free = nullptr;
 };
@@ -309,7 +315,9 @@ namespace {
 int gidx(const chaos_net* net) { return net->group == 1 ? 0 : 1; }
 
 chaos_status ensure_kernel_attrs(chaos_net* net) {
-    for (int gi = 0; gi < 2; ++gi)
+    for (int gi = 0; gi < 2; ++gi) {
+        CUDA_TRY(cudaFuncSetAttribute(net->d->fn_gated[gi], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      net->d->smem[gi]));
         for (int m = 0; m < 4; ++m) {
             KernelFn f = net->d->fn[gi][m];
             CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, net->d->smem[gi]));
@@ -319,6 +327,7 @@ chaos_status ensure_kernel_attrs(chaos_net* net) {
                                      net->d->name, gi ? net->d->gdef : 1, m, net->d->smem[gi]);
             net->occ[gi][m] = occ;
         }
+    }
     return CHAOS_OK;
 }
 
@@ -572,6 +581,8 @@ void chaos_net_destroy(chaos_net* net) {
     cudaDeviceSynchronize();
     if (net->comm) nccl_api().destroy(net->comm);
     if (net->copy_stream) cudaStreamDestroy(net->copy_stream);
+    if (net->ready_host) cudaFreeHost(net->ready_host);
+    if (net->ready) cudaFree(net->ready);
     if (net->staging_free) cudaEventDestroy(net->staging_free);
     for (cudaEvent_t e : net->chunk_ev) cudaEventDestroy(e);
     void* ptrs[] = {net->params, net->latch,  net->counter, net->loss_sum, net->partial, net->grad_out, net->claims,
@@ -687,8 +698,10 @@ chaos_status train_range(chaos_net* net, const float* d_images, const int32_t* d
         k.ptime = net->ptime;
 #endif
         k.progress = net->progress;
+        k.ready = net->launch_ready;
         net->progress_enqueued += (unsigned long long)n;
-        net->d->fn[gidx(net)][kHogwild]<<<grid, net->d->nt, net->d->smem[gidx(net)], net->stream>>>(k);
+        KernelFn fn = k.ready ? net->d->fn_gated[gidx(net)] : net->d->fn[gidx(net)][kHogwild];
+        fn<<<grid, net->d->nt, net->d->smem[gidx(net)], net->stream>>>(k);
         CUDA_TRY(cudaGetLastError());
         return CHAOS_OK;
     }
@@ -741,8 +754,47 @@ chaos_status chaos_train_epoch_host(chaos_net* net, const float* h_images, const
         CUDA_TRY(cudaStreamCreateWithFlags(&net->copy_stream, cudaStreamNonBlocking));
         CUDA_TRY(cudaEventCreateWithFlags(&net->staging_free, cudaEventDisableTiming));
     }
-    // chunks of ~n/8 images (whole sync batches in sync mode; multiples of 16 images so every chunk
-    // start keeps the 16-B alignment of the TMA image copies): chunk c+1 is copied on the copy
+    if (mode == CHAOS_HOGWILD) {
+        // one launch over all n images; chunks of ~n/16 land on the copy stream, each followed by
+        // an 8-byte copy that advances the device counter `ready`; a worker that claims a group
+        // waits (spinning in its claim) until the group has landed -- no launch boundaries, only
+        // the first chunk's copy is exposed
+        long long chunk = (n + 15) / 16;
+        chunk = (chunk + 15) / 16 * 16;  // 16-image multiples keep the 16-B image alignment
+        if (chunk < 2048) chunk = 2048;
+        const long long nch = (n + chunk - 1) / chunk;
+        if (!net->ready) CUDA_TRY(cudaMalloc(&net->ready, sizeof(unsigned long long)));
+        if (net->ready_cap < nch) {
+            if (net->ready_host) cudaFreeHost(net->ready_host);
+            net->ready_host = nullptr;
+            CUDA_TRY(cudaMallocHost(&net->ready_host, sizeof(unsigned long long) * nch));
+            net->ready_cap = nch;
+        }
+        // zero the counter, then let the copy stream start (previous kernels are done with the
+        // staging buffers and with `ready` by then)
+        CUDA_TRY(cudaMemsetAsync(net->ready, 0, sizeof(unsigned long long), net->stream));
+        CUDA_TRY(cudaEventRecord(net->staging_free, net->stream));
+        CUDA_TRY(cudaStreamWaitEvent(net->copy_stream, net->staging_free, 0));
+        CUDA_TRY(cudaMemsetAsync(net->loss_sum, 0, sizeof(double), net->stream));
+        net->last_train_n = n;
+        for (long long c = 0; c < nch; ++c) {
+            const long long off = c * chunk;
+            const long long len = (n - off) < chunk ? (n - off) : chunk;
+            CUDA_TRY(cudaMemcpyAsync(net->st_x + off * 841, h_images + off * 841, sizeof(float) * 841 * len,
+                                     cudaMemcpyHostToDevice, net->copy_stream));
+            CUDA_TRY(cudaMemcpyAsync(net->st_y + off, h_labels + off, sizeof(int) * len, cudaMemcpyHostToDevice,
+                                     net->copy_stream));
+            net->ready_host[c] = static_cast<unsigned long long>(off + len);
+            CUDA_TRY(cudaMemcpyAsync(net->ready, net->ready_host + c, sizeof(unsigned long long),
+                                     cudaMemcpyHostToDevice, net->copy_stream));
+        }
+        net->launch_ready = net->ready;
+        chaos_status st = train_range(net, net->st_x, net->st_y, n, lr, mode);
+        net->launch_ready = nullptr;
+        if (st) return st;
+        return chaos_net_sync(net);
+    }
+    // sync mode: chunks of ~n/8 images in whole sync batches: chunk c+1 is copied on the copy
     // stream while chunk c trains on the net's stream
     const long long unit = (mode == CHAOS_SYNC) ? net->sync_batch : 16;
     long long chunk = (n + 7) / 8;

@@ -457,12 +457,12 @@ def test_bench_line_contract(mode, torch_cuda):
 
 
 def test_host_entry_hogwild_chunks_are_the_same_run(torch_cuda):
-    # chaos_train_epoch_host streams ~n/8-image chunks (>= 8192) through a copy stream; with one
-    # worker (1 CTA, G=1) hogwild is sequential SGD, so the chunked host run must equal the
-    # single-launch device run bit for bit across the chunk boundary
+    # chaos_train_epoch_host lands ~n/16-image chunks (>= 2048) on a copy stream while ONE launch
+    # trains, its claims gated by the landed-images counter; with one worker (1 CTA, G=1) hogwild
+    # is sequential SGD, so the streamed host run must equal the device run bit for bit
     from paper_1506_09067_b200 import OPT_MAX_CTAS
     import torch
-    n = 9000  # two chunks: 8192 + 808
+    n = 9000  # five chunks: 4 x 2048 + 808
     d = sd.prototype_dataset(19, n, 0)
     o, a, p = make("tiny", 19, torch_cuda, 1)
     a.set_option(OPT_MAX_CTAS, 1)
@@ -604,3 +604,16 @@ def test_library_nccl_communicator_one_rank(torch_cuda):
     with pytest.raises(ChaosError):
         net.dist_init(uid, 0, 1)  # already initialised
     net.close()
+
+
+def test_host_entry_hogwild_claims_each_image_once(torch_cuda):
+    # the streamed host entry at full width (all CTAs, default G): every image trained exactly once
+    from paper_1506_09067_b200 import OPT_DEBUG_CLAIMS
+    import torch
+    n = 30011
+    d = sd.prototype_dataset(23, n, 0)
+    _, net, _ = make("large", 23, torch_cuda)
+    net.set_option(OPT_DEBUG_CLAIMS, 1)
+    net.train_epoch_host(torch.from_numpy(d.x_train).pin_memory(), torch.from_numpy(d.y_train).pin_memory(), 0.001)
+    np.testing.assert_array_equal(net.debug_claims(n), np.ones(n, np.int32))
+    assert np.isfinite(net.last_train_loss())
