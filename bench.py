@@ -329,8 +329,8 @@ def main():
                "h2d_bytes_per_step": int(Xh.numel() * 4 + Yh.numel() * 4),
                "d2h_bytes_per_step": 8 if host_entry else 4,
                "path": "chaos_train_epoch_host (C ABI, host buffers)" if host_entry
-               else "DistTrainer.epoch_async(host=...): pinned H2D chunks on a copy stream overlap the "
-                    "chunk launches" if use_async
+               else "DistTrainer.epoch_async(host=...) -> chaos_train_epoch_host_async: one launch gated "
+                    "by the copy stream's landed-images counter, in-flight averages beside it" if use_async
                else "pinned H2D copy + step on the training stream"}
 
     if rank != 0:

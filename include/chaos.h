@@ -118,6 +118,11 @@ chaos_status chaos_train_epoch(chaos_net* net, const float* d_images, const int3
  * Synchronizing on return. */
 chaos_status chaos_train_epoch_host(chaos_net* net, const float* h_images, const int32_t* h_labels, int64_t n,
                                     float lr, chaos_mode mode);
+/* chaos_train_epoch_host without the final synchronization: returns once the copies and the
+ * launch(es) are enqueued (asynchronous on the net's and its copy stream).  The host buffers must
+ * stay valid (and unmodified) until the net's stream has passed the epoch (chaos_net_sync). */
+chaos_status chaos_train_epoch_host_async(chaos_net* net, const float* h_images, const int32_t* h_labels,
+                                          int64_t n, float lr, chaos_mode mode);
 /* Mean training loss (double) of the last chaos_train_epoch call; synchronizing. */
 chaos_status chaos_last_train_loss(chaos_net* net, double* mean_loss);
 

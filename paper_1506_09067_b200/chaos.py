@@ -31,7 +31,7 @@ EXPORTS = ["chaos_net_create", "chaos_net_destroy", "chaos_net_set_option", "cha
            "chaos_net_launch_info", "chaos_last_error", "chaos_last_status", "chaos_debug_phase_times",
            "chaos_batch_gradient", "chaos_apply_gradient", "chaos_progress_enqueued", "chaos_progress_wait",
            "chaos_avg_snapshot", "chaos_avg_apply", "chaos_dist_unique_id", "chaos_dist_init",
-           "chaos_dist_average", "chaos_dist_average_buffer"]
+           "chaos_dist_average", "chaos_dist_average_buffer", "chaos_train_epoch_host_async"]
 
 
 class ChaosError(RuntimeError):
@@ -72,6 +72,7 @@ def lib():
             "chaos_net_device_params_len": ([vp], C.c_int64),
             "chaos_train_epoch": ([vp, vp, vp, C.c_int64, C.c_float, C.c_int], C.c_int),
             "chaos_train_epoch_host": ([vp, fp, ip, C.c_int64, C.c_float, C.c_int], C.c_int),
+            "chaos_train_epoch_host_async": ([vp, fp, ip, C.c_int64, C.c_float, C.c_int], C.c_int),
             "chaos_last_train_loss": ([vp, C.POINTER(C.c_double)], C.c_int),
             "chaos_evaluate": ([vp, vp, vp, C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_int64)], C.c_int),
             "chaos_forward": ([vp, vp, C.c_int64, vp], C.c_int),
@@ -212,6 +213,16 @@ class Net:
             yp = labels.ctypes.data_as(C.POINTER(C.c_int32))
             n = len(labels)
         _check(lib().chaos_train_epoch_host(self._h, xp, yp, n, float(lr), int(mode)))
+
+    def train_epoch_host_async(self, images, labels, lr, mode=HOGWILD):
+        """chaos_train_epoch_host_async: pinned CPU torch tensors; returns once enqueued (the
+        tensors are kept referenced until the next sync of this net)."""
+        assert not images.is_cuda and images.is_contiguous() and images.dtype.itemsize == 4
+        assert not labels.is_cuda and labels.is_contiguous() and labels.dtype.itemsize == 4
+        self._host_refs = (images, labels)
+        xp = C.cast(C.c_void_p(images.data_ptr()), C.POINTER(C.c_float))
+        yp = C.cast(C.c_void_p(labels.data_ptr()), C.POINTER(C.c_int32))
+        _check(lib().chaos_train_epoch_host_async(self._h, xp, yp, int(labels.shape[0]), float(lr), int(mode)))
 
     def last_train_loss(self):
         v = C.c_double()

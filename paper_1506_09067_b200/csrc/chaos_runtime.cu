@@ -732,8 +732,26 @@ chaos_status chaos_train_epoch(chaos_net* net, const float* d_images, const int3
     return train_range(net, d_images, d_labels, n, lr, mode);
 }
 
+namespace {
+chaos_status host_epoch(chaos_net* net, const float* h_images, const int32_t* h_labels, int64_t n, float lr,
+                        chaos_mode mode, bool synchronize);
+}  // namespace
+
 chaos_status chaos_train_epoch_host(chaos_net* net, const float* h_images, const int32_t* h_labels, int64_t n,
                                     float lr, chaos_mode mode) {
+    return host_epoch(net, h_images, h_labels, n, lr, mode, true);
+}
+
+chaos_status chaos_train_epoch_host_async(chaos_net* net, const float* h_images, const int32_t* h_labels,
+                                          int64_t n, float lr, chaos_mode mode) {
+    return host_epoch(net, h_images, h_labels, n, lr, mode, false);
+}
+
+}  // extern "C"
+
+namespace {
+chaos_status host_epoch(chaos_net* net, const float* h_images, const int32_t* h_labels, int64_t n, float lr,
+                        chaos_mode mode, bool synchronize) {
     if (!net) return fail(CHAOS_E_INVALID, "net is NULL");
     if (n < 0) return fail(CHAOS_E_INVALID, "n < 0");
     if (n == 0) return chaos_train_epoch(net, nullptr, nullptr, 0, lr, mode);
@@ -792,7 +810,7 @@ chaos_status chaos_train_epoch_host(chaos_net* net, const float* h_images, const
         chaos_status st = train_range(net, net->st_x, net->st_y, n, lr, mode);
         net->launch_ready = nullptr;
         if (st) return st;
-        return chaos_net_sync(net);
+        return synchronize ? chaos_net_sync(net) : CHAOS_OK;
     }
     // sync mode: chunks of ~n/8 images in whole sync batches: chunk c+1 is copied on the copy
     // stream while chunk c trains on the net's stream
@@ -823,8 +841,11 @@ chaos_status chaos_train_epoch_host(chaos_net* net, const float* h_images, const
         chaos_status st = train_range(net, net->st_x + off * 841, net->st_y + off, len, lr, mode);
         if (st) return st;
     }
-    return chaos_net_sync(net);
+    return synchronize ? chaos_net_sync(net) : CHAOS_OK;
 }
+}  // namespace
+
+extern "C" {
 
 chaos_status chaos_last_train_loss(chaos_net* net, double* mean_loss) {
     if (!net || !mean_loss) return fail(CHAOS_E_INVALID, "NULL argument");

@@ -154,6 +154,11 @@ class DistTrainer:
             self.net.train_epoch(images[lo:hi], labels[lo:hi], lr)
             self.n_launches += 1
             return
+        if hasattr(self.net, "train_epoch_host_async"):
+            # the library's streamed host entry: one launch gated by the landed-images counter
+            self.net.train_epoch_host_async(host[0][lo:hi], host[1][lo:hi], lr)
+            self.n_launches += 1
+            return
         import torch
         ts = self.net.stream
         if getattr(self, "_copy_stream", None) is None:
