@@ -315,7 +315,7 @@ class Net:
 
     PHASES = ["claim", "stage", "conv1_fwd", "conv2_fwd", "conv3_fwd", "fc_fwd", "loss", "fc2_bwd", "fc1_bwd",
               "conv3_din", "conv3_gw", "w2_load", "conv2_gw", "conv2_din", "img_reload", "conv1_gw",
-              "fc1_fwd", "p17", "p18", "p19"]
+              "fc1_fwd", "c3din_warps", "c3gw_warps", "p19"]
 
     def phase_times(self):
         """Per-phase clock64 cycles of the last hogwild epoch, summed over CTAs (timing build only)."""

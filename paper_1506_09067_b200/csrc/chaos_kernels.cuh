@@ -2505,11 +2505,20 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                             dq4[e] = make_float4(ph == 0 ? d : 0.f, ph == 1 ? d : 0.f, ph == 2 ? d : 0.f, ph == 3 ? d : 0.f);
                         }
                         __syncthreads();
+#ifdef CHAOS_TIMING
+                        const long long t_split = clock64();  // slots 17 / 18: the two warp groups' own time
+#endif
                         if (threadIdx.x < DW * 32) {
                             conv_din_win<C3, NT, true>(wb, a3, am3, a2, sS, cnt, dq4);  // output over dq4 after
+#ifdef CHAOS_TIMING
+                            if (threadIdx.x == 0 && a.ptime) a.ptime[blockIdx.x * kPhases + 17] += clock64() - t_split;
+#endif
                         } else {
                             conv_gw_win<C3, NT, MODE, C3::GWIN, DW, NT / 32 - DW>(a, slot, a2, a3, am3, O::c3w, cnt,
                                                                                   sc, dq4);
+#ifdef CHAOS_TIMING
+                            if (threadIdx.x == DW * 32 && a.ptime) a.ptime[blockIdx.x * kPhases + 18] += clock64() - t_split;
+#endif
                             __syncthreads();  // pairs with conv_din_win's deferral barrier
                         }
                     } else {
