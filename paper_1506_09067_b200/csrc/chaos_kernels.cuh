@@ -2576,6 +2576,8 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                     conv_gw_mma<C2, NT, MODE>(a, slot, a1, sS, am2, wb + C2::BLK, O::c2w, cnt, sc);
                 else if constexpr (C2::MS > 0)
                     conv_gw3<C2, NT, MODE>(a, slot, a1, sS, am2, wb + C2::BLK, O::c2w, cnt, sc);
+                else if constexpr (C2::MS < 0)  // generic, lanes over output maps, published from registers
+                    conv_gw<C2, NT, MODE, false>(a, slot, a1, sS, am2, nullptr, O::c2w, cnt, sc);
                 else
                     conv_gw<C2, NT, MODE, true>(a, slot, a1, sS, am2, wb + C2::BLK, O::c2w, cnt, sc);
                 __syncthreads();
