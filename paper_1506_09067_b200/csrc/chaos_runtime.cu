@@ -60,7 +60,13 @@ struct LargeNet {  // configs[3], configs[4]
     // (delta_in) and 8-19 (weight gradient).  Tile sweeps: profiles/r1q.
     static constexpr int NCONV = 3, NFULL = 2, GDEF = 4, GINIT = 4, INFLIGHT = 592, NT = 640, SFL = 6400;
     //                C   H   W   M   K  KP  MT  TT  GS  RB  PB  MS  GWMMA  DIN3  GWIN  DWIN  NSPL
-    using C1 = Conv<1, 29, 29, 20, 4, 2, 10, 16, 16, 2>;
+#ifndef LARGE_C1_MT  // tile sweeps (scripts): -DLARGE_C1_MT=.. -DLARGE_C1_GS=..
+#define LARGE_C1_MT 10
+#endif
+#ifndef LARGE_C1_GS
+#define LARGE_C1_GS 16
+#endif
+    using C1 = Conv<1, 29, 29, 20, 4, 2, LARGE_C1_MT, 16, LARGE_C1_GS, 2>;
     using C2 = Conv<20, 13, 13, 60, 3, 2, 10, 9, 1, 4, 1, -1, false, true, 0, false, 1>;
     using C3 = Conv<60, 5, 5, 100, 2, 2, 4, 4, 1, 5, 2, 13, false, false, 4, true, 1>;
     using F1 = Full<400, 150, true>;
