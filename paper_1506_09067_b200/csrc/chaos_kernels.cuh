@@ -44,6 +44,17 @@ enum Latch : int { kLatchLabel = 1, kLatchNonfinite = 2 };
 
 __host__ __device__ constexpr int round4(int x) { return (x + 3) / 4 * 4; }
 
+// 2-conv nets whose conv2 delta_in splits each band's output-map loop over Net::DINSPLIT warps
+// (conv_din<..., MSPLIT>).
+template <class N, class = void>
+struct DinPair {
+    static constexpr int value = 1;
+};
+template <class N>
+struct DinPair<N, std::void_t<decltype(N::DINSPLIT)>> {
+    static constexpr int value = N::DINSPLIT;
+};
+
 // Nets whose conv3 / FC1 weights are too large to stage in shared memory (Table I large net,
 // SURVEY NEXT-1) declare BIGW = true: W1 + W2 are staged once per iteration and kept; conv3
 // and FC1 weights are read from L2 on demand.
@@ -157,7 +168,11 @@ struct SLayout {
     static constexpr int Z = HH + (Net::NFULL >= 2 ? round4(G * F1::OUT) : 0);
     static constexpr int BS = Z + G * kZStride;
     static constexpr int WB = BS + kBiasScratch;
-    static constexpr int FLOATS = WB + WBUF;
+    static constexpr int DPB = (Net::NCONV == 2 && DinPair<Net>::value > 1)
+                                   ? (Net::NT / 32 / DinPair<Net>::value) * (DinPair<Net>::value - 1) * C2::RB * C2::W *
+                                         (C2::C < 32 ? C2::C : 32)
+                                   : 0;
+    static constexpr int FLOATS = WB + WBUF + DPB;  // DPB: conv_din pair partial bands
     static constexpr int AM1 = 0;  // argmax bytes
     static constexpr int AM2 = AM1 + (C1::KP > 1 ? (G * C1::OUT_SZ + 15) / 16 * 16 : 0);  // pool 1x1: no argmax
     static constexpr int AM3 = AM2 + (Net::NCONV >= 2 ? (G * C2::OUT_SZ + 15) / 16 * 16 : 0);
@@ -1080,9 +1095,15 @@ __device__ __forceinline__ void conv_gw3(const KArgs& a, int slot, const float* 
 // band accumulator: exactly the argmax-sparse MACs, no atomics, no divergence.  W is the
 // staged (pre-update) snapshot (SURVEY C-9).  dout may alias in (in place).
 // ------------------------------------------------------------------------------------
-template <class L, int NT>
+// MSPLIT > 1: each (image, band, 32 maps) task is split over a group of MSPLIT warps, warp k of the
+// group taking output maps [k*M/MSPLIT, (k+1)*M/MSPLIT); warps 1.. leave their partial bands in
+// pbuf ([NT/32/MSPLIT][MSPLIT-1][RB*W][min(C,32)] floats, lane-fastest) and warp 0 adds them in order
+// (deterministic) and writes -- MSPLIT times the warp tasks for layers with few (the medium
+// net's conv2: 20 tasks for 16 warps).  Named barrier 1 + group.
+template <class L, int NT, int MSPLIT = 1>
 __device__ __forceinline__ void conv_din(const float* __restrict__ wsm, const float* __restrict__ dp,
-                                         const uint8_t* __restrict__ am, const float* in, float* dout, int cnt) {
+                                         const uint8_t* __restrict__ am, const float* in, float* dout, int cnt,
+                                         float* __restrict__ pbuf = nullptr) {
     constexpr int K = L::K, KP = L::KP, KK = L::KK, PW = L::PW, PH = L::PH, P = L::P, M = L::M, C = L::C;
     constexpr int HW = L::H * L::W, RB = L::RB, NB = L::NB;
     constexpr int R2 = (NB == 1) ? 0 : RB / KP;       // window rows per band step
@@ -1093,13 +1114,20 @@ __device__ __forceinline__ void conv_din(const float* __restrict__ wsm, const fl
     constexpr int NW = NT / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int total = cnt * NB * NCW;
-    for (int vw = warp; vw < total; vw += NW) {
+    constexpr bool PAIR = MSPLIT > 1;
+    static_assert(!PAIR || (NW % MSPLIT == 0 && NW / MSPLIT <= 15), "warp groups, named barriers 1..15");
+    const int half = PAIR ? (warp % MSPLIT) : 0;  // the warp's part of the map loop
+    const int grp = warp / MSPLIT;
+    const int m_lo = half * M / MSPLIT, m_hi = (half + 1) * M / MSPLIT;
+    for (int vw = PAIR ? grp : warp; vw < total; vw += PAIR ? NW / MSPLIT : NW) {
         const int cw = vw % NCW;
         const int t = vw / NCW;
         const int b = t % NB;
         const int g = t / NB;
-        const int n = cw * 32 + lane;
-        if (n >= C) continue;
+        const int n0 = cw * 32 + lane;
+        if (!PAIR && n0 >= C) continue;  // (pairs: every lane reaches the pair barriers)
+        const bool act = n0 < C;
+        const int n = act ? n0 : 0;
         float acc[RB][L::W];
 #pragma unroll
         for (int r = 0; r < RB; ++r)
@@ -1110,7 +1138,7 @@ __device__ __forceinline__ void conv_din(const float* __restrict__ wsm, const fl
         const uint8_t* amg = am + g * L::OUT_SZ;
         const int pr0 = b * R2;
 #pragma unroll 1
-        for (int m = 0; m < M; ++m) {
+        for (int m = m_lo; m < m_hi; ++m) {
             float w[KK];
 #pragma unroll
             for (int tp = 0; tp < KK; ++tp) w[tp] = wn[tp * L::MP + m];
@@ -1151,6 +1179,28 @@ __device__ __forceinline__ void conv_din(const float* __restrict__ wsm, const fl
                     }
                 }
             }
+        }
+        if constexpr (PAIR) {
+            constexpr int CL = C < 32 ? C : 32;  // lanes that carry a map
+            constexpr int SL = RB * L::W * CL;   // one partial band
+            float* pb = pbuf + grp * (MSPLIT - 1) * SL + (lane < CL ? lane : 0);
+            if (half > 0 && lane < CL) {
+#pragma unroll
+                for (int r = 0; r < RB; ++r)
+#pragma unroll
+                    for (int c = 0; c < L::W; ++c) pb[(half - 1) * SL + (r * L::W + c) * CL] = acc[r][c];
+            }
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(32 * MSPLIT) : "memory");
+            if (half == 0 && lane < CL) {
+#pragma unroll
+                for (int k = 0; k < MSPLIT - 1; ++k)
+#pragma unroll
+                    for (int r = 0; r < RB; ++r)
+#pragma unroll
+                        for (int c = 0; c < L::W; ++c) acc[r][c] += pb[k * SL + (r * L::W + c) * CL];
+            }
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(32 * MSPLIT) : "memory");  // pb free again
+            if (half != 0 || !act) continue;
         }
         const float* ib = in + g * L::IN_SZ + n * HW + b * RB * L::W;
         float* ob = dout + g * L::IN_SZ + n * HW + b * RB * L::W;
@@ -2600,7 +2650,10 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 conv_gw<C2, NT, MODE, false>(a, slot, a1, a2, am2, nullptr, O::c2w, cnt, sc);
                 __syncthreads();
                 PTIME(12);
-                conv_din<C2, NT>(wb + W2OFF, a2, am2, a1, a1, cnt);
+                if constexpr (DinPair<Net>::value > 1)
+                    conv_din<C2, NT, DinPair<Net>::value>(wb + W2OFF, a2, am2, a1, a1, cnt, wb + S::WBUF);
+                else
+                    conv_din<C2, NT>(wb + W2OFF, a2, am2, a1, a1, cnt);
                 __syncthreads();
                 PTIME(13);
             }

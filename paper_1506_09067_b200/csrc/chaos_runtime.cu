@@ -39,6 +39,10 @@ struct TinyNet {  // configs[0], configs[1]: conv5 4x4 -> tanh -> pool2 -> FC 84
 };
 struct MediumNet {  // configs[2] = Table I medium
     static constexpr int NCONV = 2, NFULL = 2, GDEF = 4, GINIT = 4, INFLIGHT = 592, NT = 512, SFL = 6000;
+#ifndef MEDIUM_DINSPLIT
+#define MEDIUM_DINSPLIT 4
+#endif
+    static constexpr int DINSPLIT = MEDIUM_DINSPLIT;  // conv2 delta_in: warps per (image, band) task
     using C1 = Conv<1, 29, 29, 20, 4, 2, 10, 16, 16, 2>;
     using C2 = Conv<20, 13, 13, 40, 5, 3, 4, 25, 1, 3>;
     using C3 = C2;
