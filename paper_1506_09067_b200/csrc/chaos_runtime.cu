@@ -52,6 +52,10 @@ struct MediumNet {  // configs[2] = Table I medium
 struct PaperSmallNet {  // Table I small: conv5 4x4 -> pool2 -> conv10 5x5 -> pool3
                         // -> FC 90->50 tanh -> FC 50->10; same generic kernels as the medium net
     static constexpr int NCONV = 2, NFULL = 2, GDEF = 4, GINIT = 1, INFLIGHT = 148, NT = 256, SFL = 3364;
+#ifndef PSMALL_DINSPLIT
+#define PSMALL_DINSPLIT 2
+#endif
+    static constexpr int DINSPLIT = PSMALL_DINSPLIT;
     using C1 = Conv<1, 29, 29, 5, 4, 2, /*MT*/ 5, /*TT*/ 16, /*GS*/ 32, /*RB*/ 2>;
     using C2 = Conv<5, 13, 13, 10, 5, 3, /*MT*/ 2, /*TT*/ 25, /*GS*/ 1, /*RB*/ 3>;
     using C3 = C2;
