@@ -90,7 +90,7 @@ struct Conv {
     static constexpr int NBAND = PB > 0 ? (PH + PB - 1) / PB : 0;
     static constexpr int BR = PB * KP + K - 1;                        // input rows per band
     static constexpr int HAND = NBAND > 1 ? (NBAND - 1) * (K - 1) * WR * C : 0;  // hand-off floats per image
-    // weight gradient by (set of MS output maps, 32 input maps) warps (conv_gw3) when MS > 0
+    // MS < 0: the weight gradient by the generic conv_gw published from registers (lanes over maps)
     static constexpr int MS = MS_;
     // weight gradient on the tensor cores (conv_gw_mma)
     static constexpr bool GWMMA = GWMMA_;
@@ -438,11 +438,9 @@ __device__ __forceinline__ float warp_sum(float v) {
 // one pooled window x one image; the KP*KP conv outputs of the window stay in registers,
 // the weights of the MT maps are warp-uniform vector loads from the staged block.
 // ------------------------------------------------------------------------------------
-template <class L, int NT, bool PFW = false>
+template <class L, int NT>
 __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const float* __restrict__ wsm,
                                          float* __restrict__ out, uint8_t* __restrict__ am, int cnt) {
-    // PFW: the weights are in global memory (BIGW conv3): each thread prefetches one tap row of
-    // the next input map's weights into L1, so the block's loads of map n+1 hit L1
     constexpr int MT = L::MT, KP = L::KP, K = L::K, PW = L::PW, P = L::P, MG = L::M / MT;
     constexpr int PS = KP + K - 1;
     constexpr bool A4 = (MT % 4 == 0) || (MG == 1);
@@ -470,10 +468,6 @@ __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const flo
         const float* wb = wsm + mg * MT;
 #pragma unroll 1
         for (int n = half * CH; n < (half + 1) * CH; ++n) {
-            if constexpr (PFW) {
-                if (n + 1 < (half + 1) * CH)
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(wb + ((n + 1) * L::KK + threadIdx.x % L::KK) * L::MP));
-            }
             float patch[PS][PS];
 #pragma unroll
             for (int u = 0; u < PS; ++u)
@@ -975,111 +969,6 @@ __device__ __forceinline__ void conv_gw_mma(const KArgs& a, int slot, const floa
     }
     if constexpr (L::MP > M) {  // padding columns of the block publish zeros
         for (int e = threadIdx.x; e < L::ROWS * (L::MP - M); e += NT)
-            scr[(e / (L::MP - M)) * L::MP + M + e % (L::MP - M)] = 0.f;
-    }
-    sync_for_async();
-    publish_bulk<MODE>(a, slot, woff, scr, L::BLK);
-}
-
-// ------------------------------------------------------------------------------------
-// PHASE(conv_gw3) conv weight gradient (KP == 2), one warp per (set of MS output maps,
-// 32 input maps); lanes over the input map n:
-//   gW[n][i][j][m] = sum_g sum_w dp[g][m][w] * in[g][n][argpos(g,m,w) + (i,j)],  gb[m] = sum dp
-// For each (image, pooled row) the lane loads the BR x WR band of its input map that the
-// row's windows can reach into registers once; then for every window and every m of the set
-// the argmax phase (the same for all lanes: one m, one window) selects, by a warp-uniform
-// two-level branch, which compile-time band registers feed the K*K MACs.  All lanes read the
-// same relative position, so the band loads are conflict-free; delta / argmax are broadcasts.
-// Fixed (g, window) summation order per element (deterministic).
-// ------------------------------------------------------------------------------------
-template <class L, int NT, int MODE>
-__device__ __forceinline__ void conv_gw3(const KArgs& a, int slot, const float* __restrict__ in,
-                                         const float* __restrict__ dp, const uint8_t* __restrict__ am,
-                                         float* __restrict__ scr, int woff, int cnt, float sc) {
-    constexpr int K = L::K, KP = L::KP, KK = L::KK, PW = L::PW, PH = L::PH, P = L::P, M = L::M, C = L::C;
-    constexpr int W = L::W, HW = L::H * L::W, MS = L::MS, NSET = (M + MS - 1) / MS;
-    constexpr int NCW = (C + 31) / 32, BH = KP + K - 1, BW = PW * KP + K - 1;
-    constexpr int NW = NT / 32;
-    static_assert(KP == 2, "conv_gw3 handles 2x2 pooling");
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int task = warp; task < NSET * NCW; task += NW) {
-        const int cw = task % NCW;
-        const int m0 = (task / NCW) * MS;
-        const int n = cw * 32 + lane;
-        const bool act = n < C;
-        float acc[MS][KK];
-        float accb[MS];
-#pragma unroll
-        for (int q = 0; q < MS; ++q) {
-            accb[q] = 0.f;
-#pragma unroll
-            for (int t = 0; t < KK; ++t) acc[q][t] = 0.f;
-        }
-#pragma unroll 1
-        for (int g = 0; g < cnt; ++g) {
-            const float* ing = in + g * L::IN_SZ + (act ? n : 0) * HW;
-            const float* dpg = dp + g * L::OUT_SZ;
-            const uint8_t* amg = am + g * L::OUT_SZ;
-#pragma unroll 1
-            for (int pr = 0; pr < PH; ++pr) {
-                float band[BH][BW];
-#pragma unroll
-                for (int r = 0; r < BH; ++r)
-#pragma unroll
-                    for (int c = 0; c < BW; ++c) band[r][c] = ing[(pr * KP + r) * W + c];
-#pragma unroll
-                for (int q = 0; q < MS; ++q) {
-                    if (MS * NSET == M || m0 + q < M) {  // warp-uniform
-                        const int ob = (m0 + q) * P + pr * PW;
-                        float dv[PW];
-                        int av[PW];
-#pragma unroll
-                        for (int pc = 0; pc < PW; ++pc) {
-                            dv[pc] = dpg[ob + pc];
-                            av[pc] = amg[ob + pc];
-                        }
-#pragma unroll
-                        for (int pc = 0; pc < PW; ++pc) {
-                            const float d = dv[pc];
-                            const int arg = av[pc];
-                            accb[q] += d;
-                            if (arg < 2) {
-                                if (arg == 0) {
-#pragma unroll
-                                    for (int t = 0; t < KK; ++t)
-                                        acc[q][t] = fmaf(d, band[t / K][pc * KP + t % K], acc[q][t]);
-                                } else {
-#pragma unroll
-                                    for (int t = 0; t < KK; ++t)
-                                        acc[q][t] = fmaf(d, band[t / K][pc * KP + 1 + t % K], acc[q][t]);
-                                }
-                            } else {
-                                if (arg == 2) {
-#pragma unroll
-                                    for (int t = 0; t < KK; ++t)
-                                        acc[q][t] = fmaf(d, band[1 + t / K][pc * KP + t % K], acc[q][t]);
-                                } else {
-#pragma unroll
-                                    for (int t = 0; t < KK; ++t)
-                                        acc[q][t] = fmaf(d, band[1 + t / K][pc * KP + 1 + t % K], acc[q][t]);
-                                }
-                            }
-                        }
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < MS; ++q) {
-            if (act && (MS * NSET == M || m0 + q < M)) {
-#pragma unroll
-                for (int t = 0; t < KK; ++t) scr[(n * KK + t) * L::MP + m0 + q] = sc * acc[q][t];
-                if (n == 0) scr[L::WFL + m0 + q] = sc * accb[q];
-            }
-        }
-    }
-    if constexpr (L::MP > M) {  // padding columns of the block publish zeros
-        for (int e = threadIdx.x; e < (L::ROWS + 1) * (L::MP - M); e += NT)
             scr[(e / (L::MP - M)) * L::MP + M + e % (L::MP - M)] = 0.f;
     }
     sync_for_async();
@@ -2593,8 +2482,6 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 PTIME(9);
                 if constexpr (C3::GWMMA)
                     conv_gw_mma<C3, NT, MODE>(a, slot, a2, a3, am3, wb, O::c3w, cnt, sc);
-                else if constexpr (C3::MS > 0)
-                    conv_gw3<C3, NT, MODE>(a, slot, a2, a3, am3, wb, O::c3w, cnt, sc);
                 else
                     conv_gw<C3, NT, MODE, true>(a, slot, a2, a3, am3, wb, O::c3w, cnt, sc);
                 }
@@ -2624,8 +2511,6 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 } else {
                 if constexpr (C2::GWMMA)
                     conv_gw_mma<C2, NT, MODE>(a, slot, a1, sS, am2, wb + C2::BLK, O::c2w, cnt, sc);
-                else if constexpr (C2::MS > 0)
-                    conv_gw3<C2, NT, MODE>(a, slot, a1, sS, am2, wb + C2::BLK, O::c2w, cnt, sc);
                 else if constexpr (C2::MS < 0)  // generic, lanes over output maps, published from registers
                     conv_gw<C2, NT, MODE, false>(a, slot, a1, sS, am2, nullptr, O::c2w, cnt, sc);
                 else

@@ -76,7 +76,7 @@ struct LargeNet {  // configs[3], configs[4]
 #endif
     using C1 = Conv<1, 29, 29, 20, 4, 2, LARGE_C1_MT, 16, LARGE_C1_GS, 2>;
     using C2 = Conv<20, 13, 13, 60, 3, 2, 10, 9, 1, 4, 1, -1, false, true, 0, false, 1>;
-    using C3 = Conv<60, 5, 5, 100, 2, 2, 4, 4, 1, 5, 2, 13, false, false, 4, true, 1>;
+    using C3 = Conv<60, 5, 5, 100, 2, 2, 4, 4, 1, 5, 2, 0, false, false, 4, true, 1>;
     using F1 = Full<400, 150, true>;
     using F2 = Full<150, 10, false>;
 };
