@@ -172,7 +172,10 @@ struct SLayout {
                                    ? (Net::NT / 32 / DinPair<Net>::value) * (DinPair<Net>::value - 1) * C2::RB * C2::W *
                                          (C2::C < 32 ? C2::C : 32)
                                    : 0;
-    static constexpr int FLOATS = WB + WBUF + DPB;  // DPB: conv_din pair partial bands
+    // FWB: the 1-conv nets' (tiny) FC weights + bias, TMA-staged per iteration (read twice, by
+    // the forward and by delta_in, instead of twice from L2)
+    static constexpr int FWB = (Net::NCONV == 1 && Net::NFULL == 1) ? F1::WFL + F1::BFL : 0;
+    static constexpr int FLOATS = WB + WBUF + DPB + FWB;  // DPB: conv_din pair partial bands
     static constexpr int AM1 = 0;  // argmax bytes
     static constexpr int AM2 = AM1 + (C1::KP > 1 ? (G * C1::OUT_SZ + 15) / 16 * 16 : 0);  // pool 1x1: no argmax
     static constexpr int AM3 = AM2 + (Net::NCONV >= 2 ? (G * C2::OUT_SZ + 15) / 16 * 16 : 0);
@@ -1370,7 +1373,7 @@ __device__ __forceinline__ void conv_din2(const float* __restrict__ wsm, const f
 // PHASE(fc_fwd) fully connected forward: one warp per output row, lanes over inputs,
 // weights streamed from L2 (__ldcg: on-demand reads of the shared store, no stale L1 copy).
 // ------------------------------------------------------------------------------------
-template <class F, int G, int NT>
+template <class F, int G, int NT, bool SMEMW = false>  // SMEMW: W and b staged in shared memory
 __device__ __forceinline__ void fc_fwd(const float* __restrict__ Wg, const float* __restrict__ bg,
                                        const float* __restrict__ in, float* __restrict__ out, int ostride,
                                        int cnt) {
@@ -1383,11 +1386,11 @@ __device__ __forceinline__ void fc_fwd(const float* __restrict__ Wg, const float
         const float* wr = Wg + static_cast<long long>(o) * F::IN;
 #pragma unroll 4
         for (int i = lane; i < F::IN; i += 32) {
-            const float w = __ldcg(wr + i);
+            const float w = SMEMW ? wr[i] : __ldcg(wr + i);
 #pragma unroll
             for (int g = 0; g < G; ++g) acc[g] = fmaf(w, in[g * F::IN + i], acc[g]);
         }
-        const float b = __ldcg(bg + o);
+        const float b = SMEMW ? bg[o] : __ldcg(bg + o);
 #pragma unroll
         for (int g = 0; g < G; ++g) {
             const float s = warp_sum(acc[g]) + b;
@@ -2052,7 +2055,8 @@ __device__ __forceinline__ void fc_bwd3(const KArgs& a, int slot, int woff, int 
 template <class F, int G, int NT, int MODE, int SHALF>
 __device__ __forceinline__ void fc_bwd(const KArgs& a, int slot, int woff, int boff, float* __restrict__ in,
                                        const float* __restrict__ dz, int dstride, float* __restrict__ S,
-                                       float* __restrict__ bsc, int cnt, float sc) {
+                                       float* __restrict__ bsc, int cnt, float sc,
+                                       const float* __restrict__ wstaged = nullptr) {  // W staged in smem
     constexpr int RPC0 = SHALF / F::IN;  // rows per chunk
     constexpr int RPC = (RPC0 >= F::OUT) ? F::OUT : ((RPC0 * F::IN) % 4 == 0 ? RPC0 : RPC0 / 4 * 4);
     static_assert(RPC >= 1, "S half must hold a weight row");
@@ -2086,7 +2090,9 @@ __device__ __forceinline__ void fc_bwd(const KArgs& a, int slot, int woff, int b
                     float w[4];
 #pragma unroll
                     for (int q = 0; q < 4; ++q)
-                        w[q] = (o + q < o1) ? __ldcg(Wg + static_cast<long long>(o + q) * F::IN + col) : 0.f;
+                        w[q] = (o + q < o1) ? (wstaged ? wstaged[(o + q) * F::IN + col]
+                                                       : __ldcg(Wg + static_cast<long long>(o + q) * F::IN + col))
+                                            : 0.f;
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         if (o + q < o1) {
@@ -2187,6 +2193,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
     float* zz = fa + S::Z;
     float* bsc = fa + S::BS;
     float* wb = fa + S::WB;
+    float* fwb = fa + S::WB + S::WBUF + S::DPB;  // S::FWB floats (tiny: FC weights)
     uint8_t* amb = smem + kHdrBytes + S::FLOATS * 4;
     uint8_t* am1 = amb + S::AM1;
     uint8_t* am2 = amb + S::AM2;
@@ -2261,6 +2268,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 }
         }
         if constexpr (NCONV >= 2) L1.issue(wb + W2OFF, P + O::c2w, C2::BLK);
+        if constexpr (S::FWB > 0) L1.issue(fwb, P + O::f1w, S::FWB);  // FC W then b (contiguous)
         if (!x_bulk)
             for (int i = threadIdx.x; i < cnt * IMG; i += NT) sS[i] = __ldg(xsrc + i);
         L0.wait();
@@ -2310,7 +2318,12 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             PTIME(16);
             fc_fwd<F2, G, NT>(P + O::f2w, P + O::f2b, hh, zz, kZStride, cnt);
         } else {
-            fc_fwd<F1, G, NT>(P + O::f1w, P + O::f1b, alast, zz, kZStride, cnt);
+            if constexpr (S::FWB > 0) {
+                L1.wait();
+                fc_fwd<F1, G, NT, true>(fwb, fwb + F1::WFL, alast, zz, kZStride, cnt);
+            } else {
+                fc_fwd<F1, G, NT>(P + O::f1w, P + O::f1b, alast, zz, kZStride, cnt);
+            }
         }
         __syncthreads();
         PTIME(5);
@@ -2383,7 +2396,8 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                     fc_bwd<F1, G, NT, MODE, SHALF>(a, slot, O::f1w, O::f1b, alast, hh, F1::OUT, sS, bsc, cnt, sc);
                 }
             } else {
-                fc_bwd<F1, G, NT, MODE, SHALF>(a, slot, O::f1w, O::f1b, alast, zz, kZStride, sS, bsc, cnt, sc);
+                fc_bwd<F1, G, NT, MODE, SHALF>(a, slot, O::f1w, O::f1b, alast, zz, kZStride, sS, bsc, cnt, sc,
+                                               S::FWB > 0 ? fwb : nullptr);
             }
             wait_publish_reads();
             PTIME(8);
