@@ -2395,11 +2395,17 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 } else {
                     fc_bwd<F1, G, NT, MODE, SHALF>(a, slot, O::f1w, O::f1b, alast, hh, F1::OUT, sS, bsc, cnt, sc);
                 }
+            } else if constexpr (S::FWB > 0) {
+                // tiny: the gradient chunk goes to S's upper half, so the images in its lower half
+                // survive for conv1's gradient (no reload, no wait for the publish's reads here)
+                static_assert(F1::WFL <= SHALF && G * IMG <= SHALF, "one chunk above the images");
+                fc_bwd<F1, G, NT, MODE, SHALF>(a, slot, O::f1w, O::f1b, alast, zz, kZStride, sS + SHALF, bsc, cnt,
+                                               sc, fwb);
+                __syncthreads();
             } else {
-                fc_bwd<F1, G, NT, MODE, SHALF>(a, slot, O::f1w, O::f1b, alast, zz, kZStride, sS, bsc, cnt, sc,
-                                               S::FWB > 0 ? fwb : nullptr);
+                fc_bwd<F1, G, NT, MODE, SHALF>(a, slot, O::f1w, O::f1b, alast, zz, kZStride, sS, bsc, cnt, sc);
             }
-            wait_publish_reads();
+            if constexpr (S::FWB == 0) wait_publish_reads();
             PTIME(8);
             // ---------------- a6/a7: pool + conv backward, publish per layer
             if constexpr (NCONV == 3 && BIG) {
@@ -2557,14 +2563,16 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 PTIME(13);
             }
             // conv1: the images again (S was reused as scratch), then its gradient
-            fence_async_smem();
-            wait_publish_reads();
-            if (x_bulk) {
-                L0.issue(sS, xsrc, cnt * IMG);
-                L0.wait();
-            } else {
-                for (int i = threadIdx.x; i < cnt * IMG; i += NT) sS[i] = __ldg(xsrc + i);
-                __syncthreads();
+            if constexpr (S::FWB == 0) {
+                fence_async_smem();
+                wait_publish_reads();
+                if (x_bulk) {
+                    L0.issue(sS, xsrc, cnt * IMG);
+                    L0.wait();
+                } else {
+                    for (int i = threadIdx.x; i < cnt * IMG; i += NT) sS[i] = __ldg(xsrc + i);
+                    __syncthreads();
+                }
             }
             PTIME(14);
             conv_gw<C1, NT, MODE, true>(a, slot, sS, a1, am1, wb, O::c1w, cnt, sc);
