@@ -31,7 +31,13 @@ namespace {
 // sequential SGD with 592.  GINIT is the group G a new net starts with.
 struct TinyNet {  // configs[0], configs[1]: conv5 4x4 -> tanh -> pool2 -> FC 845->10
     static constexpr int NCONV = 1, NFULL = 1, GDEF = 4, GINIT = 1, INFLIGHT = 148, NT = 256, SFL = 2 * 8456;
-    using C1 = Conv<1, 29, 29, 5, 4, 2, /*MT*/ 5, /*TT*/ 16, /*GS*/ 32, /*RB*/ 2>;
+#ifndef TINY_C1_GS  // tile sweeps: -DTINY_C1_GS=.. -DTINY_C1_TT=..
+#define TINY_C1_GS 16
+#endif
+#ifndef TINY_C1_TT
+#define TINY_C1_TT 16
+#endif
+    using C1 = Conv<1, 29, 29, 5, 4, 2, /*MT*/ 5, /*TT*/ TINY_C1_TT, /*GS*/ TINY_C1_GS, /*RB*/ 2>;
     using C2 = C1;
     using C3 = C1;
     using F1 = Full<845, 10, false>;
