@@ -29,8 +29,11 @@ namespace {
 // are in flight per GPU (#CTAs x G).  Measured on the B200 (scripts/hogwild_sweep.py): the tiny
 // net at lr 0.001 blows up in epoch 1 with 592-1184 in flight, the large net trains like
 // sequential SGD with 592.  GINIT is the group G a new net starts with.
+#ifndef TINY_NT
+#define TINY_NT 512
+#endif
 struct TinyNet {  // configs[0], configs[1]: conv5 4x4 -> tanh -> pool2 -> FC 845->10
-    static constexpr int NCONV = 1, NFULL = 1, GDEF = 4, GINIT = 1, INFLIGHT = 148, NT = 256, SFL = 2 * 8456;
+    static constexpr int NCONV = 1, NFULL = 1, GDEF = 4, GINIT = 1, INFLIGHT = 148, NT = TINY_NT, SFL = 2 * 8456;
 #ifndef TINY_C1_GS  // tile sweeps: -DTINY_C1_GS=.. -DTINY_C1_TT=..
 #define TINY_C1_GS 16
 #endif
