@@ -58,9 +58,12 @@ struct MediumNet {  // configs[2] = Table I medium
     using F1 = Full<360, 150, true>;
     using F2 = Full<150, 10, false>;
 };
+#ifndef PSMALL_NT
+#define PSMALL_NT 512
+#endif
 struct PaperSmallNet {  // Table I small: conv5 4x4 -> pool2 -> conv10 5x5 -> pool3
                         // -> FC 90->50 tanh -> FC 50->10; same generic kernels as the medium net
-    static constexpr int NCONV = 2, NFULL = 2, GDEF = 4, GINIT = 1, INFLIGHT = 148, NT = 256, SFL = 3364;
+    static constexpr int NCONV = 2, NFULL = 2, GDEF = 4, GINIT = 1, INFLIGHT = 148, NT = PSMALL_NT, SFL = 3364;
 #ifndef PSMALL_DINSPLIT
 #define PSMALL_DINSPLIT 2
 #endif
