@@ -46,8 +46,11 @@ struct TinyNet {  // configs[0], configs[1]: conv5 4x4 -> tanh -> pool2 -> FC 84
     using F1 = Full<845, 10, false>;
     using F2 = F1;
 };
+#ifndef MEDIUM_NT
+#define MEDIUM_NT 512
+#endif
 struct MediumNet {  // configs[2] = Table I medium
-    static constexpr int NCONV = 2, NFULL = 2, GDEF = 4, GINIT = 4, INFLIGHT = 592, NT = 512, SFL = 6000;
+    static constexpr int NCONV = 2, NFULL = 2, GDEF = 4, GINIT = 4, INFLIGHT = 592, NT = MEDIUM_NT, SFL = 6000;
 #ifndef MEDIUM_DINSPLIT
 #define MEDIUM_DINSPLIT 4
 #endif
