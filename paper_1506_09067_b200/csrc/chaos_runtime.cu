@@ -56,7 +56,13 @@ struct MediumNet {  // configs[2] = Table I medium
 #endif
     static constexpr int DINSPLIT = MEDIUM_DINSPLIT;  // conv2 delta_in: warps per (image, band) task
     using C1 = Conv<1, 29, 29, 20, 4, 2, 10, 16, 16, 2>;
-    using C2 = Conv<20, 13, 13, 40, 5, 3, 4, 25, 1, 3>;
+#ifndef MEDIUM_C2_MT
+#define MEDIUM_C2_MT 4
+#endif
+#ifndef MEDIUM_C2_NSPL
+#define MEDIUM_C2_NSPL 1
+#endif
+    using C2 = Conv<20, 13, 13, 40, 5, 3, MEDIUM_C2_MT, 25, 1, 3, 0, 0, false, false, 0, false, MEDIUM_C2_NSPL>;
     using C3 = C2;
     using F1 = Full<360, 150, true>;
     using F2 = Full<150, 10, false>;
