@@ -2418,7 +2418,13 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 conv_din_gm<C3, NT, Net::RB3>(P + O::c3w, a3, am3, a2, a1, cnt);
                 __syncthreads();
                 PTIME(9);
-                conv_gw_wt<C3, NT, MODE, 4, 2>(a, slot, a2, a3, am3, O::c3w, cnt, sc);
+#ifndef CHAOS_PL_GW_NM  // tile sweeps (Table I large conv3 weight gradient)
+#define CHAOS_PL_GW_NM 4
+#endif
+#ifndef CHAOS_PL_GW_KR
+#define CHAOS_PL_GW_KR 3
+#endif
+                conv_gw_wt<C3, NT, MODE, CHAOS_PL_GW_NM, CHAOS_PL_GW_KR>(a, slot, a2, a3, am3, O::c3w, cnt, sc);
                 __syncthreads();
                 PTIME(10);
                 for (int e = threadIdx.x; e < cnt * C2::OUT_SZ; e += NT) a2[e] = a1[e];

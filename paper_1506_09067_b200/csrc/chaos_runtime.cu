@@ -106,7 +106,10 @@ struct PaperLargeNet {  // Table I large: conv
                        // -> pool2 -> conv100 6x6 -> pool2 -> FC 900->150 tanh -> FC 150->10.  383,160
                        // weights: W1 + W2 staged and kept, W3 (864 KB) and FC1 (540 KB) read from L2 (BIGW);
                        // one image per worker (224 KB of shared memory)
-    static constexpr int NCONV = 3, NFULL = 2, GDEF = 1, GINIT = 1, INFLIGHT = 148, NT = 384, SFL = 1800, RB3 = 4;
+#ifndef PL_RB3
+#define PL_RB3 4
+#endif
+    static constexpr int NCONV = 3, NFULL = 2, GDEF = 1, GINIT = 1, INFLIGHT = 148, NT = 384, SFL = 1800, RB3 = PL_RB3;
     static constexpr bool BIGW = true;
     //                C   H   W    M  K  KP  MT  TT  GS  RB  PB  MS  GWMMA  DIN3  GWIN  DWIN  NSPL
     using C1 = Conv<1, 29, 29, 20, 4, 1, 10, 16, 16, 1>;
