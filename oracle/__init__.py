@@ -27,6 +27,11 @@ def build(force: bool = False) -> str:
     return LIB_PATH
 
 
+class _Read(C.Structure):
+    _fields_ = [("group", C.c_int32), ("layer", C.c_int32), ("purpose", C.c_int32), ("n_incl", C.c_int32),
+                ("e0", C.c_int64), ("e1", C.c_int64), ("incl_off", C.c_int64)]
+
+
 class _Layer(C.Structure):
     _fields_ = [("kind", C.c_int32), ("units", C.c_int32), ("kernel", C.c_int32), ("act", C.c_int32)]
 
@@ -55,10 +60,13 @@ def lib():
         _lib.orc_trace_len.restype = C.c_int64
         _lib.orc_forward.argtypes = [ap, dp, fp, dp, dp, C.POINTER(C.c_uint8)]
         _lib.orc_sample_grad.argtypes = [ap, dp, fp, C.c_int32, dp, dp]
+        _lib.orc_sample_grad2.argtypes = [ap, dp, dp, fp, C.c_int32, dp, dp]
+        _lib.orc_replay.argtypes = [ap, dp, fp, ip, C.c_int32, C.POINTER(C.c_int64), ip, C.c_int32,
+                                    C.POINTER(_Read), ip, C.c_double, dp, dp, dp]
         _lib.orc_train_sgd.argtypes = [ap, dp, fp, ip, C.c_int64, C.c_double, dp]
         _lib.orc_train_sync.argtypes = [ap, dp, fp, ip, C.c_int64, C.c_double, C.c_int64, dp]
         _lib.orc_evaluate.argtypes = [ap, dp, fp, ip, C.c_int64, dp, C.POINTER(C.c_int64), dp, ip]
-        for f in ("orc_forward", "orc_sample_grad", "orc_train_sgd", "orc_train_sync", "orc_evaluate"):
+        for f in ("orc_forward", "orc_sample_grad", "orc_sample_grad2", "orc_replay", "orc_train_sgd", "orc_train_sync", "orc_evaluate"):
             getattr(_lib, f).restype = C.c_int32
     return _lib
 
@@ -138,6 +146,39 @@ class Oracle:
         loss = C.c_double()
         _check(lib().orc_sample_grad(C.byref(self.arch), _d(params), _f(x), int(label), _d(g), C.byref(loss)))
         return loss.value, g
+
+    def sample_grad2(self, p_fwd, p_bwd, x, label):
+        """(loss, grad) of one sample: forward at p_fwd, delta_in back-propagated at p_bwd."""
+        pf, pb = self._p(p_fwd), self._p(p_bwd)
+        x = self._x(x)
+        g = np.zeros(self.n_params)
+        loss = C.c_double()
+        _check(lib().orc_sample_grad2(C.byref(self.arch), _d(pf), _d(pb), _f(x), int(label), _d(g), C.byref(loss)))
+        return loss.value, g
+
+    def replay(self, params0, X, Y, groups, reads, lr, pubs_in=None):
+        """Hogwild schedule replay (orc_replay).  groups: [(first, count)]; reads: iterable of
+        (group, layer, purpose, e0, e1, [included group ids]).  Returns (params, pubs[n_groups][P])."""
+        p0 = self._p(params0)
+        X = self._x(X)
+        Y = np.ascontiguousarray(Y, np.int32)
+        ng = len(groups)
+        gf = np.ascontiguousarray([g[0] for g in groups], np.int64)
+        gc = np.ascontiguousarray([g[1] for g in groups], np.int32)
+        reads = list(reads)
+        rd = (_Read * max(len(reads), 1))()
+        incl = []
+        for k, (grp, layer, purpose, e0, e1, inc) in enumerate(reads):
+            rd[k] = _Read(grp, layer, purpose, len(inc), e0, e1, len(incl))
+            incl.extend(int(j) for j in inc)
+        inc = np.ascontiguousarray(incl if incl else [0], np.int32)
+        out = np.zeros(self.n_params)
+        pubs = np.zeros((max(ng, 1), self.n_params))
+        pin = None if pubs_in is None else np.ascontiguousarray(pubs_in, np.float64)
+        _check(lib().orc_replay(C.byref(self.arch), _d(p0), _f(X), _i(Y), ng,
+                                gf.ctypes.data_as(C.POINTER(C.c_int64)), _i(gc), len(reads), rd, _i(inc),
+                                float(lr), _d(out), _d(pubs), None if pin is None else _d(pin)))
+        return out, pubs[:ng]
 
     def train_sgd(self, params, X, Y, lr):
         p = self._p(params).copy()

@@ -365,6 +365,30 @@ static int grad_one(work* w, const double* P, const float* x, int label, double*
     return ORC_OK;
 }
 
+/* One sample's gradient with the forward pass at Pf and the back-propagated partial derivatives
+ * (delta_in = W^T delta) at Pb: the two weight reads a hogwild worker makes may see different
+ * versions of the shared weights ("on-demand" reads).  Pf == Pb is orc_sample_grad. */
+int32_t orc_sample_grad2(const orc_arch* a, const double* Pf, const double* Pb, const float* x, int32_t label,
+                         double* grad_accum, double* loss) {
+    if (!a || !Pf || !Pb || !x || !grad_accum) return ORC_E_INVALID;
+    work w;
+    int rc = work_init(&w, a);
+    if (!rc) {
+        if (label < 0 || label >= w.p.n_classes) {
+            rc = ORC_E_LABEL;
+        } else {
+            const int64_t n_in = (int64_t)a->in_c * a->in_h * a->in_w;
+            load_image(&w.p, w.A, x, n_in);
+            forward_plan(&w.p, Pf, w.A, w.AM);
+            const plan_layer* last = &w.p.L[w.p.n - 1];
+            if (loss) *loss = softmax_ce(w.A + last->out_off, w.p.n_classes, label, NULL);
+            backward_plan(&w, Pb, label, grad_accum);
+        }
+    }
+    work_free(&w);
+    return rc;
+}
+
 int32_t orc_sample_grad(const orc_arch* a, const double* params, const float* x, int32_t label,
                         double* grad_accum, double* loss) {
     if (!a || !params || !x || !grad_accum) return ORC_E_INVALID;
@@ -375,9 +399,34 @@ int32_t orc_sample_grad(const orc_arch* a, const double* params, const float* x,
     return rc;
 }
 
+/* Sequential SGD, its own loop (not orc_train_sync with B = 1): for each sample i in index order
+ * (no shuffling), the gradient at the current W, then W <- W - lr * g_i right away (P:132
+ * with a single worker: it takes the next image, forward, back-propagate, adjust the weights). */
 int32_t orc_train_sgd(const orc_arch* a, double* params, const float* X, const int32_t* Y, int64_t n, double lr,
                       double* sum_loss) {
-    return orc_train_sync(a, params, X, Y, n, lr, 1, sum_loss);
+    if (!a || !params || n < 0 || (n > 0 && (!X || !Y))) return ORC_E_INVALID;
+    work w;
+    int rc = work_init(&w, a);
+    if (rc) {
+        work_free(&w);
+        return rc;
+    }
+    const int64_t np = w.p.n_params;
+    const int64_t n_in = (int64_t)a->in_c * a->in_h * a->in_w;
+    double* g = (double*)calloc((size_t)np, sizeof(double));
+    double ls = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        double li = 0.0;
+        memset(g, 0, sizeof(double) * (size_t)np);
+        rc = grad_one(&w, params, X + i * n_in, Y[i], g, &li, n_in);
+        if (rc) break;
+        ls += li;
+        for (int64_t j = 0; j < np; ++j) params[j] -= lr * g[j]; /* adjust before the next image */
+    }
+    if (sum_loss) *sum_loss = ls;
+    free(g);
+    work_free(&w);
+    return rc;
 }
 
 int32_t orc_train_sync(const orc_arch* a, double* params, const float* X, const int32_t* Y, int64_t n, double lr,
@@ -447,5 +496,121 @@ int32_t orc_evaluate(const orc_arch* a, const double* params, const float* X, co
     if (mean_loss) *mean_loss = n > 0 ? total / (double)n : 0.0;
     if (n_errors) *n_errors = errs;
     work_free(&w);
+    return rc;
+}
+
+/* Hogwild schedule replay (PAPER.md:138 controlled hogwild, P:140
+ * arbitrary order of synchronization).  Group k (a worker's claim of images
+ * [g_first[k], g_first[k] + g_count[k])) reads the shared weights and publishes, per weighted
+ * layer, pub_k = -lr * sum over its images of that layer's gradient.  A read (orc_read) states
+ * which earlier groups' publishes of that layer the worker saw on the elements [e0, e1) of the
+ * layer's normative W-then-b block, for the forward pass (purpose 0) or for the delta_in
+ * back-propagation (purpose 1).  Elements no read covers are read at W0 (purpose 1 falls back to
+ * the purpose-0 read of the same element).  Groups are evaluated in an order where every group
+ * follows the groups it saw (ORC_E_INVALID if the sets are cyclic or self-referencing).
+ * Result: params_out = W0 + sum_k pub_k (sum in group index order); pubs_out (may be NULL):
+ * [n_groups][n_params] the publishes.  pubs_in (may be NULL): use these publishes for what the
+ * reads include instead of the replayed ones (checks one group at a time against recorded data). */
+int32_t orc_replay(const orc_arch* a, const double* params0, const float* X, const int32_t* Y, int32_t n_groups,
+                   const int64_t* g_first, const int32_t* g_count, int32_t n_reads, const orc_read* reads,
+                   const int32_t* incl, double lr, double* params_out, double* pubs_out, const double* pubs_in) {
+    if (!a || !params0 || n_groups < 0 || (n_groups > 0 && (!g_first || !g_count || !X || !Y)) ||
+        (n_reads > 0 && (!reads || !incl)) || !params_out)
+        return ORC_E_INVALID;
+    plan p;
+    int rc = make_plan(a, &p, NULL, 0);
+    if (rc) return rc;
+    const int64_t np = p.n_params;
+    const int64_t n_in = (int64_t)a->in_c * a->in_h * a->in_w;
+    /* weighted-layer blocks: [start, end) in the normative layout */
+    int64_t bstart[16], bend[16];
+    int nl = 0;
+    for (int l = 0; l < p.n; ++l)
+        if (p.L[l].kind != ORC_POOL) {
+            bstart[nl] = p.L[l].woff;
+            bend[nl] = p.L[l].boff + p.L[l].nb;
+            ++nl;
+        }
+    for (int r = 0; r < n_reads; ++r) {
+        const orc_read* q = &reads[r];
+        if (q->group < 0 || q->group >= n_groups || q->layer < 0 || q->layer >= nl || q->purpose < 0 ||
+            q->purpose > 1 || q->e0 < 0 || q->e1 < q->e0 || bstart[q->layer] + q->e1 > bend[q->layer] ||
+            q->n_incl < 0)
+            return ORC_E_INVALID;
+        for (int32_t t = 0; t < q->n_incl; ++t)
+            if (incl[q->incl_off + t] < 0 || incl[q->incl_off + t] >= n_groups || incl[q->incl_off + t] == q->group)
+                return ORC_E_INVALID;
+    }
+    double* pubs = (double*)calloc((size_t)(n_groups > 0 ? n_groups : 1) * (size_t)np, sizeof(double));
+    double* Wf = (double*)malloc(sizeof(double) * (size_t)np);
+    double* Wb = (double*)malloc(sizeof(double) * (size_t)np);
+    double* g = (double*)malloc(sizeof(double) * (size_t)np);
+    char* done = (char*)calloc((size_t)(n_groups > 0 ? n_groups : 1), 1);
+    char* covf = (char*)malloc((size_t)np);
+    char* covb = (char*)malloc((size_t)np);
+    if (!pubs || !Wf || !Wb || !g || !done || !covf || !covb) rc = ORC_E_INVALID;
+    int32_t n_done = 0;
+    while (!rc && n_done < n_groups) {
+        int progressed = 0;
+        for (int32_t k = 0; k < n_groups && !rc; ++k) {
+            if (done[k]) continue;
+            int ready = 1; /* every group this one saw is evaluated */
+            for (int r = 0; r < n_reads && ready; ++r)
+                if (reads[r].group == k)
+                    for (int32_t t = 0; t < reads[r].n_incl; ++t)
+                        if (!done[incl[reads[r].incl_off + t]]) ready = 0;
+            if (!ready) continue;
+            /* the weights this group read: W0 + the publishes it saw, element by element */
+            memcpy(Wf, params0, sizeof(double) * (size_t)np);
+            memcpy(Wb, params0, sizeof(double) * (size_t)np);
+            memset(covf, 0, (size_t)np);
+            memset(covb, 0, (size_t)np);
+            for (int r = 0; r < n_reads; ++r) {
+                const orc_read* q = &reads[r];
+                if (q->group != k) continue;
+                double* W = q->purpose == 0 ? Wf : Wb;
+                char* cov = q->purpose == 0 ? covf : covb;
+                for (int64_t e = bstart[q->layer] + q->e0; e < bstart[q->layer] + q->e1; ++e) {
+                    if (cov[e]) { /* two reads of one element for one purpose: ambiguous */
+                        rc = ORC_E_INVALID;
+                        break;
+                    }
+                    cov[e] = 1;
+                    double v = params0[e];
+                    for (int32_t t = 0; t < q->n_incl; ++t) {
+                        const int32_t j = incl[q->incl_off + t];
+                        v += (pubs_in ? pubs_in : pubs)[(int64_t)j * np + e];
+                    }
+                    W[e] = v;
+                }
+            }
+            for (int64_t e = 0; e < np; ++e)
+                if (!covb[e]) Wb[e] = Wf[e]; /* delta_in reads default to the forward read */
+            /* pub_k = -lr * sum over the group's images of the gradient (index order) */
+            memset(g, 0, sizeof(double) * (size_t)np);
+            for (int32_t i = 0; i < g_count[k] && !rc; ++i) {
+                const int64_t s = g_first[k] + i;
+                rc = orc_sample_grad2(a, Wf, Wb, X + s * n_in, Y[s], g, NULL);
+            }
+            for (int64_t e = 0; e < np; ++e) pubs[(int64_t)k * np + e] = -lr * g[e];
+            done[k] = 1;
+            ++n_done;
+            progressed = 1;
+        }
+        if (!progressed && !rc) rc = ORC_E_INVALID; /* a cycle: no group can go first */
+    }
+    if (!rc) {
+        memcpy(params_out, params0, sizeof(double) * (size_t)np);
+        for (int32_t k = 0; k < n_groups; ++k)
+            for (int64_t e = 0; e < np; ++e) params_out[e] += pubs[(int64_t)k * np + e];
+        if (pubs_out) memcpy(pubs_out, pubs, sizeof(double) * (size_t)n_groups * (size_t)np);
+    }
+    free(pubs);
+    free(Wf);
+    free(Wb);
+    free(g);
+    free(done);
+    free(covf);
+    free(covb);
     return rc;
 }

@@ -59,8 +59,14 @@ int32_t orc_forward(const orc_arch* a, const double* params, const float* x,
 int32_t orc_sample_grad(const orc_arch* a, const double* params, const float* x, int32_t label,
                         double* grad_accum, double* loss);
 
+/* orc_sample_grad with the forward pass at Pf and delta_in (W^T delta) at Pb (a
+ * hogwild worker's reads may see different versions of the shared weights). */
+int32_t orc_sample_grad2(const orc_arch* a, const double* Pf, const double* Pb, const float* x, int32_t label,
+                         double* grad_accum, double* loss);
+
 /* Sequential SGD over samples 0..n-1 in index order (P:132 with one worker;
- * P:324 no shuffling): W <- W - lr * g_i after every sample.  sum_loss may be NULL. */
+ * P:324 no shuffling): W <- W - lr * g_i after every sample -- its own per-sample loop,
+ * independent of orc_train_sync.  sum_loss may be NULL. */
 int32_t orc_train_sgd(const orc_arch* a, double* params, const float* X, const int32_t* Y,
                       int64_t n, double lr, double* sum_loss);
 
@@ -75,6 +81,24 @@ int32_t orc_train_sync(const orc_arch* a, double* params, const float* X, const 
  * losses / preds (may be NULL) receive per-sample values. */
 int32_t orc_evaluate(const orc_arch* a, const double* params, const float* X, const int32_t* Y,
                      int64_t n, double* mean_loss, int64_t* n_errors, double* losses, int32_t* preds);
+
+/* One read of the shared weights by a hogwild group (see orc_replay). */
+typedef struct {
+    int32_t group;   /* reading group */
+    int32_t layer;   /* weighted layer index (0-based, pools not counted) */
+    int32_t purpose; /* 0: forward pass; 1: delta_in back-propagation */
+    int32_t n_incl;  /* number of groups whose publish of this layer the read saw */
+    int64_t e0, e1;  /* element range within the layer's normative W-then-b block */
+    int64_t incl_off; /* their group ids: incl[incl_off .. incl_off + n_incl) */
+} orc_read;
+
+/* Hogwild schedule replay (C-1 step 9): group k = images [g_first[k], +g_count[k]),
+ * each reading the weights as W0 + the publishes its reads name, publishing -lr * sum of its
+ * images' gradients per layer.  params_out = W0 + sum of all publishes; pubs_out (may be NULL)
+ * [n_groups][n_params]; pubs_in (may be NULL) replaces the replayed publishes the reads include. */
+int32_t orc_replay(const orc_arch* a, const double* params0, const float* X, const int32_t* Y, int32_t n_groups,
+                   const int64_t* g_first, const int32_t* g_count, int32_t n_reads, const orc_read* reads,
+                   const int32_t* incl, double lr, double* params_out, double* pubs_out, const double* pubs_in);
 
 #ifdef __cplusplus
 }

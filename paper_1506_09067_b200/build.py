@@ -26,6 +26,20 @@ def build(force=False, verbose=False, timing=False):
     return out
 
 
+def build_variant(name, defs=(), timing=False, only_net=None):
+    """A/B experiments: libchaos_<name>.so with extra -D definitions (optionally one net only,
+    CHAOS_ONLY_NET: ~4x faster to compile).  Load it with CHAOS_LIB=<path>."""
+    out = os.path.join(HERE, f"libchaos_{name}.so")
+    cmd = ["nvcc", *NVCC_FLAGS, "-I" + os.path.join(ROOT, "include"), "-o", out, *SRC]
+    extra = [f"-D{d}" for d in defs]
+    if timing:
+        extra.append("-DCHAOS_TIMING")
+    if only_net:
+        extra += ["-DCHAOS_ONLY_NET", f"-DCHAOS_ONLY_NET_{only_net}=1"]
+    subprocess.check_call(cmd[:1] + extra + cmd[1:])
+    return out
+
+
 if __name__ == "__main__":
     import sys
     build(force="--force" in sys.argv, verbose="-v" in sys.argv, timing="--timing" in sys.argv)

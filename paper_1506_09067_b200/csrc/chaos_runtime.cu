@@ -227,23 +227,33 @@ NetDesc make_desc(const char* name, std::vector<LayerSig> sig) {
 const std::vector<NetDesc>& registry() {
     static const std::vector<NetDesc> r = [] {
         std::vector<NetDesc> v;
+#if !defined(CHAOS_ONLY_NET) || CHAOS_ONLY_NET_TinyNet
         v.push_back(make_desc<TinyNet>("tiny", {{CHAOS_CONV, 5, 4, CHAOS_TANH}, {CHAOS_MAXPOOL, 0, 2, 0},
                                                 {CHAOS_FULL, 10, 0, CHAOS_IDENTITY}}));
+#endif
+#if !defined(CHAOS_ONLY_NET) || CHAOS_ONLY_NET_MediumNet
         v.push_back(make_desc<MediumNet>(
             "medium", {{CHAOS_CONV, 20, 4, CHAOS_TANH}, {CHAOS_MAXPOOL, 0, 2, 0}, {CHAOS_CONV, 40, 5, CHAOS_TANH},
                        {CHAOS_MAXPOOL, 0, 3, 0}, {CHAOS_FULL, 150, 0, CHAOS_TANH}, {CHAOS_FULL, 10, 0, CHAOS_IDENTITY}}));
+#endif
+#if !defined(CHAOS_ONLY_NET) || CHAOS_ONLY_NET_PaperSmallNet
         v.push_back(make_desc<PaperSmallNet>(
             "paper_small", {{CHAOS_CONV, 5, 4, CHAOS_TANH}, {CHAOS_MAXPOOL, 0, 2, 0}, {CHAOS_CONV, 10, 5, CHAOS_TANH},
                             {CHAOS_MAXPOOL, 0, 3, 0}, {CHAOS_FULL, 50, 0, CHAOS_TANH},
                             {CHAOS_FULL, 10, 0, CHAOS_IDENTITY}}));
+#endif
+#if !defined(CHAOS_ONLY_NET) || CHAOS_ONLY_NET_LargeNet
         v.push_back(make_desc<LargeNet>(
             "large", {{CHAOS_CONV, 20, 4, CHAOS_TANH}, {CHAOS_MAXPOOL, 0, 2, 0}, {CHAOS_CONV, 60, 3, CHAOS_TANH},
                       {CHAOS_MAXPOOL, 0, 2, 0}, {CHAOS_CONV, 100, 2, CHAOS_TANH}, {CHAOS_MAXPOOL, 0, 2, 0},
                       {CHAOS_FULL, 150, 0, CHAOS_TANH}, {CHAOS_FULL, 10, 0, CHAOS_IDENTITY}}));
+#endif
+#if !defined(CHAOS_ONLY_NET) || CHAOS_ONLY_NET_PaperLargeNet
         v.push_back(make_desc<PaperLargeNet>(
             "paper_large", {{CHAOS_CONV, 20, 4, CHAOS_TANH}, {CHAOS_MAXPOOL, 0, 1, 0}, {CHAOS_CONV, 60, 5, CHAOS_TANH},
                             {CHAOS_MAXPOOL, 0, 2, 0}, {CHAOS_CONV, 100, 6, CHAOS_TANH}, {CHAOS_MAXPOOL, 0, 2, 0},
                             {CHAOS_FULL, 150, 0, CHAOS_TANH}, {CHAOS_FULL, 10, 0, CHAOS_IDENTITY}}));
+#endif
         return v;
     }();
     return r;

@@ -1,4 +1,6 @@
 """Shared test helpers: the parity tolerance of DESIGN.md (reading R9 / SURVEY C-15)."""
+import itertools
+
 import numpy as np
 
 
@@ -83,3 +85,32 @@ def tie_free_prefix(oracle, arch, params, X, Y, lr, gap=5e-6):
             return i
         p, _ = oracle.train_sgd(p, X[i:i + 1], Y[i:i + 1], lr)
     return len(Y)
+
+
+def interval_orders(n):
+    """All strict interval orders on n samples, as the set of predecessors of each sample.
+
+    Enumerated as the distinct read-before-publish patterns of n workers: each sample i
+    reads at time r_i and publishes at time w_i > r_i; j precedes i iff w_j < r_i."""
+    pats = set()
+    for perm in itertools.permutations(range(2 * n)):
+        r = perm[:n]
+        w = perm[n:]
+        if any(w[i] < r[i] for i in range(n)):
+            continue
+        pats.add(tuple(frozenset(j for j in range(n) if w[j] < r[i]) for i in range(n)))
+    return sorted(pats, key=str)
+
+
+def compose_replay(o, p, X, Y, lr, preds):
+    """Whole-sample hogwild outcome by composition (no orc_replay): sample i's gradient at
+    W0 - lr * sum_{j in preds[i]} g_j, the final W = W0 - lr * sum of all gradients."""
+    n = len(Y)
+    order = sorted(range(n), key=lambda i: len(preds[i]))
+    g = {}
+    for i in order:
+        w = np.asarray(p, np.float64).copy()
+        for j in sorted(preds[i]):
+            w -= lr * g[j]
+        g[i] = o.sample_grad(w, X[i], Y[i])[1]
+    return np.asarray(p, np.float64) - lr * sum(g[i] for i in range(n))

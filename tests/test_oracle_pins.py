@@ -121,12 +121,24 @@ def test_identity_conv_passes_input():
 # --------------------------------------------------------------------------------------
 # torch float64 autograd (library routine) on the BASELINE.json nets
 # --------------------------------------------------------------------------------------
-def torch_grad(arch, params, X, Y):
-    """Sum-reduction CE gradient with torch's own conv2d/max_pool2d/linear/cross_entropy."""
+def torch_grad(arch, params, X, Y, params_bwd=None):
+    """Sum-reduction CE gradient with torch's own conv2d/max_pool2d/linear/cross_entropy.
+
+    params_bwd (optional): the weights the back-propagated partial derivatives use (delta_in =
+    W_bwd^T delta), while the forward pass and the weight gradients use params -- built as
+    layer(x.detach(), W) + layer(x, W_bwd) - layer(x, W_bwd).detach(): the value is layer(x, W),
+    d/dW flows through the first term only, d/dx through the second only."""
     import torch
     import torch.nn.functional as F
     P = torch.tensor(params, dtype=torch.float64, requires_grad=True)
+    Pb = None if params_bwd is None else torch.tensor(params_bwd, dtype=torch.float64)
     x = torch.tensor(np.asarray(X, np.float64)).reshape(len(Y), 1, 29, 29)
+
+    def split(fn, h, W, b, Wb_, bb_):
+        if Pb is None:
+            return fn(h, W, b)
+        return fn(h.detach(), W, b) + fn(h, Wb_, bb_) - fn(h, Wb_, bb_).detach()
+
     off = 0
     h = x
     c = 1
@@ -135,8 +147,10 @@ def torch_grad(arch, params, X, Y):
             nw = units * c * k * k
             W = P[off:off + nw].reshape(units, c, k, k)
             b = P[off + nw:off + nw + units]
+            Wb_ = None if Pb is None else Pb[off:off + nw].reshape(units, c, k, k)
+            bb_ = None if Pb is None else Pb[off + nw:off + nw + units]
             off += nw + units
-            h = F.conv2d(h, W, b)
+            h = split(F.conv2d, h, W, b, Wb_, bb_)
             h = torch.tanh(h) if act == T_ else h
             c = units
         elif kind == P_:
@@ -146,8 +160,10 @@ def torch_grad(arch, params, X, Y):
             nin = h.shape[1]
             W = P[off:off + units * nin].reshape(units, nin)
             b = P[off + units * nin:off + units * nin + units]
+            Wb_ = None if Pb is None else Pb[off:off + units * nin].reshape(units, nin)
+            bb_ = None if Pb is None else Pb[off + units * nin:off + units * nin + units]
             off += units * nin + units
-            h = F.linear(h, W, b)
+            h = split(F.linear, h, W, b, Wb_, bb_)
             h = torch.tanh(h) if act == T_ else h
     loss = F.cross_entropy(h, torch.tensor(np.asarray(Y, np.int64)), reduction="sum")
     loss.backward()
@@ -314,6 +330,7 @@ def test_pool_gradient_routes_to_argmax_only():
 
 
 def test_sync_batch1_equals_sequential_bitwise():
+    # orc_train_sgd is its own per-sample loop (not orc_train_sync with B = 1): two code paths
     o = Oracle(sd.ARCHS["tiny"])
     d = sd.prototype_dataset(7, 20, 0)
     p = sd.init_params(7, o.blocks())
@@ -321,6 +338,185 @@ def test_sync_batch1_equals_sequential_bitwise():
     b, lb = o.train_sync(p, d.x_train, d.y_train, 0.01, 1)
     np.testing.assert_array_equal(a, b)
     assert la == lb
+
+
+# --------------------------------------------------------------------------------------
+# Multi-step trajectories against torch float64 autograd (library routine): W is updated
+# between samples (sequential SGD, P:132 one worker) and between blocks (sync mode)
+# --------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["tiny", "large", "paper_small"])
+def test_sequential_sgd_trajectory_against_torch_f64(name):
+    arch = sd.ARCHS[name]
+    o = Oracle(arch)
+    d = sd.prototype_dataset(31, 4, 0)
+    p0 = sd.init_params(31, o.blocks()).astype(np.float64)
+    lr = 0.1
+    w = p0.copy()
+    tl = 0.0
+    for i in range(4):  # torch: gradient at the current W, update, next sample
+        li, gi, _ = torch_grad(arch, w, d.x_train[i:i + 1], d.y_train[i:i + 1])
+        w = w - lr * gi
+        tl += li
+    got, gl = o.train_sgd(p0, d.x_train, d.y_train, lr)
+    np.testing.assert_allclose(got - p0, w - p0, rtol=1e-9, atol=1e-12 * np.abs(w - p0).max())
+    assert gl == pytest.approx(tl, rel=1e-12)
+    # teeth: a trainer that left W stale across the 4 samples (= one summed step) is far off
+    stale, _ = o.train_sync(p0, d.x_train, d.y_train, lr, 4)
+    assert np.abs((stale - p0) - (w - p0)).max() > 1e-3 * np.abs(w - p0).max()
+
+
+@pytest.mark.parametrize("name", ["tiny", "medium"])
+def test_sync_blocks_trajectory_against_torch_f64(name):
+    arch = sd.ARCHS[name]
+    o = Oracle(arch)
+    d = sd.prototype_dataset(32, 7, 0)
+    p0 = sd.init_params(32, o.blocks()).astype(np.float64)
+    lr, B = 0.05, 3  # blocks [0,3) [3,6) [6,7): the last partial block is one update
+    w = p0.copy()
+    for s0 in range(0, 7, B):
+        _, gs, _ = torch_grad(arch, w, d.x_train[s0:s0 + B], d.y_train[s0:s0 + B])  # sum at block-start W
+        w = w - lr * gs
+    got, _ = o.train_sync(p0, d.x_train, d.y_train, lr, B)
+    np.testing.assert_allclose(got - p0, w - p0, rtol=1e-9, atol=1e-12 * np.abs(w - p0).max())
+    # teeth: per-sample updates inside a block (W not held at the block start) differ
+    seq, _ = o.train_sgd(p0, d.x_train, d.y_train, lr)
+    assert np.abs((seq - p0) - (w - p0)).max() > 1e-3 * np.abs(w - p0).max()
+
+
+# --------------------------------------------------------------------------------------
+# Hogwild schedule replay (orc_replay, SURVEY C-1 step 9)
+# --------------------------------------------------------------------------------------
+def _whole_layer_reads(o, k, preds):
+    out = []
+    for l, (_, nw, nb) in enumerate(o.blocks()):
+        out.append((k, l, 0, 0, nw + nb, sorted(preds)))
+    return out
+
+
+def test_sample_grad2_against_torch_f64():
+    # forward at Pf, delta_in at Pb (a worker whose backward re-read saw newer weights)
+    arch = sd.ARCHS["large"]
+    o = Oracle(arch)
+    d = sd.prototype_dataset(33, 2, 0)
+    pf = sd.init_params(33, o.blocks()).astype(np.float64)
+    pb = pf + 0.05 * np.random.default_rng(0).standard_normal(o.n_params)
+    tl, tg, _ = torch_grad(arch, pf, d.x_train, d.y_train, params_bwd=pb)
+    g = np.zeros(o.n_params)
+    lsum = 0.0
+    for i in range(2):
+        li, gi = o.sample_grad2(pf, pb, d.x_train[i], d.y_train[i])
+        g += gi
+        lsum += li
+    assert lsum == pytest.approx(tl, rel=1e-12)
+    np.testing.assert_allclose(g, tg, rtol=1e-10, atol=1e-12 * np.abs(tg).max())
+    # the last layer's gradients do not depend on Pb; an earlier layer's do
+    _, g_same = o.sample_grad(pf, d.x_train[0], d.y_train[0])
+    _, g_mix = o.sample_grad2(pf, pb, d.x_train[0], d.y_train[0])
+    np.testing.assert_array_equal(g_mix[-1510:], g_same[-1510:])
+    assert np.abs(g_mix[:340] - g_same[:340]).max() > 1e-6
+
+
+def test_replay_total_order_is_sequential_sgd():
+    o = Oracle(sd.ARCHS["tiny"])
+    d = sd.prototype_dataset(34, 5, 0)
+    p = sd.init_params(34, o.blocks()).astype(np.float64)
+    reads = [r for k in range(5) for r in _whole_layer_reads(o, k, range(k))]
+    got, _ = o.replay(p, d.x_train, d.y_train, [(k, 1) for k in range(5)], reads, 0.05)
+    ref, _ = o.train_sgd(p, d.x_train, d.y_train, 0.05)
+    np.testing.assert_allclose(got, ref, rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("G", [1, 2])
+def test_replay_all_concurrent_is_sync(G):
+    # every group reads W0 (saw no publish): one summed step, = sync mode with B = n
+    o = Oracle(sd.ARCHS["tiny"])
+    d = sd.prototype_dataset(35, 6, 0)
+    p = sd.init_params(35, o.blocks()).astype(np.float64)
+    got, pubs = o.replay(p, d.x_train, d.y_train, [(s, G) for s in range(0, 6, G)], [], 0.05)
+    ref, _ = o.train_sync(p, d.x_train, d.y_train, 0.05, 6)
+    np.testing.assert_allclose(got, ref, rtol=0, atol=1e-15)
+    np.testing.assert_allclose(pubs.sum(0), ref - p, rtol=0, atol=1e-15)
+
+
+def test_replay_interval_orders_match_composition():
+    # whole-sample staleness patterns (the 19 interval orders on 3 samples): the replay equals
+    # composing per-sample gradients at W0 - lr * sum of the predecessors' gradients
+    from helpers import interval_orders, compose_replay
+    o = Oracle(sd.ARCHS["tiny"])
+    d = sd.prototype_dataset(36, 3, 0)
+    p = sd.init_params(36, o.blocks()).astype(np.float64)
+    orders = interval_orders(3)
+    assert len(orders) == 19 and len(interval_orders(2)) == 3
+    outs = []
+    for preds in orders:
+        reads = [r for k in range(3) for r in _whole_layer_reads(o, k, preds[k])]
+        got, _ = o.replay(p, d.x_train, d.y_train, [(k, 1) for k in range(3)], reads, 0.5)
+        np.testing.assert_allclose(got, compose_replay(o, p, d.x_train, d.y_train, 0.5, preds), rtol=0, atol=1e-14)
+        outs.append(got)
+    # distinct orders give distinct results at this lr (the replay is sensitive to the schedule)
+    assert len({np.round(x, 9).tobytes() for x in outs}) >= 10
+
+
+def test_replay_mixed_layer_read_against_torch_f64():
+    # group 1 saw group 0's output-layer publish only (per-layer publishing, R5), forward and
+    # delta_in; and group 2 saw group 0's publish of every layer for its forward pass but
+    # delta_in at W0 for the output layer
+    arch = sd.ARCHS["large"]
+    o = Oracle(arch)
+    d = sd.prototype_dataset(37, 3, 0)
+    p = sd.init_params(37, o.blocks()).astype(np.float64)
+    lr = 0.3
+    bl = o.blocks()
+    nl = len(bl)
+    sizes = [nw + nb for _, nw, nb in bl]
+    starts = np.cumsum([0] + sizes)
+    reads = [(1, nl - 1, 0, 0, sizes[-1], [0])]
+    reads += [(2, l, 0, 0, sizes[l], [0]) for l in range(nl)]
+    reads += [(2, nl - 1, 1, 0, sizes[-1], [])]
+    got, pubs = o.replay(p, d.x_train, d.y_train, [(0, 1), (1, 1), (2, 1)], reads, lr)
+    _, g0, _ = torch_grad(arch, p, d.x_train[:1], d.y_train[:1])
+    pub0 = -lr * g0
+    w1 = p.copy()
+    w1[starts[-2]:] += pub0[starts[-2]:]
+    _, g1, _ = torch_grad(arch, w1, d.x_train[1:2], d.y_train[1:2])
+    w2f = p + pub0
+    w2b = w2f.copy()
+    w2b[starts[-2]:] = p[starts[-2]:]
+    _, g2, _ = torch_grad(arch, w2f, d.x_train[2:3], d.y_train[2:3], params_bwd=w2b)
+    ref = p - lr * (g0 + g1 + g2)
+    np.testing.assert_allclose(got - p, ref - p, rtol=1e-9, atol=1e-12 * np.abs(ref - p).max())
+    np.testing.assert_allclose(pubs[1], -lr * g1, rtol=1e-9, atol=1e-12 * np.abs(g1).max() * lr)
+
+
+def test_replay_partial_range_read():
+    # an FC read split in two row ranges that saw different publishes (chunked staging)
+    arch = sd.ARCHS["tiny"]
+    o = Oracle(arch)
+    d = sd.prototype_dataset(38, 2, 0)
+    p = sd.init_params(38, o.blocks()).astype(np.float64)
+    lr = 0.4
+    (_, nw0, nb0), (_, nw1, nb1) = o.blocks()
+    half = 5 * 845  # rows 0-4 of the FC W
+    reads = [(1, 1, 0, 0, half, [0]), (1, 1, 0, half, nw1 + nb1, [])]
+    got, _ = o.replay(p, d.x_train, d.y_train, [(0, 1), (1, 1)], reads, lr)
+    _, g0 = o.sample_grad(p, d.x_train[0], d.y_train[0])
+    w1 = p.copy()
+    s = nw0 + nb0
+    w1[s:s + half] -= lr * g0[s:s + half]
+    _, g1, _ = torch_grad(arch, w1, d.x_train[1:2], d.y_train[1:2])
+    np.testing.assert_allclose(got, p - lr * g0 - lr * g1, rtol=1e-10, atol=1e-14)
+
+
+def test_replay_rejects_cycles_and_bad_reads():
+    o = Oracle(sd.ARCHS["tiny"])
+    d = sd.prototype_dataset(39, 2, 0)
+    p = sd.init_params(39, o.blocks())
+    with pytest.raises(OracleError):  # 0 saw 1 and 1 saw 0
+        o.replay(p, d.x_train, d.y_train, [(0, 1), (1, 1)], [(0, 0, 0, 0, 5, [1]), (1, 0, 0, 0, 5, [0])], 0.1)
+    with pytest.raises(OracleError):  # a group cannot see its own publish
+        o.replay(p, d.x_train, d.y_train, [(0, 1), (1, 1)], [(0, 0, 0, 0, 5, [0])], 0.1)
+    with pytest.raises(OracleError):  # range beyond the layer
+        o.replay(p, d.x_train, d.y_train, [(0, 1), (1, 1)], [(1, 0, 0, 0, 10 ** 6, [0])], 0.1)
 
 
 def test_sync_permutation_within_batch():
@@ -331,16 +527,6 @@ def test_sync_permutation_within_batch():
     perm = np.random.default_rng(0).permutation(8)
     b, _ = o.train_sync(p, d.x_train[perm], d.y_train[perm], 0.01, 8)
     np.testing.assert_allclose(a, b, rtol=1e-12, atol=1e-15)
-
-
-def test_sync_full_batch_is_all_concurrent_replay():
-    # brute force, 3 samples: B = n equals every sample read at W0, one summed update
-    o = Oracle(sd.ARCHS["tiny"])
-    d = sd.prototype_dataset(9, 3, 0)
-    p = sd.init_params(9, o.blocks()).astype(np.float64)
-    gs = [o.sample_grad(p, d.x_train[i], d.y_train[i])[1] for i in range(3)]
-    a, _ = o.train_sync(p, d.x_train, d.y_train, 0.02, 3)
-    np.testing.assert_allclose(a, p - 0.02 * ((gs[0] + gs[1]) + gs[2]), rtol=0, atol=1e-15)
 
 
 def test_evaluate_brute_force():
