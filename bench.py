@@ -100,7 +100,14 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def make_data(world, rank):
+def make_data(world, rank, scaling="weak"):
+    if scaling == "strong":
+        # configs[3] (the D-5 headline): the 60,000 configs[3] images split into P contiguous shards
+        w = sd.WORKLOADS["config3"]
+        d = sd.make_dataset(w, PER_GPU, 10000)
+        lo, hi = rank * PER_GPU // world, (rank + 1) * PER_GPU // world
+        lo, hi = lo // 4 * 4, (hi // 4 * 4 if rank < world - 1 else PER_GPU)  # 16-B aligned image groups
+        return w, d.x_train[lo:hi], d.y_train[lo:hi], d.x_test, d.y_test
     if world == 1:
         w = sd.WORKLOADS["config3"]
         d = sd.make_dataset(w, PER_GPU, 10000)
@@ -109,6 +116,20 @@ def make_data(world, rank):
     xs, ys = sd.prototype_samples(w.seed, rank * PER_GPU, PER_GPU)
     xt, yt = sd.prototype_samples(w.seed, w.n_train, 10000)
     return w, xs, ys, xt, yt
+
+
+def host_identity():
+    """lscpu model name and the host's logical CPU count (SURVEY D-8)."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.split(":")[0].strip() == "Model name":
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
 
 
 def cpu_baseline(arch, seconds=12.0):
@@ -127,7 +148,8 @@ def cpu_baseline(arch, seconds=12.0):
     o.train_sgd(p, xs[:n], ys[:n], w.lr0)
     dt = time.perf_counter() - t
     return {"value": n / dt, "unit": "samples/s", "cores": 1, "kind": "oracle",
-            "sample": f"sequential SGD (oracle, float64, 1 thread) over the first {n} images of configs[3]"}
+            "sample": f"sequential SGD (oracle, float64, 1 thread) over the first {n} images of configs[3]",
+            **host_identity()}
 
 
 def run_reference(args):
@@ -153,7 +175,8 @@ def run_reference(args):
             "config": {"workload": "configs[3] large net, sequential SGD (the oracle) on a bounded sample",
                        "images_per_step": per_step, "arch": "large"},
             "cpu_baseline": {"value": v, "unit": "samples/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{per_step} images of configs[3] per step, oracle float64, 1 thread"},
+                             "sample": f"{per_step} images of configs[3] per step, oracle float64, 1 thread",
+                             **host_identity()},
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -181,6 +204,9 @@ def main():
                          "NCCL average; 'async' = one launch per shard with in-flight averages every K images on "
                          "a second stream (SURVEY NEXT-2)")
     ap.add_argument("--reserve-sms", type=int, default=4, help="--avg async: SMs left to the comm kernels")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: 60,000 images per GPU per step (configs[4] shards for N > 1); strong: the "
+                         "60,000 configs[3] images split over the N GPUs (SURVEY D-5 headline)")
     ap.add_argument("--comm", default="torch", choices=["torch", "chaos"],
                     help="hogwild averaging collectives: torch.distributed or the library's own NCCL "
                          "communicator (chaos_dist_*)")
@@ -221,7 +247,8 @@ def main():
         xt, yt = sd.prototype_samples(wl.seed, wl.n_train, 10000)
         w = wl
     else:
-        w, xs, ys, xt, yt = make_data(world if not args.force_dist else max(world, 2), rank)
+        w, xs, ys, xt, yt = make_data(world if not args.force_dist or args.scaling == "strong" else max(world, 2),
+                                      rank, args.scaling)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     net = Net(sd.ARCHS[args.arch], init_seed=w.seed, stream=stream)
@@ -277,7 +304,14 @@ def main():
     if distributed:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     elapsed = float(tmax.item())
-    total = PER_GPU * world * args.steps
+    per_gpu_images = int(ys.shape[0])
+    if distributed:  # every rank's shard length (strong scaling: shards differ by a few images)
+        nt = torch.tensor([per_gpu_images], dtype=torch.int64, device="cuda")
+        dist.all_reduce(nt)
+        images_per_step = int(nt.item())
+    else:
+        images_per_step = per_gpu_images
+    total = images_per_step * args.steps
     value = total / elapsed
     train_loss = net.last_train_loss() if args.mode == "hogwild" else None
 
@@ -325,7 +359,7 @@ def main():
         dt = torch.tensor([time.perf_counter() - t], dtype=torch.float64, device="cuda")
         if distributed:
             dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-        e2e = {"value": PER_GPU * world * args.steps / float(dt.item()), "unit": "samples/s",
+        e2e = {"value": images_per_step * args.steps / float(dt.item()), "unit": "samples/s",
                "h2d_bytes_per_step": int(Xh.numel() * 4 + Yh.numel() * 4),
                "d2h_bytes_per_step": 8 if host_entry else 4,
                "path": "chaos_train_epoch_host (C ABI, host buffers)" if host_entry
@@ -333,34 +367,57 @@ def main():
                     "by the copy stream's landed-images counter, in-flight averages beside it" if use_async
                else "pinned H2D copy + step on the training stream"}
 
+    # per-interval all-reduce time (SURVEY D-6): the K-interval average of the parameters alone,
+    # device-timed on the training stream (what one interval's blocking collective costs)
+    allreduce_ms = None
+    if distributed:
+        params = net.device_params()
+        buf = params.clone()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        for _ in range(3):
+            trainer._average(buf)
+        a0.record(stream)
+        for _ in range(20):
+            trainer._average(buf)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        allreduce_ms = a0.elapsed_time(a1) / 20
+
     if rank != 0:
         if distributed:
             dist.destroy_process_group()
         return
     # roofline of the dominant kernel: the persistent worker (one launch per step at N=1)
     kern_s = statistics.median(per_step_ms) / 1e3 if not distributed else elapsed / args.steps
-    achieved = ALGO_FLOP[args.arch] * PER_GPU / kern_s / 1e12
-    traffic = None
+    achieved = ALGO_FLOP[args.arch] * per_gpu_images / kern_s / 1e12
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "latest_traffic.json")
     if os.path.exists(tp):
         try:
             t = json.load(open(tp)).get(args.arch)
             traffic = t["dram_bytes_per_launch"] if t else None
+            traffic_src = (f"not measured in this run: dram__bytes_read+write per launch from the committed "
+                           f"ncu --set full capture {t.get('source', 'profiles/')}") if t else None
         except Exception:
             traffic = None
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": (f"configs[3] {args.arch} net, hogwild (CHAOS), 60,000 images per GPU per step"
-                                + ("" if not distributed else f"; configs[4] generator, NCCL average every {args.k}"
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": ((f"configs[3] {args.arch} net, hogwild (CHAOS), 60,000 images per GPU per step"
+                                 if args.scaling == "weak" else
+                                 f"configs[3] {args.arch} net, hogwild (CHAOS), 60,000 images split over "
+                                 f"{world} GPUs per step (strong scaling)")
+                                + ("" if not distributed else f"; {'configs[4] generator, ' if args.scaling == 'weak' else ''}NCCL average every {args.k}"
                                    + (f" images in flight (async, {args.reserve_sms} SMs reserved)" if use_async
                                       else " images (blocking)")))
                    if args.mode == "hogwild" else
                    (f"configs[3] {args.arch} net, deterministic sync SGD, global batch {args.sync_batch}, "
                     f"60,000 images per GPU per step" + ("" if not distributed else
                                                          "; one NCCL gradient all-reduce per batch")),
-                   "arch": args.arch, "mode": args.mode, "images_per_gpu_per_step": PER_GPU,
+                   "arch": args.arch, "mode": args.mode, "images_per_gpu_per_step": per_gpu_images,
+                   "images_per_step": images_per_step,
                    "sync_batch": args.sync_batch if args.mode == "sync" else None,
                    "group_G": info["group"], "publish_group": info["group"], "ctas": info["grid"], "threads_per_cta": info["block"],
                    "smem_bytes_per_cta": info["smem_bytes"], "sync_interval_K": args.k if distributed else None,
@@ -369,7 +426,7 @@ def main():
                    "comm": (args.comm if distributed and args.mode == "hogwild" else None),
                    "l2": "inputs (202 MB/GPU) larger than the 126 MB L2", "parallelism": f"dp{world}"},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic,
+                     "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic, "traffic_source": traffic_src,
                      "kernel": f"chaos_worker<{KERNEL_NET[args.arch]},{info['group']},{info['block']},"
                                f"{'kHogwild' if args.mode == 'hogwild' else 'kSync'}>",
                      "flop_per_image": ALGO_FLOP[args.arch],
@@ -384,6 +441,9 @@ def main():
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.arch)
+    if distributed:
+        line["allreduce_ms_per_interval"] = allreduce_ms
+        line["eval"]["model"] = "the averaged replicas (identical on every rank after the epoch's final average)"
     if args.force_dist:
         line["config"]["force_dist"] = True
         line["collectives"] = trainer.n_collectives

@@ -80,11 +80,20 @@ typedef enum { CHAOS_HOGWILD = 0, CHAOS_SYNC = 1 } chaos_mode;
 typedef enum {
     CHAOS_OPT_STREAM = 0,        /* value = (int64_t)cudaStream_t */
     CHAOS_OPT_SYNC_BATCH = 1,    /* B >= 1, default 64 */
-    CHAOS_OPT_GROUP = 2,         /* G, images per CTA per claim: compiled values 1 and the net's default */
+    CHAOS_OPT_GROUP = 2,         /* G, images per CTA per claim: compiled values 1 and the net's default.
+                                    A worker publishes each layer's G-image gradient sum once (G_pub = G,
+                                    the paper's delayed updates); SURVEY's separate
+                                    CHAOS_OPT_PUBLISH_GROUP is not exposed: publishing per image inside a
+                                    G-image group would need G gradient buffers per layer in shared memory
+                                    (the 227 KB budget holds one); G = 1 gives G_pub = 1 */
     CHAOS_OPT_MAX_CTAS = 3,      /* cap on resident CTAs (1 => a single worker = sequential SGD when G=1) */
     CHAOS_OPT_DEBUG_CLAIMS = 4,  /* 1 => count claims per image into a device buffer (exactly-once test) */
-    CHAOS_OPT_RESERVE_SMS = 5    /* hogwild: leave this many SMs free of training CTAs (room for concurrent
-                                    averaging / NCCL kernels, chaos_progress_wait), in [0, #SMs), default 0 */
+    CHAOS_OPT_RESERVE_SMS = 5,   /* hogwild: leave this many SMs free of training CTAs (room for concurrent
+                                    averaging / NCCL kernels, chaos_progress_wait), in [0, #SMs), default 0;
+                                    set it before chaos_dist_init, which caps the communicator's CTAs at it */
+    CHAOS_OPT_DEBUG_TRACE = 6,   /* 1 => hogwild epochs record their schedule (chaos_debug_trace); tiny and
+                                    large nets; CHAOS_E_UNSUPPORTED elsewhere */
+    CHAOS_OPT_DEBUG_STAGGER = 7  /* trace epochs: CTA b starts b * value cycles late (varied interleavings) */
 } chaos_option;
 
 typedef struct chaos_net chaos_net;
@@ -188,6 +197,24 @@ chaos_status chaos_dist_unique_id(void* host_id);
 chaos_status chaos_dist_init(chaos_net* net, const void* host_id, int32_t rank, int32_t world);
 chaos_status chaos_dist_average(chaos_net* net);
 chaos_status chaos_dist_average_buffer(chaos_net* net, float* d_buf, int64_t n, int64_t stream);
+
+/* Debug (controlled hogwild / arbitrary order of synchronization; checked by
+ * replaying the recorded schedule in the oracle): after a hogwild epoch
+ * run with CHAOS_OPT_DEBUG_TRACE=1 over n images with group size G (n_groups = ceil(n / G)), copies
+ * host_records[n_groups][32] (int64, group k = images [k*G, min(k*G+G, n))): for weighted layer
+ * l < 5, [6l+0] the rank of its publish on the "started" event counter, [6l+1] the rank on the
+ * "done" counter (counted after the layer's reductions completed), [6l+2] / [6l+3] the done count
+ * when the forward read of that layer began / the started count when it ended, [6l+4] / [6l+5] the
+ * same for the delta_in read (-1: the forward read serves it); [30] the worker (CTA), [31] its
+ * iteration.  A publish j was seen by a read iff done_j < read begin; not seen iff started_j >= read
+ * end; otherwise it overlapped the read (torn reads possible).  host_pubs (may be NULL):
+ * [n_groups][num_params] each group's publish (-lr * its gradient sum), normative layout.
+ * host_reads (may be NULL): [n_groups][2][num_params] the weight values each group actually read,
+ * [.][0] for its forward pass, [.][1] for its delta_in back-propagation (NaN where the forward
+ * read's copy served), normative layout.
+ * Synchronizing; CHAOS_E_INVALID if the last epoch did not record n_groups groups. */
+chaos_status chaos_debug_trace(chaos_net* net, int64_t* host_records, int64_t n_groups, float* host_pubs,
+                               float* host_reads);
 
 /* Debug: copies the per-image claim counts of the last hogwild epoch (needs
  * CHAOS_OPT_DEBUG_CLAIMS=1 before the epoch) into host_counts[n]. */

@@ -20,6 +20,8 @@ CHAOS_CONV, CHAOS_MAXPOOL, CHAOS_FULL = 1, 2, 3
 CHAOS_TANH, CHAOS_IDENTITY = 0, 1
 HOGWILD, SYNC = 0, 1
 OPT_STREAM, OPT_SYNC_BATCH, OPT_GROUP, OPT_MAX_CTAS, OPT_DEBUG_CLAIMS, OPT_RESERVE_SMS = 0, 1, 2, 3, 4, 5
+OPT_DEBUG_TRACE, OPT_DEBUG_STAGGER = 6, 7
+TRACE_REC = 32  # int64 per group in chaos_debug_trace records
 STATUS = {0: "CHAOS_OK", -1: "CHAOS_E_INVALID", -2: "CHAOS_E_ARCH", -3: "CHAOS_E_UNSUPPORTED",
           -4: "CHAOS_E_LABEL", -5: "CHAOS_E_NONFINITE", -6: "CHAOS_E_CUDA", -7: "CHAOS_E_NCCL"}
 
@@ -31,7 +33,7 @@ EXPORTS = ["chaos_net_create", "chaos_net_destroy", "chaos_net_set_option", "cha
            "chaos_net_launch_info", "chaos_last_error", "chaos_last_status", "chaos_debug_phase_times",
            "chaos_batch_gradient", "chaos_apply_gradient", "chaos_progress_enqueued", "chaos_progress_wait",
            "chaos_avg_snapshot", "chaos_avg_apply", "chaos_dist_unique_id", "chaos_dist_init",
-           "chaos_dist_average", "chaos_dist_average_buffer", "chaos_train_epoch_host_async"]
+           "chaos_dist_average", "chaos_dist_average_buffer", "chaos_train_epoch_host_async", "chaos_debug_trace"]
 
 
 class ChaosError(RuntimeError):
@@ -78,6 +80,7 @@ def lib():
             "chaos_forward": ([vp, vp, C.c_int64, vp], C.c_int),
             "chaos_compute_gradients": ([vp, vp, vp, C.c_int64, fp], C.c_int),
             "chaos_debug_claims": ([vp, ip, C.c_int64], C.c_int),
+            "chaos_debug_trace": ([vp, C.POINTER(C.c_int64), C.c_int64, fp, fp], C.c_int),
             "chaos_batch_gradient": ([vp, vp, vp, C.c_int64, vp], C.c_int),
             "chaos_apply_gradient": ([vp, vp, C.c_float], C.c_int),
             "chaos_net_sync": ([vp], C.c_int),
@@ -125,6 +128,31 @@ def _ptr(t):
     return C.c_void_p(t.data_ptr())
 
 
+def _check_batch(images, labels, n_in, device, cuda):
+    """Images float32 with n * n_in elements, labels int32 of shape (n,), both on the net's device
+    (cuda) or both host tensors/arrays (not cuda).  Raises ValueError (never stripped by -O)."""
+    import torch
+    n = int(labels.shape[0]) if labels is not None else int(images.shape[0])
+    if isinstance(images, torch.Tensor):
+        if images.dtype != torch.float32:
+            raise ValueError(f"images must be float32, got {images.dtype}")
+        if images.is_cuda != cuda or (cuda and images.device != device):
+            raise ValueError(f"images must be on {device if cuda else 'the host'}, got {images.device}")
+        if not images.is_contiguous():
+            raise ValueError("images must be contiguous")
+    numel = images.numel() if isinstance(images, torch.Tensor) else int(np.asarray(images).size)
+    if numel != n * n_in:
+        raise ValueError(f"images must hold n * {n_in} = {n * n_in} values for n = {n} labels")
+    if labels is not None and isinstance(labels, torch.Tensor):
+        if labels.dtype != torch.int32:
+            raise ValueError(f"labels must be int32, got {labels.dtype}")
+        if labels.is_cuda != cuda or (cuda and labels.device != device):
+            raise ValueError(f"labels must be on {device if cuda else 'the host'}, got {labels.device}")
+        if labels.dim() != 1 or not labels.is_contiguous():
+            raise ValueError("labels must be a contiguous 1-D tensor")
+    return n
+
+
 class _CudaArray:
     """__cuda_array_interface__ wrapper so torch.as_tensor can alias the library's buffer."""
 
@@ -152,6 +180,7 @@ class Net:
         s = stream if stream is not None else torch.cuda.current_stream()
         self.set_option(OPT_STREAM, s.cuda_stream)
         self._stream = s
+        self.device = torch.device("cuda", torch.cuda.current_device())
 
     def close(self):
         if getattr(self, "_h", None):
@@ -194,21 +223,24 @@ class Net:
 
     def train_epoch(self, images, labels, lr, mode=HOGWILD):
         """chaos_train_epoch: asynchronous on the net's stream; images/labels CUDA tensors."""
-        n = int(labels.shape[0])
+        n = _check_batch(images, labels, self.n_in, self.device, True)
         _check(lib().chaos_train_epoch(self._h, _ptr(images), _ptr(labels), n, float(lr), int(mode)))
 
     def train_epoch_host(self, images, labels, lr, mode=HOGWILD):
         """chaos_train_epoch_host: host (ideally pinned) buffers; synchronizing."""
         import torch
         if isinstance(images, torch.Tensor):
-            assert not images.is_cuda and images.is_contiguous() and images.dtype == torch.float32
-            assert not labels.is_cuda and labels.is_contiguous() and labels.dtype == torch.int32
+            if not isinstance(labels, torch.Tensor):
+                raise ValueError("images and labels must both be torch tensors or both numpy arrays")
+            _check_batch(images, labels, self.n_in, None, False)
             xp = C.cast(C.c_void_p(images.data_ptr()), C.POINTER(C.c_float))
             yp = C.cast(C.c_void_p(labels.data_ptr()), C.POINTER(C.c_int32))
             n = int(labels.shape[0])
         else:
             images = np.ascontiguousarray(images, np.float32)
             labels = np.ascontiguousarray(labels, np.int32)
+            if labels.ndim != 1 or images.size != len(labels) * self.n_in:
+                raise ValueError(f"images must hold n * {self.n_in} values for n = {len(labels)} labels")
             xp = images.ctypes.data_as(C.POINTER(C.c_float))
             yp = labels.ctypes.data_as(C.POINTER(C.c_int32))
             n = len(labels)
@@ -217,9 +249,10 @@ class Net:
     def train_epoch_host_async(self, images, labels, lr, mode=HOGWILD):
         """chaos_train_epoch_host_async: pinned CPU torch tensors; returns once enqueued (the
         tensors are kept referenced until the next sync of this net)."""
-        assert not images.is_cuda and images.is_contiguous() and images.dtype.itemsize == 4
-        assert not labels.is_cuda and labels.is_contiguous() and labels.dtype.itemsize == 4
-        self._host_refs = (images, labels)
+        _check_batch(images, labels, self.n_in, None, False)
+        # the library waits for a previous async epoch's copies before starting the next one, so
+        # the tensors must stay referenced until then (and until sync())
+        self._host_refs = getattr(self, "_host_refs", [])[-1:] + [(images, labels)]
         xp = C.cast(C.c_void_p(images.data_ptr()), C.POINTER(C.c_float))
         yp = C.cast(C.c_void_p(labels.data_ptr()), C.POINTER(C.c_int32))
         _check(lib().chaos_train_epoch_host_async(self._h, xp, yp, int(labels.shape[0]), float(lr), int(mode)))
@@ -232,7 +265,7 @@ class Net:
     def evaluate(self, images, labels):
         ml = C.c_double()
         ne = C.c_int64()
-        n = int(labels.shape[0])
+        n = _check_batch(images, labels, self.n_in, self.device, True)
         if n == 0:
             _check(lib().chaos_evaluate(self._h, None, None, 0, C.byref(ml), C.byref(ne)))
         else:
@@ -242,6 +275,7 @@ class Net:
     def forward(self, images):
         import torch
         n = int(images.shape[0])
+        _check_batch(images, None, self.n_in, self.device, True)
         out = torch.empty((n, self.n_classes), dtype=torch.float32, device=images.device)
         if n:
             _check(lib().chaos_forward(self._h, _ptr(images), n, _ptr(out)))
@@ -249,7 +283,7 @@ class Net:
 
     def compute_gradients(self, images, labels):
         g = np.zeros(self.n_params, np.float32)
-        n = int(labels.shape[0])
+        n = _check_batch(images, labels, self.n_in, self.device, True)
         gp = g.ctypes.data_as(C.POINTER(C.c_float))
         if n == 0:
             _check(lib().chaos_compute_gradients(self._h, None, None, 0, gp))
@@ -260,7 +294,7 @@ class Net:
     def batch_gradient(self, images, labels, grad):
         """chaos_batch_gradient: grad (CUDA float32, device_params().numel()) = sum of the images'
         gradients at the current weights, internal layout; asynchronous on the net's stream."""
-        n = int(labels.shape[0])
+        n = _check_batch(images, labels, self.n_in, self.device, True)
         if grad.numel() != int(lib().chaos_net_device_params_len(self._h)) or grad.dtype.itemsize != 4:
             raise ValueError("grad must hold chaos_net_device_params_len float32 values")
         if n == 0:
@@ -308,6 +342,19 @@ class Net:
         """chaos_dist_average_buffer: in-place average of a CUDA float32 tensor on `stream`."""
         _check(lib().chaos_dist_average_buffer(self._h, _ptr(buf), int(buf.numel()), stream.cuda_stream))
 
+    def debug_trace(self, n_groups, pubs=True, reads=False):
+        """chaos_debug_trace: (records int64 [n_groups][32], publishes float32 [n_groups][n_params]
+        or None, weights read float32 [n_groups][2][n_params] or None; normative) of the last
+        hogwild epoch run with OPT_DEBUG_TRACE = 1."""
+        rec = np.zeros((n_groups, TRACE_REC), np.int64)
+        pb = np.zeros((n_groups, self.n_params), np.float32) if pubs else None
+        rd = np.zeros((n_groups, 2, self.n_params), np.float32) if reads else None
+        fpp = C.POINTER(C.c_float)
+        _check(lib().chaos_debug_trace(self._h, rec.ctypes.data_as(C.POINTER(C.c_int64)), n_groups,
+                                       pb.ctypes.data_as(fpp) if pubs else None,
+                                       rd.ctypes.data_as(fpp) if reads else None))
+        return (rec, pb, rd) if reads else (rec, pb)
+
     def debug_claims(self, n):
         out = np.zeros(n, np.int32)
         _check(lib().chaos_debug_claims(self._h, out.ctypes.data_as(C.POINTER(C.c_int32)), n))
@@ -325,6 +372,7 @@ class Net:
 
     def sync(self):
         _check(lib().chaos_net_sync(self._h))
+        self._host_refs = []
 
     def launch_info(self):
         v = [C.c_int32() for _ in range(4)]

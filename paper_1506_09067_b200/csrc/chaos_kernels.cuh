@@ -39,7 +39,16 @@ constexpr int kZStride = 16;  // logits / output-delta row stride in shared memo
 constexpr int kHdrBytes = 256;
 constexpr int kBiasScratch = 256;  // floats: FC bias-gradient scratch
 
-enum Mode : int { kHogwild = 0, kSync = 1, kEval = 2, kForward = 3 };
+// kTrace: hogwild (kHogwild semantics) that also records, per claimed group and weighted layer,
+// when its weight reads and its publishes happened on two global event counters, and stores each
+// group's publish in its own slot -- the schedule a replay of the method re-runs (debug only)
+enum Mode : int { kHogwild = 0, kSync = 1, kEval = 2, kForward = 3, kTrace = 4 };
+__host__ __device__ constexpr bool is_hog(int mode) { return mode == kHogwild || mode == kTrace; }
+// kTrace record layout per group (int64): [l * 6 + k] for weighted layer l < 5, k = 0 publish
+// started (rank on the started counter), 1 publish done (rank on the done counter), 2/3 forward
+// read (done count at its start / started count at its end), 4/5 the delta_in read (-1: the
+// forward read's values serve); [30] = worker (CTA), [31] = the worker's iteration.
+constexpr int kTraceRec = 32;
 enum Latch : int { kLatchLabel = 1, kLatchNonfinite = 2 };
 
 __host__ __device__ constexpr int round4(int x) { return (x + 3) / 4 * 4; }
@@ -72,7 +81,7 @@ __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 // Tuning knobs: MT maps per thread in the forward; TT taps per thread and GS split of the
 // (image, window) sum in the weight gradient; RB input rows per band in delta_in.
 template <int C_, int H_, int W_, int M_, int K_, int KP_, int MT_, int TT_, int GS_, int RB_, int PB_ = 0,
-          int MS_ = 0, bool GWMMA_ = false, bool DIN3_ = false, int GWIN_ = 0, bool DWIN_ = false, int NSPL_ = 1>
+          int MS_ = 0, bool UNUSED_ = false, bool DIN3_ = false, int GWIN_ = 0, bool DWIN_ = false, int NSPL_ = 1>
 struct Conv {
     static constexpr int C = C_, H = H_, W = W_, M = M_, K = K_, KP = KP_;
     static constexpr int OH = H - K + 1, OW = W - K + 1;
@@ -84,7 +93,7 @@ struct Conv {
     static constexpr int IN_SZ = C * H * W, OUT_SZ = M * P;
     static constexpr int MT = MT_, TT = TT_, GS = GS_, RB = RB_;
     static constexpr int NB = (H + RB - 1) / RB;
-    // delta_in by window-row bands (conv_din2) when PB > 0: PB window rows per band
+    // delta_in by window-row bands (conv_din3) when PB > 0: PB window rows per band
     static constexpr int PB = PB_;
     static constexpr int HR = PH * KP + K - 1, WR = PW * KP + K - 1;  // input rows/cols that receive delta
     static constexpr int NBAND = PB > 0 ? (PH + PB - 1) / PB : 0;
@@ -92,8 +101,7 @@ struct Conv {
     static constexpr int HAND = NBAND > 1 ? (NBAND - 1) * (K - 1) * WR * C : 0;  // hand-off floats per image
     // MS < 0: the weight gradient by the generic conv_gw published from registers (lanes over maps)
     static constexpr int MS = MS_;
-    // weight gradient on the tensor cores (conv_gw_mma)
-    static constexpr bool GWMMA = GWMMA_;
+    static_assert(!UNUSED_, "slot of the removed tensor-core weight-gradient knob");
     // delta_in with the compact shifted-block loop (conv_din3)
     static constexpr bool DIN3 = DIN3_;
     // dense per-window weight gradient (conv_gw_win) with GWIN output maps per thread, run on the
@@ -201,6 +209,11 @@ struct KArgs {
     unsigned long long* ptime;   // CHAOS_TIMING builds: per-CTA clock64 cycles per phase [grid][kPhases]
     unsigned long long* progress; // hogwild: monotonic count of images whose updates are published
     const unsigned long long* ready;  // hogwild from host buffers: images [0, *ready) have landed
+    unsigned long long* tctr;     // kTrace: [0] publishes started, [1] publishes done
+    long long* trec;              // kTrace: [group][kTraceRec]
+    long long stagger;            // kTrace: CTA b starts after b * stagger cycles
+    float* tw;                    // kTrace: the weight values each group read, [group][2][pint]
+                                  // (internal layout; [.][0] forward reads, [.][1] delta_in reads)
 };
 
 // Phase timing (instrumented build only, -DCHAOS_TIMING): thread 0 adds the clock64 cycles
@@ -322,14 +335,16 @@ __device__ __forceinline__ void wait_publish_reads() {
 template <int MODE>
 __device__ __forceinline__ void publish_bulk(const KArgs& a, int slot, int goff, const float* src, int floats) {
     if (threadIdx.x == 0) {
-        float* dst = (MODE == kHogwild) ? a.params + goff
-                                        : a.partial + static_cast<long long>(slot) * a.pstride + goff;
+        float* dst = is_hog(MODE) ? a.params + goff : a.partial + static_cast<long long>(slot) * a.pstride + goff;
         for (int off = 0; off < floats; off += 16384) {
             const int chunk = (floats - off) > 16384 ? 16384 : (floats - off);
-            if constexpr (MODE == kHogwild)
+            if constexpr (is_hog(MODE))
                 bulk_reduce_add(dst + off, src + off, static_cast<uint32_t>(chunk) * 4u);
             else
                 bulk_s2g(dst + off, src + off, static_cast<uint32_t>(chunk) * 4u);
+            if constexpr (MODE == kTrace)  // and the group's own copy
+                bulk_s2g(a.partial + static_cast<long long>(slot) * a.pstride + goff + off, src + off,
+                         static_cast<uint32_t>(chunk) * 4u);
         }
         bulk_commit();
     }
@@ -337,9 +352,9 @@ __device__ __forceinline__ void publish_bulk(const KArgs& a, int slot, int goff,
 // Direct per-element publish (layers whose gradient does not fit the scratch).
 template <int MODE>
 __device__ __forceinline__ void publish_elem(const KArgs& a, int slot, int idx, float g_scaled) {
-    if constexpr (MODE == kHogwild)
+    if constexpr (is_hog(MODE))
         red_add(a.params + idx, g_scaled);
-    else
+    if constexpr (!is_hog(MODE) || MODE == kTrace)
         a.partial[static_cast<long long>(slot) * a.pstride + idx] = g_scaled;
 }
 
@@ -347,11 +362,84 @@ __device__ __forceinline__ void publish_elem(const KArgs& a, int slot, int idx, 
 // into the shared weights; sync = plain 16-B store into this group's slot.
 template <int MODE>
 __device__ __forceinline__ void publish_vec4(const KArgs& a, int slot, int idx, float4 g_scaled) {
-    if constexpr (MODE == kHogwild)
+    if constexpr (is_hog(MODE))
         red_add4(a.params + idx, g_scaled);
-    else
+    if constexpr (!is_hog(MODE) || MODE == kTrace)
         *reinterpret_cast<float4*>(a.partial + static_cast<long long>(slot) * a.pstride + idx) = g_scaled;
 }
+
+// kTrace event marks (every thread calls them, converged; debug builds of the schedule only).
+// Read start: the done count before any thread / TMA read of the layer; read end: the started
+// count after the last read.  Publish start: counted before any thread issues a reduction of the
+// layer; publish done: counted after every thread's reductions and the bulk ones completed.
+__device__ __forceinline__ void trace_read_begin(const KArgs& a, int slot, int k) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long v;
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.tctr + 1) : "memory");
+        a.trec[static_cast<long long>(slot) * kTraceRec + k] = static_cast<long long>(v);
+        fence_proxy_async();  // the TMA reads issued next follow the load
+    }
+    __syncthreads();
+}
+__device__ __forceinline__ void trace_read_end(const KArgs& a, int slot, int k) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        fence_proxy_async();
+        __threadfence();
+        a.trec[static_cast<long long>(slot) * kTraceRec + k] = static_cast<long long>(atomicAdd(a.tctr, 0ull));
+    }
+    __syncthreads();
+}
+__device__ __forceinline__ void trace_pub_begin(const KArgs& a, int slot, int l) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        a.trec[static_cast<long long>(slot) * kTraceRec + l * 6] = static_cast<long long>(atomicAdd(a.tctr, 1ull));
+        __threadfence();
+    }
+    __syncthreads();
+}
+__device__ __forceinline__ void trace_pub_end(const KArgs& a, int slot, int l) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        bulk_wait_all<0>();
+        fence_proxy_async();
+        __threadfence();
+        a.trec[static_cast<long long>(slot) * kTraceRec + l * 6 + 1] =
+            static_cast<long long>(atomicAdd(a.tctr + 1, 1ull));
+    }
+    __syncthreads();
+}
+// kTrace: copy `floats` weight values a group just read into shared memory (staged at src) to
+// its record of reads (purpose 0 forward, 1 delta_in) at internal offset goff (thread 0; waits
+// until the copy has read src, so the buffer can be refilled right after)
+__device__ __forceinline__ void trace_dump(const KArgs& a, int slot, int purpose, int goff, const float* src,
+                                           int floats) {
+    fence_async_smem();  // generic writes of src (e.g. biases loaded by threads) -> async proxy
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        fence_proxy_async();
+        float* dst = a.tw + (static_cast<long long>(slot) * 2 + purpose) * a.pstride + goff;
+        for (int off = 0; off < floats; off += 16384) {
+            const int chunk = (floats - off) > 16384 ? 16384 : (floats - off);
+            bulk_s2g(dst + off, src + off, static_cast<uint32_t>(chunk) * 4u);
+        }
+        bulk_commit();
+        bulk_wait_read<0>();
+    }
+    __syncthreads();
+}
+#define TR_DUMP(p, goff, src, floats) \
+    do { if constexpr (MODE == kTrace) trace_dump(a, slot, (p), (goff), (src), (floats)); } while (0)
+#define TR_RB(l, p) \
+    do { if constexpr (MODE == kTrace) trace_read_begin(a, slot, (l) * 6 + 2 + 2 * (p)); } while (0)
+#define TR_RE(l, p) \
+    do { if constexpr (MODE == kTrace) trace_read_end(a, slot, (l) * 6 + 3 + 2 * (p)); } while (0)
+#define TR_PB(l) \
+    do { if constexpr (MODE == kTrace) trace_pub_begin(a, slot, (l)); } while (0)
+#define TR_PE(l) \
+    do { if constexpr (MODE == kTrace) trace_pub_end(a, slot, (l)); } while (0)
 
 // A4: p is 16-B aligned; A2: p is 8-B aligned
 template <int N, bool A4, bool A2 = false>
@@ -384,35 +472,6 @@ __device__ __forceinline__ void load_vec(float (&v)[N], const float* p) {
 #pragma unroll
         for (int q = 0; q < N; ++q) v[q] = p[q];
     }
-}
-
-// ------------------------------------------------------------------------------------
-// Tensor-core helpers: mma.sync m16n8k8 TF32 with the 3-pass split (a = a_hi + a_lo,
-// b = b_hi + b_lo; D += a_hi b_lo + a_lo b_hi + a_hi b_hi), which keeps the products to
-// ~2^-21 relative -- fp32-level accuracy for the R9 tolerance (a single TF32 pass is 2^-11).
-// Fragment layout (lane = 4*g8 + t): A 16x8 row-major {(g8,t), (g8+8,t), (g8,t+4), (g8+8,t+4)};
-// B 8x8 {(t,g8), (t+4,g8)}; C 16x8 {(g8,2t), (g8,2t+1), (g8+8,2t), (g8+8,2t+1)}.
-// ------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t to_tf32(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return r;
-}
-__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
-    hi = to_tf32(x);
-    lo = to_tf32(x - __uint_as_float(hi));
-}
-__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ void mma3(float (&d)[4], const uint32_t (&ah)[4], const uint32_t (&al)[4], uint32_t bh0,
-                                     uint32_t bh1, uint32_t bl0, uint32_t bl1) {
-    mma_tf32(d, ah, bl0, bl1);
-    mma_tf32(d, al, bh0, bh1);
-    mma_tf32(d, ah, bh0, bh1);
 }
 
 // Sums 32 values across the warp's lanes at once (v[k] of every lane -> lane k): 16+8+4+2+1
@@ -711,6 +770,71 @@ __device__ __forceinline__ void conv_gw(const KArgs& a, int slot, const float* _
 }
 
 // ------------------------------------------------------------------------------------
+// PHASE(conv_gw_m) conv weight gradient, argmax-routed, lanes over output maps, NPT input maps
+// per thread (KP == 2):
+//   gW[n][i][j][m] = sum_g sum_pp dp[g][m][pp] * in[g][n][2pr(pp)+a+i][2pc(pp)+b+j],  gb[m] = sum dp
+// where (a, b) is the argmax phase of (g, m, pp).  One (d, phase) load per window serves the NPT
+// input maps' K*K gathers (each a load of <= 4 distinct words per warp: one wavefront); the
+// window columns are unrolled so the gather offsets are immediates plus the phase offset.
+// Fixed (g, pp) order per weight (deterministic); direct coalesced publish from registers.
+// ------------------------------------------------------------------------------------
+// Runs on warps [W0, W0 + NWARP) (all warps by default) so it can overlap another phase.
+template <class L, int NT, int MODE, int NPT, int W0 = 0, int NWARP = NT / 32>
+__device__ __forceinline__ void conv_gw_m(const KArgs& a, int slot, const float* __restrict__ in,
+                                          const float* __restrict__ dp, const uint8_t* __restrict__ am, int woff,
+                                          int cnt, float sc) {
+    constexpr int K = L::K, KP = L::KP, KK = L::KK, PW = L::PW, PH = L::PH, P = L::P, M = L::M, C = L::C;
+    constexpr int W = L::W, HW = L::H * L::W;
+    constexpr int NQ = C / NPT;
+    static_assert(KP == 2 && C % NPT == 0, "2x2 pooling, NPT divides C");
+    const int tid = static_cast<int>(threadIdx.x) - W0 * 32;
+    if (tid < 0 || tid >= NWARP * 32) return;
+    for (int it = tid; it < M * NQ; it += NWARP * 32) {
+        const int m = it % M;
+        const int n0 = (it / M) * NPT;
+        float acc[NPT][KK];
+        float accb = 0.f;
+#pragma unroll
+        for (int k = 0; k < NPT; ++k)
+#pragma unroll
+            for (int t = 0; t < KK; ++t) acc[k][t] = 0.f;
+#pragma unroll 1
+        for (int g = 0; g < cnt; ++g) {
+            const float* dpg = dp + g * L::OUT_SZ + m * P;
+            const uint8_t* amg = am + g * L::OUT_SZ + m * P;
+            const float* ing = in + g * L::IN_SZ + n0 * HW;
+#pragma unroll 1
+            for (int pr = 0; pr < PH; ++pr) {
+                const float* inr = ing + pr * KP * W;
+                float dv[PW];
+                int av[PW];
+#pragma unroll
+                for (int pc = 0; pc < PW; ++pc) {
+                    dv[pc] = dpg[pr * PW + pc];
+                    av[pc] = amg[pr * PW + pc];
+                }
+#pragma unroll
+                for (int pc = 0; pc < PW; ++pc) {
+                    const float d = dv[pc];
+                    const float* base = inr + pc * KP + (av[pc] >> 1) * W + (av[pc] & 1);
+                    accb += d;
+#pragma unroll
+                    for (int k = 0; k < NPT; ++k)
+#pragma unroll
+                        for (int t = 0; t < KK; ++t)
+                            acc[k][t] = fmaf(d, base[k * HW + (t / K) * W + (t % K)], acc[k][t]);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < NPT; ++k)
+#pragma unroll
+            for (int t = 0; t < KK; ++t) publish_elem<MODE>(a, slot, woff + ((n0 + k) * KK + t) * L::MP + m, sc * acc[k][t]);
+        if (n0 == 0) publish_elem<MODE>(a, slot, woff + L::WFL + m, sc * accb);
+    }
+}
+
+// ------------------------------------------------------------------------------------
 // PHASE(conv_gw_win) conv weight gradient, dense per pooling window, branch-free (KP == 2):
 //   gW[n][i][j][m] = sum_g sum_w sum_{phase q} Dz_q[g][m][w] * in[g][n][2pr+a(q)+i][2pc+b(q)+j]
 // where Dz_q = d[g][m][w] if the argmax of (g, m, w) has phase q, else 0 (4x the argmax-sparse
@@ -884,98 +1008,6 @@ __device__ __forceinline__ void conv_gw_wt(const KArgs& a, int slot, const float
                 publish_vec4<MODE>(a, slot, woff + L::WFL + m0 + q4,
                                    make_float4(sc * accb[q4], sc * accb[q4 + 1], sc * accb[q4 + 2], sc * accb[q4 + 3]));
     }
-}
-
-// ------------------------------------------------------------------------------------
-// PHASE(conv_gw_mma) conv weight gradient on the tensor cores (KP == 2), as the dense GEMM
-//   gW[k][m] = sum_g sum_p in[g][n(k)][r(p)+i(k)][c(p)+j(k)] * Dz[g][m][p]
-// over the conv positions p that lie in a pooling window (k = n*K*K + i*K + j, the row of the
-// internal weight block; Dz = the pooled delta routed to its argmax, zero elsewhere, built
-// on the fly from (dp, am) in the B fragment).  One warp per 16-row tile of k and all output
-// maps m; the A fragment is an implicit im2col gather.  Dense work is KP^2 = 4x the
-// argmax-sparse MACs, on a pipe ~4x faster than FFMA that also frees the issue slots.
-// Fixed k-step order per element (deterministic).  Bias gradient: fixed-order sums of dp.
-// ------------------------------------------------------------------------------------
-template <class L, int NT, int MODE>
-__device__ __forceinline__ void conv_gw_mma(const KArgs& a, int slot, const float* __restrict__ in,
-                                            const float* __restrict__ dp, const uint8_t* __restrict__ am,
-                                            float* __restrict__ scr, int woff, int cnt, float sc) {
-    constexpr int K = L::K, KK = L::KK, PW = L::PW, PH = L::PH, P = L::P, M = L::M, C = L::C;
-    constexpr int W = L::W, HW = L::H * L::W;
-    constexpr int RR = C * KK, MTL = (RR + 15) / 16, NTL = (M + 7) / 8;
-    constexpr int CW = PW * 2, KPOS = PH * 2 * CW, KSTEPS = (KPOS + 7) / 8;
-    constexpr int NW = NT / 32;
-    static_assert(L::KP == 2, "2x2 pooling");
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int g8 = lane >> 2, t = lane & 3;
-    for (int unit = warp; unit < MTL; unit += NW) {
-        const int kA = unit * 16 + g8, kB = kA + 8;
-        const bool vA = kA < RR, vB = kB < RR;
-        const int koA = vA ? (kA / KK) * HW + ((kA % KK) / K) * W + (kA % KK) % K : 0;
-        const int koB = vB ? (kB / KK) * HW + ((kB % KK) / K) * W + (kB % KK) % K : 0;
-        float acc[NTL][4];
-#pragma unroll
-        for (int nt = 0; nt < NTL; ++nt)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) acc[nt][q] = 0.f;
-#pragma unroll 1
-        for (int g = 0; g < cnt; ++g) {
-            const float* ing = in + g * L::IN_SZ;
-            const float* dpg = dp + g * L::OUT_SZ;
-            const uint8_t* amg = am + g * L::OUT_SZ;
-#pragma unroll 1
-            for (int ks = 0; ks < KSTEPS; ++ks) {
-                const int p0 = ks * 8 + t, p1 = p0 + 4;
-                const bool v0 = p0 < KPOS, v1 = p1 < KPOS;
-                const int r0 = p0 / CW, c0 = p0 % CW, r1 = p1 / CW, c1 = p1 % CW;
-                const int po0 = r0 * W + c0, po1 = r1 * W + c1;
-                uint32_t ah[4], al[4];
-                split_tf32((vA && v0) ? ing[koA + po0] : 0.f, ah[0], al[0]);
-                split_tf32((vB && v0) ? ing[koB + po0] : 0.f, ah[1], al[1]);
-                split_tf32((vA && v1) ? ing[koA + po1] : 0.f, ah[2], al[2]);
-                split_tf32((vB && v1) ? ing[koB + po1] : 0.f, ah[3], al[3]);
-                const int w0 = (r0 >> 1) * PW + (c0 >> 1), ph0 = ((r0 & 1) << 1) | (c0 & 1);
-                const int w1 = (r1 >> 1) * PW + (c1 >> 1), ph1 = ((r1 & 1) << 1) | (c1 & 1);
-#pragma unroll
-                for (int nt = 0; nt < NTL; ++nt) {
-                    const int m = nt * 8 + g8;
-                    const bool vm = (NTL * 8 == M) || m < M;
-                    const int o0 = m * P + w0, o1 = m * P + w1;
-                    const float b0 = (vm && v0 && amg[o0] == ph0) ? dpg[o0] : 0.f;
-                    const float b1 = (vm && v1 && amg[o1] == ph1) ? dpg[o1] : 0.f;
-                    uint32_t bh0, bl0, bh1, bl1;
-                    split_tf32(b0, bh0, bl0);
-                    split_tf32(b1, bh1, bl1);
-                    mma3(acc[nt], ah, al, bh0, bh1, bl0, bl1);
-                }
-            }
-        }
-#pragma unroll
-        for (int nt = 0; nt < NTL; ++nt) {
-            const int m = nt * 8 + 2 * t;
-            if (vA) {
-                if (m < M) scr[kA * L::MP + m] = sc * acc[nt][0];
-                if (m + 1 < M) scr[kA * L::MP + m + 1] = sc * acc[nt][1];
-            }
-            if (vB) {
-                if (m < M) scr[kB * L::MP + m] = sc * acc[nt][2];
-                if (m + 1 < M) scr[kB * L::MP + m + 1] = sc * acc[nt][3];
-            }
-        }
-    }
-    for (int m = threadIdx.x; m < L::MP; m += NT) {  // bias: fixed-order sum over (g, window)
-        float s = 0.f;
-        if (m < M)
-            for (int g = 0; g < cnt; ++g)
-                for (int w = 0; w < P; ++w) s += dp[g * L::OUT_SZ + m * P + w];
-        scr[L::WFL + m] = sc * s;
-    }
-    if constexpr (L::MP > M) {  // padding columns of the block publish zeros
-        for (int e = threadIdx.x; e < L::ROWS * (L::MP - M); e += NT)
-            scr[(e / (L::MP - M)) * L::MP + M + e % (L::MP - M)] = 0.f;
-    }
-    sync_for_async();
-    publish_bulk<MODE>(a, slot, woff, scr, L::BLK);
 }
 
 // ------------------------------------------------------------------------------------
@@ -1210,173 +1242,14 @@ __device__ __forceinline__ void conv_din_gm(const float* __restrict__ wg, const 
 }
 
 // ------------------------------------------------------------------------------------
-// PHASE(conv_din2) partial derivatives of the previous layer, by window-row bands (KP == 2):
-//   dout[g][n][y][x] = (1 - in^2) * sum_m sum_w [argpos(g,m,w) + (i,j) == (y,x)] W[m][n][i][j] d[g][m][w]
-// One warp per (image g, band of PB window rows, 32 input maps n); lanes over n.  A band's
-// windows scatter into input rows [band*PB*KP, band*PB*KP + BR): a BR x WR register block,
-// so every window of the band is visited exactly once per m and its 2-bit argmax phase picks,
-// by a warp-uniform two-level branch, which compile-time registers its K*K MACs land in.
-// Weights for 4 output maps per LDS.128 (W[n][tap][m..m+3]).  Adjacent bands overlap in
-// K-1 rows: each band hands its last K-1 rows to the next through `hand` (fixed order, no
-// atomics), then every band writes the rows it owns, times (1 - in^2), to `out` (may alias `in`).
-// Requires one warp per task (G * NBAND * ceil(C/32) <= warps); rows/cols that receive no
-// delta (floor-dropped) are written as 0.  W is the staged pre-update snapshot (R5).
-// ------------------------------------------------------------------------------------
-template <class L, int NT>
-__device__ __forceinline__ void conv_din2(const float* __restrict__ wsm, const float* __restrict__ dp,
-                                          const uint8_t* __restrict__ am, const float* in, float* out,
-                                          float* __restrict__ hand, int cnt) {
-    constexpr int K = L::K, KP = L::KP, KK = L::KK, PW = L::PW, PH = L::PH, P = L::P, M = L::M, C = L::C;
-    constexpr int H = L::H, W = L::W, HW = H * W, PB = L::PB, NBAND = L::NBAND, BR = L::BR, WR = L::WR;
-    constexpr int NCW = (C + 31) / 32;
-    static_assert(KP == 2, "conv_din2 handles 2x2 pooling");
-    static_assert(NBAND == 1 || KP >= K - 1, "band overlap must stay within adjacent bands");
-    static_assert(M % 4 == 0 && L::MP == M, "4 output maps per vector load");
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int total = cnt * NBAND * NCW;
-    const bool has = warp < total;
-    const int cw = warp % NCW;
-    const int band = (warp / NCW) % NBAND;
-    const int g = warp / (NCW * NBAND);
-    const int n = cw * 32 + lane;
-    const bool act = has && n < C;
-    float acc[BR][WR];
-#pragma unroll
-    for (int r = 0; r < BR; ++r)
-#pragma unroll
-        for (int c = 0; c < WR; ++c) acc[r][c] = 0.f;
-    if (has) {
-        const int pr0 = band * PB;
-        const float* dpg = dp + g * L::OUT_SZ;
-        const uint8_t* amg = am + g * L::OUT_SZ;
-        const float* wn = wsm + (act ? n : 0) * KK * L::MP;
-        // per output map: K*K weights (4 maps per LDS.128 + select when K*K is small, else scalar
-        // loads), then every window's (delta, argmax) loaded before the first branch
-        constexpr bool W4 = KK <= 4;
-#pragma unroll 1
-        for (int m4 = 0; m4 < M; m4 += 4) {
-            float4 w4[W4 ? KK : 1];
-            if constexpr (W4) {
-#pragma unroll
-                for (int tp = 0; tp < KK; ++tp) w4[tp] = *reinterpret_cast<const float4*>(wn + tp * L::MP + m4);
-            }
-#pragma unroll 1
-            for (int mm = 0; mm < 4; ++mm) {
-                const int m = m4 + mm;
-                float w[KK];
-#pragma unroll
-                for (int tp = 0; tp < KK; ++tp) {
-                    if constexpr (W4)
-                        w[tp] = mm == 0 ? w4[tp].x : mm == 1 ? w4[tp].y : mm == 2 ? w4[tp].z : w4[tp].w;
-                    else
-                        w[tp] = wn[tp * L::MP + m];
-                }
-                float dv[PB][PW];
-                int av[PB][PW];
-#pragma unroll
-                for (int wr = 0; wr < PB; ++wr)
-#pragma unroll
-                    for (int pc = 0; pc < PW; ++pc) {
-                        const bool ok = pr0 + wr < PH;
-                        const int o = m * P + (ok ? pr0 + wr : 0) * PW + pc;
-                        dv[wr][pc] = dpg[o];
-                        av[wr][pc] = ok ? static_cast<int>(amg[o]) : -1;
-                    }
-#pragma unroll
-                for (int wr = 0; wr < PB; ++wr) {
-#pragma unroll
-                    for (int pc = 0; pc < PW; ++pc) {
-                        const float d = dv[wr][pc];
-                        const int arg = av[wr][pc];
-                        // warp-uniform two-level branch on the argmax phase (a, b)
-                        if (arg < 2) {
-                            if (arg == 0) {
-#pragma unroll
-                                for (int i = 0; i < K; ++i)
-#pragma unroll
-                                    for (int j = 0; j < K; ++j)
-                                        acc[wr * KP + i][pc * KP + j] = fmaf(w[i * K + j], d, acc[wr * KP + i][pc * KP + j]);
-                            } else if (arg == 1) {
-#pragma unroll
-                                for (int i = 0; i < K; ++i)
-#pragma unroll
-                                    for (int j = 0; j < K; ++j)
-                                        acc[wr * KP + i][pc * KP + 1 + j] =
-                                            fmaf(w[i * K + j], d, acc[wr * KP + i][pc * KP + 1 + j]);
-                            }
-                        } else {
-                            if (arg == 2) {
-#pragma unroll
-                                for (int i = 0; i < K; ++i)
-#pragma unroll
-                                    for (int j = 0; j < K; ++j)
-                                        acc[wr * KP + 1 + i][pc * KP + j] =
-                                            fmaf(w[i * K + j], d, acc[wr * KP + 1 + i][pc * KP + j]);
-                            } else {
-#pragma unroll
-                                for (int i = 0; i < K; ++i)
-#pragma unroll
-                                    for (int j = 0; j < K; ++j)
-                                        acc[wr * KP + 1 + i][pc * KP + 1 + j] =
-                                            fmaf(w[i * K + j], d, acc[wr * KP + 1 + i][pc * KP + 1 + j]);
-                            }
-                        }
-                    }
-                }
-            }
-        }
-    }
-    if constexpr (NBAND > 1) {
-        // hand the last K-1 rows to the next band: hand[g][band][r][c][n]
-        if (act && band < NBAND - 1) {
-            float* hb = hand + ((g * (NBAND - 1) + band) * (K - 1)) * WR * C + n;
-#pragma unroll
-            for (int r = 0; r < K - 1; ++r)
-#pragma unroll
-                for (int c = 0; c < WR; ++c) hb[(r * WR + c) * C] = acc[BR - (K - 1) + r][c];
-        }
-        __syncthreads();
-        if (act && band > 0) {
-            const float* hb = hand + ((g * (NBAND - 1) + band - 1) * (K - 1)) * WR * C + n;
-#pragma unroll
-            for (int r = 0; r < K - 1; ++r)
-#pragma unroll
-                for (int c = 0; c < WR; ++c) acc[r][c] += hb[(r * WR + c) * C];
-        }
-    }
-    if (act) {
-        // rows owned: [y0, y1); the last band also owns the rows below (0 if never reached)
-        const int y0 = band * PB * KP;
-        const float* ib = in + g * L::IN_SZ + n * HW;
-        float* ob = out + g * L::IN_SZ + n * HW;
-#pragma unroll
-        for (int lr = 0; lr < BR; ++lr) {
-            const int y = y0 + lr;
-            const bool own = (band == NBAND - 1) ? (y < H) : (lr < PB * KP);
-            if (own) {
-#pragma unroll
-                for (int x = 0; x < W; ++x) {
-                    const float v = ib[y * W + x];
-                    ob[y * W + x] = (x < WR ? acc[lr][x] : 0.f) * (1.f - v * v);
-                }
-            }
-        }
-        if (band == NBAND - 1) {
-            for (int y = y0 + BR; y < H; ++y)
-#pragma unroll
-                for (int x = 0; x < W; ++x) ob[y * W + x] = 0.f;
-        }
-    }
-}
-
-// ------------------------------------------------------------------------------------
 // PHASE(fc_fwd) fully connected forward: one warp per output row, lanes over inputs,
 // weights streamed from L2 (__ldcg: on-demand reads of the shared store, no stale L1 copy).
 // ------------------------------------------------------------------------------------
-template <class F, int G, int NT, bool SMEMW = false>  // SMEMW: W and b staged in shared memory
+// TD (kTrace only): every weight / bias value read is also stored at td[w index] / td[WFL + o]
+template <class F, int G, int NT, bool SMEMW = false, bool TD = false>  // SMEMW: W and b staged in shared memory
 __device__ __forceinline__ void fc_fwd(const float* __restrict__ Wg, const float* __restrict__ bg,
                                        const float* __restrict__ in, float* __restrict__ out, int ostride,
-                                       int cnt) {
+                                       int cnt, float* __restrict__ td = nullptr) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int NW = NT / 32;
     for (int o = warp; o < F::OUT; o += NW) {
@@ -1387,10 +1260,13 @@ __device__ __forceinline__ void fc_fwd(const float* __restrict__ Wg, const float
 #pragma unroll 4
         for (int i = lane; i < F::IN; i += 32) {
             const float w = SMEMW ? wr[i] : __ldcg(wr + i);
+            if constexpr (TD) td[o * F::IN + i] = w;
 #pragma unroll
             for (int g = 0; g < G; ++g) acc[g] = fmaf(w, in[g * F::IN + i], acc[g]);
         }
         const float b = SMEMW ? bg[o] : __ldcg(bg + o);
+        if constexpr (TD)
+            if (lane == 0) td[F::WFL + o] = b;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
             const float s = warp_sum(acc[g]) + b;
@@ -1400,13 +1276,15 @@ __device__ __forceinline__ void fc_fwd(const float* __restrict__ Wg, const float
 }
 
 // ------------------------------------------------------------------------------------
-// PHASE(conv_din3) conv_din2 with a compact loop body: the task's PB window rows are a
+// PHASE(conv_din3) delta_in by window-row bands (KP == 2), compact loop body: the task's PB window rows are a
 // runtime loop over ONE window row's (KP+K-1) x WR register block, which shifts down by KP
 // rows after each window row (its first KP rows are then final for this task).  The
 // unrolled code is one window row (PW windows x 4 phases), so it stays in the instruction
 // cache.  The first window row's KP rows wait in `pend` for the previous band's hand-off.
 // ------------------------------------------------------------------------------------
-template <class L, int NT, bool DEFER = false>
+// WTP > 0: the weights come from a transposed copy [m][C*K*K] with row pitch WTP (odd: lanes over
+// input maps then read conflict-free; the staged [C*K*K][MP] layout puts them 540 floats apart)
+template <class L, int NT, bool DEFER = false, int WTP = 0>
 __device__ __forceinline__ void conv_din3(const float* __restrict__ wsm, const float* __restrict__ dp,
                                           const uint8_t* __restrict__ am, const float* in, float* out,
                                           float* __restrict__ hand, int cnt) {
@@ -1446,8 +1324,8 @@ __device__ __forceinline__ void conv_din3(const float* __restrict__ wsm, const f
     if (has) {
         const float* dpg = dp + g * L::OUT_SZ;
         const uint8_t* amg = am + g * L::OUT_SZ;
-        const float* wn = wsm + (act ? n : 0) * KK * L::MP;
-        constexpr bool W4 = KK <= 4;
+        const float* wn = wsm + (act ? n : 0) * (WTP > 0 ? KK : KK * L::MP);
+        constexpr bool W4 = KK <= 4 && WTP == 0;
 #pragma unroll 1
         for (int wr = 0; wr < PB; ++wr) {
             const int pr = band * PB + wr;
@@ -1468,6 +1346,8 @@ __device__ __forceinline__ void conv_din3(const float* __restrict__ wsm, const f
                     for (int tp = 0; tp < KK; ++tp) {
                         if constexpr (W4)
                             w[tp] = mm == 0 ? w4[tp].x : mm == 1 ? w4[tp].y : mm == 2 ? w4[tp].z : w4[tp].w;
+                        else if constexpr (WTP > 0)
+                            w[tp] = wn[m * WTP + tp];
                         else
                             w[tp] = wn[tp * L::MP + m];
                     }
@@ -1701,6 +1581,86 @@ __device__ __forceinline__ void conv_din_win(const float* __restrict__ wsm, cons
 }
 
 // ------------------------------------------------------------------------------------
+// PHASE(conv_din_winp) conv_din_win from the phase-expanded delta with the delta loads of output
+// map m+1 issued before map m's FMAs (software pipelined: the warp's FMAs no longer wait on
+// their shared-memory loads; one warp per (image, 32 input maps) leaves few warps to hide them).
+// ------------------------------------------------------------------------------------
+template <class L, int NT, bool DEFER = false>
+__device__ __forceinline__ void conv_din_winp(const float* __restrict__ wsm, const float* __restrict__ in,
+                                              float* __restrict__ out, int cnt, const float4* __restrict__ dq4) {
+    constexpr int K = L::K, KP = L::KP, KK = L::KK, PW = L::PW, P = L::P, M = L::M, C = L::C;
+    constexpr int H = L::H, W = L::W, HW = H * W, HR = L::HR, WR = L::WR;
+    constexpr int NCW = (C + 31) / 32;
+    static_assert(KP == 2 && M % 4 == 0 && L::MP == M, "2x2 pooling, 4 maps per vector load");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool has = warp < cnt * NCW;
+    if (!DEFER && !has) return;
+    const int cw = warp % NCW, g = has ? warp / NCW : 0;
+    const int n = cw * 32 + lane;
+    const bool act = has && n < C;
+    const float* wn = wsm + (act ? n : 0) * KK * L::MP;
+    const float4* dqg = dq4 + g * L::OUT_SZ;
+    float acc[HR][WR];
+#pragma unroll
+    for (int y = 0; y < HR; ++y)
+#pragma unroll
+        for (int x = 0; x < WR; ++x) acc[y][x] = 0.f;
+    float4 cur[P];
+    if (has) {
+#pragma unroll
+        for (int w = 0; w < P; ++w) cur[w] = dqg[w];
+    }
+#pragma unroll 1
+    for (int m4 = 0; m4 < (has ? M : 0); m4 += 4) {
+        float4 w4[KK];
+#pragma unroll
+        for (int tp = 0; tp < KK; ++tp) w4[tp] = *reinterpret_cast<const float4*>(wn + tp * L::MP + m4);
+#pragma unroll
+        for (int mm = 0; mm < 4; ++mm) {
+            const int m = m4 + mm;
+            float4 nxt[P];
+            const int mn = (m + 1 < M) ? m + 1 : m;
+#pragma unroll
+            for (int w = 0; w < P; ++w) nxt[w] = dqg[mn * P + w];
+#pragma unroll
+            for (int w = 0; w < P; ++w) {
+                const int pr = w / PW, pc = w % PW;
+                const float dqv[4] = {cur[w].x, cur[w].y, cur[w].z, cur[w].w};
+#pragma unroll
+                for (int aa = 0; aa < KP; ++aa)
+#pragma unroll
+                    for (int bb = 0; bb < KP; ++bb) {
+                        const float dq = dqv[aa * KP + bb];
+#pragma unroll
+                        for (int i = 0; i < K; ++i)
+#pragma unroll
+                            for (int j = 0; j < K; ++j) {
+                                const float4 t = w4[i * K + j];
+                                const float wv = mm == 0 ? t.x : mm == 1 ? t.y : mm == 2 ? t.z : t.w;
+                                acc[pr * KP + aa + i][pc * KP + bb + j] =
+                                    fmaf(wv, dq, acc[pr * KP + aa + i][pc * KP + bb + j]);
+                            }
+                    }
+            }
+#pragma unroll
+            for (int w = 0; w < P; ++w) cur[w] = nxt[w];
+        }
+    }
+    if constexpr (DEFER) __syncthreads();
+    if (act) {
+        const float* ib = in + g * L::IN_SZ + n * HW;
+        float* ob = out + g * L::IN_SZ + n * HW;
+#pragma unroll
+        for (int y = 0; y < H; ++y)
+#pragma unroll
+            for (int x = 0; x < W; ++x) {
+                const float v = ib[y * W + x];
+                ob[y * W + x] = (y < HR && x < WR ? acc[y < HR ? y : 0][x < WR ? x : 0] : 0.f) * (1.f - v * v);
+            }
+    }
+}
+
+// ------------------------------------------------------------------------------------
 // PHASE(fc_fwd2) fully connected forward, IN % 4 == 0: one warp per NR output rows, lanes
 // over 16-B column quads; every weight load of the NR rows is issued before the first FMA
 // (__ldcg: on-demand reads of the shared store from L2), activations are LDS.128 broadcasts
@@ -1861,10 +1821,12 @@ __device__ __forceinline__ void fc_bwd2(const KArgs& a, int slot, int woff, int 
 // RCH rows are TMA bulk-copied (cp.async.bulk) into two buffers, the copy of chunk c+2
 // overlapping the compute of chunk c+1; one warp per row, lanes over 16-B column quads.
 // ------------------------------------------------------------------------------------
-template <class F, int G, int NT, int RCH>
+template <class F, int G, int NT, int RCH, int MODE = kHogwild>
 __device__ __forceinline__ void fc_fwd3(const float* __restrict__ Wg, const float* __restrict__ bg,
                                         const float* __restrict__ in, float* __restrict__ out, int ostride, int cnt,
-                                        float* __restrict__ buf, Loader& LA, Loader& LB, float* __restrict__ sb) {
+                                        float* __restrict__ buf, Loader& LA, Loader& LB, float* __restrict__ sb,
+                                        const KArgs* ta = nullptr, int slot = 0, int woff = 0) {
+    // MODE == kTrace: each chunk / the biases as read go to the group's forward read record (ta)
     // sb: F::OUT floats of shared scratch for the biases (loaded once, up front)
     static_assert(F::IN % 4 == 0 && (RCH * F::IN) % 4 == 0, "16-B chunks");
     constexpr int IN4 = F::IN / 4, NK = (IN4 + 31) / 32, NW = NT / 32;
@@ -1875,12 +1837,14 @@ __device__ __forceinline__ void fc_fwd3(const float* __restrict__ Wg, const floa
     if (NCH > 1) LB.issue(buf + RCH * F::IN, Wg + RCH * F::IN, rows(1) * F::IN);
     for (int o = threadIdx.x; o < F::OUT; o += NT) sb[o] = __ldcg(bg + o);
     __syncthreads();
+    if constexpr (MODE == kTrace) trace_dump(*ta, slot, 0, woff + F::WFL, sb, F::BFL);  // 16-B multiple
     for (int c = 0; c < NCH; ++c) {
         const float* cb = buf + (c & 1) * RCH * F::IN;
         if (c & 1)
             LB.wait();
         else
             LA.wait();
+        if constexpr (MODE == kTrace) trace_dump(*ta, slot, 0, woff + c * RCH * F::IN, cb, rows(c) * F::IN);
         // RPW rows per warp pass: each activation quad loaded from shared memory feeds RPW rows
         constexpr int RPW = 2;
         for (int r0 = warp * RPW; r0 < rows(c); r0 += NW * RPW) {
@@ -1980,6 +1944,7 @@ __device__ __forceinline__ void fc_bwd3(const KArgs& a, int slot, int woff, int 
             else
                 LA.wait();
         }
+        if constexpr (MODE == kTrace) trace_dump(a, slot, 1, woff + c * RCH * F::IN, cb, rows(c) * F::IN);
         if (act) {
             for (int r = rg; r < rows(c); r += NRG) {
                 const int o = c * RCH + r;
@@ -2057,6 +2022,10 @@ __device__ __forceinline__ void fc_bwd(const KArgs& a, int slot, int woff, int b
                                        const float* __restrict__ dz, int dstride, float* __restrict__ S,
                                        float* __restrict__ bsc, int cnt, float sc,
                                        const float* __restrict__ wstaged = nullptr) {  // W staged in smem
+    // kTrace: the W values read from global for delta_in go to the group's delta_in read record
+    float* td = nullptr;
+    if constexpr (MODE == kTrace) td = a.tw + (static_cast<long long>(slot) * 2 + 1) * a.pstride + woff;
+    (void)td;
     constexpr int RPC0 = SHALF / F::IN;  // rows per chunk
     constexpr int RPC = (RPC0 >= F::OUT) ? F::OUT : ((RPC0 * F::IN) % 4 == 0 ? RPC0 : RPC0 / 4 * 4);
     static_assert(RPC >= 1, "S half must hold a weight row");
@@ -2093,6 +2062,12 @@ __device__ __forceinline__ void fc_bwd(const KArgs& a, int slot, int woff, int b
                         w[q] = (o + q < o1) ? (wstaged ? wstaged[(o + q) * F::IN + col]
                                                        : __ldcg(Wg + static_cast<long long>(o + q) * F::IN + col))
                                             : 0.f;
+                    if constexpr (MODE == kTrace) {
+                        if (!wstaged) {
+                            for (int q = 0; q < 4; ++q)
+                                if (o + q < o1) td[(o + q) * F::IN + col] = w[q];
+                        }
+                    }
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         if (o + q < o1) {
@@ -2158,7 +2133,8 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
     constexpr int NCONV = Net::NCONV, NFULL = Net::NFULL;
     constexpr int IMG = C1::IN_SZ;
     constexpr int SHALF = S::SFL / 2 / 4 * 4;
-    constexpr bool TRAIN = (MODE == kHogwild || MODE == kSync);
+    constexpr bool TRAIN = (is_hog(MODE) || MODE == kSync);
+    static_assert(MODE != kTrace || Net::TRACE, "kTrace is instantiated for nets with trace points only");
     // weight-buffer placement: W1 at 0, W2 at the tail (prefetched during conv1), W3 in two
     // halves (first half prefetched during conv2 into [0, W3A), second after conv2)
     // BIGW nets (Table I large): W1 at 0 and W2 right after it, both staged once per iteration
@@ -2171,13 +2147,27 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
     // FC1 weights staged through WB in two chunks of FRCH rows (large net: WB is free between
     // the conv3 forward and the conv3 backward, which re-fetches W3)
     constexpr bool FCSTAGE = (NCONV == 3) && (NFULL == 2) && (F1::IN % 4 == 0) && !BIG;
+    // conv2 delta_in from a transposed W2 copy (pitch C2_WTP, odd), 3-conv staged nets
+#ifndef CHAOS_C2_WTP
+#define CHAOS_C2_WTP 1
+#endif
+#ifndef CHAOS_C2_GWM  // conv2 weight gradient: conv_gw_m with this many input maps per thread (0: conv_gw)
+#define CHAOS_C2_GWM 4
+#endif
+#ifndef CHAOS_C3_DINP  // conv3 delta_in: the software-pipelined conv_din_winp
+#define CHAOS_C3_DINP 1
+#endif
+#ifndef CHAOS_C2_PAR  // conv2 backward: delta_in (window-row bands, PB >= 2) beside conv_gw_m on the other warps
+#define CHAOS_C2_PAR 0
+#endif
+    constexpr int C2_WTP = (CHAOS_C2_WTP && NCONV == 3 && !BIG && C2::DIN3 && C2::GWIN == 0) ? (C2::ROWS | 1) : 0;
     constexpr int FRCH = FCSTAGE ? (S::WBUF / (2 * F1::IN)) : 1;
     static_assert(!FCSTAGE || FRCH >= 1, "FC1 chunk must hold a row");
     static_assert(NCONV < 2 || C1::BLK <= W2OFF, "W1 and W2 must not overlap");
     static_assert(NCONV < 2 || C2::PB == 0 || G * C2::NBAND * ((C2::C + 31) / 32) <= NT / 32,
-                  "conv_din2 needs one warp per (image, band, 32 maps)");
+                  "conv_din3 needs one warp per (image, band, 32 maps)");
     static_assert(NCONV < 3 || C3::PB == 0 || G * C3::NBAND * ((C3::C + 31) / 32) <= NT / 32,
-                  "conv_din2 needs one warp per (image, band, 32 maps)");
+                  "conv_din3 needs one warp per (image, band, 32 maps)");
 
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // 6 mbarriers
@@ -2199,7 +2189,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
     uint8_t* am2 = amb + S::AM2;
     uint8_t* am3 = amb + S::AM3;
     const float* P = a.params;
-    const float sc = (MODE == kHogwild) ? a.neg_lr : 1.f;
+    const float sc = is_hog(MODE) ? a.neg_lr : 1.f;
     (void)a2;
     (void)a3;
     (void)am2;
@@ -2220,11 +2210,14 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
     int pending_progress = 0;   // hogwild: images of the previous iteration not yet counted in a.progress
     long long t_last = clock64();
     (void)t_last;
+    if constexpr (MODE == kTrace)  // debug: CTA b starts b * stagger cycles late (varied interleavings)
+        if (threadIdx.x == 0 && a.stagger > 0)
+            while (clock64() - t_last < a.stagger * static_cast<long long>(blockIdx.x)) __nanosleep(1000);
     for (;;) {
         // ---------------- a1: claim the next unprocessed images
         if (threadIdx.x == 0) {
             long long base;
-            if constexpr (MODE == kHogwild) {
+            if constexpr (is_hog(MODE)) {
                 base = next_claim >= 0 ? next_claim
                                        : static_cast<long long>(atomicAdd(a.counter, static_cast<unsigned long long>(G)));
                 if constexpr (GATED)  // host entry: the copy stream advances *ready after each chunk
@@ -2242,6 +2235,14 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
         const int slot = static_cast<int>(base / G);
         const int cnt = static_cast<int>(min(static_cast<long long>(G), a.n - base));
         ++iter;
+        if constexpr (MODE == kTrace) {
+            if (threadIdx.x == 0) {
+                a.trec[static_cast<long long>(slot) * kTraceRec + 30] = blockIdx.x;
+                a.trec[static_cast<long long>(slot) * kTraceRec + 31] = iter - 1;
+            }
+        }
+        TR_RB(0, 0);  // W1 (and W2 / the staged FC weights) are read from here on
+        if constexpr (NCONV >= 2 || S::FWB > 0) TR_RB(1, 0);
         if (threadIdx.x < cnt) {
             int lab = 0;
             if constexpr (MODE != kForward) {
@@ -2252,7 +2253,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 }
             }
             s_lab[threadIdx.x] = lab;
-            if constexpr (MODE == kHogwild)
+            if constexpr (is_hog(MODE))
                 if (a.claims) atomicAdd(a.claims + base + threadIdx.x, 1);
         }
         // stage images (bulk when 16-B aligned) + W1 on bar0, prefetch W2 on bar1
@@ -2273,6 +2274,8 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             for (int i = threadIdx.x; i < cnt * IMG; i += NT) sS[i] = __ldg(xsrc + i);
         L0.wait();
         if (!x_bulk) __syncthreads();
+        TR_RE(0, 0);
+        TR_DUMP(0, O::c1w, wb, C1::BLK);
         PTIME(1);
 
         // ---------------- a2: conv -> tanh -> pool, layer by layer
@@ -2282,8 +2285,11 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             fence_async_smem();
             __syncthreads();
             PTIME(2);
+            if constexpr (NCONV >= 3 && !BIG) TR_RB(2, 0);
             if constexpr (NCONV >= 3 && !BIG) L2.issue(wb, P + O::c3w, W3A);  // W1 region is dead: W3's first half
             L1.wait();
+            TR_RE(1, 0);
+            if constexpr (!BIG) TR_DUMP(0, O::c2w, wb + W2OFF, C2::BLK);
             conv_fwd<C2, NT>(a1, wb + W2OFF, a2, am2, cnt);
             alast = a2;
         }
@@ -2300,6 +2306,8 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             L3.issue(wb + W3A, P + O::c3w + W3A, C3::BLK - W3A);
             L2.wait();
             L3.wait();
+            TR_RE(2, 0);
+            TR_DUMP(0, O::c3w, wb, C3::BLK);
             conv_fwd<C3, NT>(a2, wb, a3, am3, cnt);
             alast = a3;
         }
@@ -2308,7 +2316,12 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
         PTIME(4);
         // ---------------- a3: full layers
         if constexpr (NFULL == 2) {
-            if constexpr (FCSTAGE)
+            TR_RB(3, 0);
+            TR_RB(3, 1);  // FC1's delta_in reuses chunks staged now and re-fetches the others later
+            if constexpr (FCSTAGE && MODE == kTrace)
+                fc_fwd3<F1, G, NT, FRCH, MODE>(P + O::f1w, P + O::f1b, alast, hh, F1::OUT, cnt, wb, L4, L5, sS, &a,
+                                               slot, O::f1w);
+            else if constexpr (FCSTAGE)
                 fc_fwd3<F1, G, NT, FRCH>(P + O::f1w, P + O::f1b, alast, hh, F1::OUT, cnt, wb, L4, L5, sS);
             else if constexpr (F1::IN % 4 == 0)
                 fc_fwd2<F1, G, NT, (NT > 512 || BIG ? 2 : 4)>(P + O::f1w, P + O::f1b, alast, hh, F1::OUT, cnt);
@@ -2316,16 +2329,25 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 fc_fwd<F1, G, NT>(P + O::f1w, P + O::f1b, alast, hh, F1::OUT, cnt);
             __syncthreads();
             PTIME(16);
-            fc_fwd<F2, G, NT>(P + O::f2w, P + O::f2b, hh, zz, kZStride, cnt);
+            TR_RE(3, 0);
+            TR_RB(4, 0);
+            if constexpr (MODE == kTrace)
+                fc_fwd<F2, G, NT, false, true>(P + O::f2w, P + O::f2b, hh, zz, kZStride, cnt,
+                                               a.tw + static_cast<long long>(slot) * 2 * a.pstride + O::f2w);
+            else
+                fc_fwd<F2, G, NT>(P + O::f2w, P + O::f2b, hh, zz, kZStride, cnt);
         } else {
             if constexpr (S::FWB > 0) {
                 L1.wait();
+                TR_RE(1, 0);
+                TR_DUMP(0, O::f1w, fwb, S::FWB);
                 fc_fwd<F1, G, NT, true>(fwb, fwb + F1::WFL, alast, zz, kZStride, cnt);
             } else {
                 fc_fwd<F1, G, NT>(P + O::f1w, P + O::f1b, alast, zz, kZStride, cnt);
             }
         }
         __syncthreads();
+        if constexpr (NFULL == 2) TR_RE(4, 0);
         PTIME(5);
         // ---------------- a4: softmax cross-entropy, output delta
         if (threadIdx.x < cnt) {
@@ -2360,7 +2382,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
         if constexpr (TRAIN) {
             __syncthreads();
             PTIME(6);
-            if constexpr (MODE == kHogwild)  // the claim's round trip overlaps the backward pass
+            if constexpr (is_hog(MODE))  // the claim's round trip overlaps the backward pass
                 if (threadIdx.x == 0) {
                     next_claim = static_cast<long long>(atomicAdd(a.counter, static_cast<unsigned long long>(G)));
                     if (pending_progress && a.progress)
@@ -2374,8 +2396,12 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             }
             // ---------------- a5: full layers backward, one bulk publish per chunk / layer
             if constexpr (NFULL == 2) {
+                TR_RB(4, 1);
+                TR_PB(4);
                 fc_bwd<F2, G, NT, MODE, SHALF>(a, slot, O::f2w, O::f2b, hh, zz, kZStride, sS, bsc, cnt, sc);
                 wait_publish_reads();
+                TR_RE(4, 1);
+                TR_PE(4);
                 PTIME(7);
                 if constexpr (BIG) {
                     constexpr int NRG = NT / (F1::IN / 4) < 4 ? NT / (F1::IN / 4) : 4;
@@ -2386,6 +2412,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                     static_assert((NRG - 1) * G * F1::IN <= S::SFL, "row-group partials must fit in S");
                     fence_async_smem();
                     wait_publish_reads();  // the FC2 publish has read its buffers; WB is free
+                    TR_PB(3);
                     fc_bwd3<F1, G, NT, MODE, NRG, FRCH, true>(a, slot, O::f1w, O::f1b, alast, hh, F1::OUT, sS, bsc,
                                                                cnt, sc, wb, L4, L5);
                 } else if constexpr (F1::IN % 4 == 0 && (F1::IN / 4) * 4 <= NT) {
@@ -2399,13 +2426,19 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 // tiny: the gradient chunk goes to S's upper half, so the images in its lower half
                 // survive for conv1's gradient (no reload, no wait for the publish's reads here)
                 static_assert(F1::WFL <= SHALF && G * IMG <= SHALF, "one chunk above the images");
+                TR_PB(1);
                 fc_bwd<F1, G, NT, MODE, SHALF>(a, slot, O::f1w, O::f1b, alast, zz, kZStride, sS + SHALF, bsc, cnt,
                                                sc, fwb);
                 __syncthreads();
+                TR_PE(1);
             } else {
                 fc_bwd<F1, G, NT, MODE, SHALF>(a, slot, O::f1w, O::f1b, alast, zz, kZStride, sS, bsc, cnt, sc);
             }
             if constexpr (S::FWB == 0) wait_publish_reads();
+            if constexpr (NFULL == 2) {
+                TR_RE(3, 1);
+                TR_PE(3);
+            }
             PTIME(8);
             // ---------------- a6/a7: pool + conv backward, publish per layer
             if constexpr (NCONV == 3 && BIG) {
@@ -2452,9 +2485,13 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                     // layer 3 yet, so for one worker it is the snapshot the forward used (R5)
                     fence_async_smem();
                     __syncthreads();
+                    TR_RB(2, 1);
                     L2.issue(wb, P + O::c3w, C3::BLK);
                     L2.wait();
+                    TR_RE(2, 1);
+                    TR_DUMP(1, O::c3w, wb, C3::BLK);
                 }
+                TR_PB(2);
                 // otherwise W3 is still staged from the forward pass (the exact snapshot it used)
                 if constexpr (C3::GWIN > 0) {
                     // delta_in (latency-bound, one warp per (image, 32 maps)) and the dense
@@ -2474,7 +2511,10 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                         const long long t_split = clock64();  // slots 17 / 18: the two warp groups' own time
 #endif
                         if (threadIdx.x < DW * 32) {
-                            conv_din_win<C3, NT, true>(wb, a3, am3, a2, sS, cnt, dq4);  // output over dq4 after
+                            if constexpr (CHAOS_C3_DINP)
+                                conv_din_winp<C3, NT, true>(wb, a2, sS, cnt, dq4);  // output over dq4 after
+                            else
+                                conv_din_win<C3, NT, true>(wb, a3, am3, a2, sS, cnt, dq4);  // output over dq4 after
 #ifdef CHAOS_TIMING
                             if (threadIdx.x == 0 && a.ptime) a.ptime[blockIdx.x * kPhases + 17] += clock64() - t_split;
 #endif
@@ -2488,10 +2528,8 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                         }
                     } else {
                         if (threadIdx.x < DW * 32) {
-                            if constexpr (C3::DWIN)
-                                conv_din_win<C3, NT>(wb, a3, am3, a2, sS, cnt);
-                            else
-                                conv_din2<C3, NT>(wb, a3, am3, a2, sS, nullptr, cnt);
+                            static_assert(C3::DWIN, "conv3 delta_in beside the dense weight gradient: conv_din_win");
+                            conv_din_win<C3, NT>(wb, a3, am3, a2, sS, cnt);
                         }
                         conv_gw_win<C3, NT, MODE, C3::GWIN, DW, NT / 32 - DW>(a, slot, a2, a3, am3, O::c3w, cnt, sc);
                     }
@@ -2500,24 +2538,52 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 } else {
                 if constexpr (C3::DIN3)
                     conv_din3<C3, NT>(wb, a3, am3, a2, sS, nullptr, cnt);  // delta for the pool2 outputs -> S
-                else if constexpr (C3::PB > 0)
-                    conv_din2<C3, NT>(wb, a3, am3, a2, sS, nullptr, cnt);
                 else
                     conv_din<C3, NT>(wb, a3, am3, a2, sS, cnt);
                 __syncthreads();
                 PTIME(9);
-                if constexpr (C3::GWMMA)
-                    conv_gw_mma<C3, NT, MODE>(a, slot, a2, a3, am3, wb, O::c3w, cnt, sc);
-                else
-                    conv_gw<C3, NT, MODE, true>(a, slot, a2, a3, am3, wb, O::c3w, cnt, sc);
+                conv_gw<C3, NT, MODE, true>(a, slot, a2, a3, am3, wb, O::c3w, cnt, sc);
                 }
                 fence_async_smem();
                 wait_publish_reads();
+                TR_PE(2);
                 PTIME(10);
+                TR_RB(1, 1);
                 L1.issue(wb, P + O::c2w, C2::BLK);  // W2 again (pre-update snapshot for delta_in)
                 L1.wait();
+                TR_RE(1, 1);
+                TR_DUMP(1, O::c2w, wb, C2::BLK);
+                if constexpr (C2_WTP > 0) {
+                    // transposed copy [m][C*K*K] (odd pitch) for the delta_in's lanes over input maps;
+                    // ordered before its reads by the barrier after the weight gradient
+                    static_assert(round4(C2::BLK) + C2::M * C2_WTP <= S::WBUF, "transposed W2 must fit in WB");
+                    float* wbt = wb + round4(C2::BLK);
+                    for (int e = threadIdx.x; e < C2::ROWS * C2::M; e += NT)
+                        wbt[(e % C2::M) * C2_WTP + e / C2::M] = wb[(e / C2::M) * C2::MP + e % C2::M];
+                }
                 PTIME(11);
-                if constexpr (C2::GWIN > 0) {
+                TR_PB(1);
+                if constexpr (CHAOS_C2_PAR && C2::MS < 0 && CHAOS_C2_GWM > 0 && C2::NBAND > 1 && C2::GWIN == 0) {
+                    // delta_in (one warp per (image, band), latency-bound) and the weight gradient
+                    // (LSU-bound, lanes over output maps) side by side; the delta_in's writes over a1
+                    // wait for its hand-off barrier, which the gradient warps join once done reading a1
+                    constexpr int DW = G * C2::NBAND * ((C2::C + 31) / 32);
+                    static_assert(C2::DIN3 && DW < NT / 32, "conv2 split");
+                    static_assert(G * C2::HAND <= S::Z - S::A2, "conv2 hand-off must fit in the dead A2/A3/HH regions");
+                    if (threadIdx.x < DW * 32) {
+                        if constexpr (C2_WTP > 0)
+                            conv_din3<C2, NT, true, C2_WTP>(wb + round4(C2::BLK), sS, am2, a1, a1, a2, cnt);
+                        else
+                            conv_din3<C2, NT, true>(wb, sS, am2, a1, a1, a2, cnt);
+                    } else {
+                        conv_gw_m<C2, NT, MODE, CHAOS_C2_GWM, DW, NT / 32 - DW>(a, slot, a1, sS, am2, O::c2w, cnt, sc);
+                        __syncthreads();  // pairs with conv_din3's hand-off barrier
+                    }
+                    __syncthreads();
+                    TR_PE(1);
+                    PTIME(12);
+                    PTIME(13);
+                } else if constexpr (C2::GWIN > 0) {
                     // delta_in (din3: one warp per (image, band), latency-bound) and the dense
                     // weight gradient (issue-bound, published from registers) side by side; the
                     // delta_in writes over a1 wait for its hand-off barrier, by which time the
@@ -2535,21 +2601,22 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                     PTIME(12);
                     PTIME(13);
                 } else {
-                if constexpr (C2::GWMMA)
-                    conv_gw_mma<C2, NT, MODE>(a, slot, a1, sS, am2, wb + C2::BLK, O::c2w, cnt, sc);
+                if constexpr (C2::MS < 0 && CHAOS_C2_GWM > 0)  // lanes over output maps, NPT input maps per thread
+                    conv_gw_m<C2, NT, MODE, CHAOS_C2_GWM>(a, slot, a1, sS, am2, O::c2w, cnt, sc);
                 else if constexpr (C2::MS < 0)  // generic, lanes over output maps, published from registers
                     conv_gw<C2, NT, MODE, false>(a, slot, a1, sS, am2, nullptr, O::c2w, cnt, sc);
                 else
                     conv_gw<C2, NT, MODE, true>(a, slot, a1, sS, am2, wb + C2::BLK, O::c2w, cnt, sc);
                 __syncthreads();
+                TR_PE(1);
                 PTIME(12);
                 if constexpr (C2::PB > 0) {
                     static_assert(G * C2::HAND <= S::A3 - S::A2 + (S::HH - S::A3) + (S::Z - S::HH),
                                   "conv2 hand-off must fit in the dead A2/A3/HH regions");
-                    if constexpr (C2::DIN3)
-                        conv_din3<C2, NT>(wb, sS, am2, a1, a1, a2, cnt);  // a2..HH are dead here
+                    if constexpr (C2::DIN3 && C2_WTP > 0)
+                        conv_din3<C2, NT, false, C2_WTP>(wb + round4(C2::BLK), sS, am2, a1, a1, a2, cnt);
                     else
-                        conv_din2<C2, NT>(wb, sS, am2, a1, a1, a2, cnt);
+                        conv_din3<C2, NT>(wb, sS, am2, a1, a1, a2, cnt);  // a2..HH are dead here
                 } else {
                     conv_din<C2, NT>(wb, sS, am2, a1, a1, cnt);
                 }
@@ -2581,19 +2648,21 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 }
             }
             PTIME(14);
+            TR_PB(0);
             conv_gw<C1, NT, MODE, true>(a, slot, sS, a1, am1, wb, O::c1w, cnt, sc);
             if (threadIdx.x == 0) bulk_wait_all<0>();  // publishes complete before the next claim
+            TR_PE(0);
 #ifndef CHAOS_NO_ITER_FENCE
-            if constexpr (MODE == kHogwild) __threadfence();  // this worker's REDs precede its next reads
+            if constexpr (is_hog(MODE)) __threadfence();  // this worker's REDs precede its next reads
 #endif
-            if constexpr (MODE == kHogwild)  // progress for the asynchronous cross-GPU averaging: the
+            if constexpr (is_hog(MODE))  // progress for the asynchronous cross-GPU averaging: the
                 pending_progress = cnt;     // reduction is issued during the next iteration (off the fences)
         }
         __syncthreads();
         PTIME(15);
     }
     if (threadIdx.x == 0) bulk_wait_all<0>();
-    if constexpr (MODE == kHogwild)
+    if constexpr (is_hog(MODE))
         if (threadIdx.x == 0 && pending_progress && a.progress)
             atomicAdd(a.progress, static_cast<unsigned long long>(pending_progress));
 }

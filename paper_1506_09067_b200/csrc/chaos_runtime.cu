@@ -34,6 +34,7 @@ namespace {
 #endif
 struct TinyNet {  // configs[0], configs[1]: conv5 4x4 -> tanh -> pool2 -> FC 845->10
     static constexpr int NCONV = 1, NFULL = 1, GDEF = 4, GINIT = 1, INFLIGHT = 148, NT = TINY_NT, SFL = 2 * 8456;
+    static constexpr bool TRACE = true;  // kTrace instantiated (hogwild schedule recording)
 #ifndef TINY_C1_GS  // tile sweeps: -DTINY_C1_GS=.. -DTINY_C1_TT=..
 #define TINY_C1_GS 16
 #endif
@@ -51,6 +52,7 @@ struct TinyNet {  // configs[0], configs[1]: conv5 4x4 -> tanh -> pool2 -> FC 84
 #endif
 struct MediumNet {  // configs[2] = Table I medium
     static constexpr int NCONV = 2, NFULL = 2, GDEF = 4, GINIT = 4, INFLIGHT = 592, NT = MEDIUM_NT, SFL = 6000;
+    static constexpr bool TRACE = false;
 #ifndef MEDIUM_DINSPLIT
 #define MEDIUM_DINSPLIT 4
 #endif
@@ -73,6 +75,7 @@ struct MediumNet {  // configs[2] = Table I medium
 struct PaperSmallNet {  // Table I small: conv5 4x4 -> pool2 -> conv10 5x5 -> pool3
                         // -> FC 90->50 tanh -> FC 50->10; same generic kernels as the medium net
     static constexpr int NCONV = 2, NFULL = 2, GDEF = 4, GINIT = 1, INFLIGHT = 148, NT = PSMALL_NT, SFL = 3364;
+    static constexpr bool TRACE = false;
 #ifndef PSMALL_DINSPLIT
 #define PSMALL_DINSPLIT 2
 #endif
@@ -88,7 +91,8 @@ struct LargeNet {  // configs[3], configs[4]
     // (3 maps, 32 input maps) in its weight gradient; conv3's backward split over warps 0-7
     // (delta_in) and 8-19 (weight gradient).  Tile sweeps: profiles/r1q.
     static constexpr int NCONV = 3, NFULL = 2, GDEF = 4, GINIT = 4, INFLIGHT = 592, NT = 640, SFL = 6400;
-    //                C   H   W   M   K  KP  MT  TT  GS  RB  PB  MS  GWMMA  DIN3  GWIN  DWIN  NSPL
+    static constexpr bool TRACE = true;
+    //                C   H   W   M   K  KP  MT  TT  GS  RB  PB  MS  (0)  DIN3  GWIN  DWIN  NSPL
 #ifndef LARGE_C1_MT  // tile sweeps (scripts): -DLARGE_C1_MT=.. -DLARGE_C1_GS=..
 #define LARGE_C1_MT 10
 #endif
@@ -96,7 +100,10 @@ struct LargeNet {  // configs[3], configs[4]
 #define LARGE_C1_GS 16
 #endif
     using C1 = Conv<1, 29, 29, 20, 4, 2, LARGE_C1_MT, 16, LARGE_C1_GS, 2>;
-    using C2 = Conv<20, 13, 13, 60, 3, 2, 10, 9, 1, 4, 1, -1, false, true, 0, false, 1>;
+#ifndef LARGE_C2_PB  // conv2 delta_in: window rows per band task
+#define LARGE_C2_PB 1
+#endif
+    using C2 = Conv<20, 13, 13, 60, 3, 2, 10, 9, 1, 4, LARGE_C2_PB, -1, false, true, 0, false, 1>;
     using C3 = Conv<60, 5, 5, 100, 2, 2, 4, 4, 1, 5, 2, 0, false, false, 4, true, 1>;
     using F1 = Full<400, 150, true>;
     using F2 = Full<150, 10, false>;
@@ -110,8 +117,9 @@ struct PaperLargeNet {  // Table I large: conv
 #define PL_RB3 4
 #endif
     static constexpr int NCONV = 3, NFULL = 2, GDEF = 1, GINIT = 1, INFLIGHT = 148, NT = 384, SFL = 1800, RB3 = PL_RB3;
+    static constexpr bool TRACE = false;
     static constexpr bool BIGW = true;
-    //                C   H   W    M  K  KP  MT  TT  GS  RB  PB  MS  GWMMA  DIN3  GWIN  DWIN  NSPL
+    //                C   H   W    M  K  KP  MT  TT  GS  RB  PB  MS  (0)  DIN3  GWIN  DWIN  NSPL
     using C1 = Conv<1, 29, 29, 20, 4, 1, 10, 16, 16, 1>;
     using C2 = Conv<20, 26, 26, 60, 5, 2, 10, 25, 1, 2>;
     using C3 = Conv<60, 11, 11, 100, 6, 2, 4, 12, 1, 2>;
@@ -143,7 +151,7 @@ struct NetDesc {
     int gdef = 1, ginit = 1, nt = 256;
     int max_inflight = 1 << 30;  // hogwild staleness cap: #CTAs x G
     // [gi][mode]: gi 0 -> G=1, gi 1 -> G=gdef
-    KernelFn fn[2][4] = {};
+    KernelFn fn[2][5] = {};  // [gi][mode]; kTrace only for nets with trace points (else nullptr)
     KernelFn fn_gated[2] = {};  // hogwild from host buffers (claims gated by the landed counter)
     int smem[2] = {0, 0};
     double flops_per_sample = 0;  // algorithmic
@@ -190,16 +198,11 @@ void fill_kernels(NetDesc& d, int gi) {
     d.fn[gi][kSync] = chaos_worker<Net, G, Net::NT, kSync>;
     d.fn[gi][kEval] = chaos_worker<Net, G, Net::NT, kEval>;
     d.fn[gi][kForward] = chaos_worker<Net, G, Net::NT, kForward>;
+    if constexpr (Net::TRACE) d.fn[gi][kTrace] = chaos_worker<Net, G, Net::NT, kTrace>;
     d.fn_gated[gi] = chaos_worker<Net, G, Net::NT, kHogwild, true>;
     d.smem[gi] = SLayout<Net, G>::BYTES;
 }
 
-template <class L>
-double conv_flops() {  // forward on needed outputs + argmax-only gW (+ delta_in) + update
-    const double fwd = 2.0 * L::M * L::P * L::KP * L::KP * L::C * L::KK;
-    const double gw = 2.0 * L::M * L::P * L::C * L::KK;
-    return fwd + gw;
-}
 
 template <class Net>
 NetDesc make_desc(const char* name, std::vector<LayerSig> sig) {
@@ -288,6 +291,7 @@ struct NcclApi {
     std::string why;
     ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
     ncclResult_t (*init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*init_rank_config)(ncclComm_t*, int, ncclUniqueId, int, ncclConfig_t*) = nullptr;  // optional
     ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                                cudaStream_t) = nullptr;
     ncclResult_t (*destroy)(ncclComm_t) = nullptr;
@@ -304,6 +308,7 @@ const NcclApi& nccl_api() {
         }
         a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
         a.init_rank = reinterpret_cast<decltype(a.init_rank)>(dlsym(h, "ncclCommInitRank"));
+        a.init_rank_config = reinterpret_cast<decltype(a.init_rank_config)>(dlsym(h, "ncclCommInitRankConfig"));
         a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
         a.destroy = reinterpret_cast<decltype(a.destroy)>(dlsym(h, "ncclCommDestroy"));
         a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
@@ -344,10 +349,20 @@ struct chaos_net {
     int reserve_sms = 0;                   // hogwild: SMs left free of training CTAs
     unsigned long long* progress = nullptr;  // device: images published by hogwild launches (monotonic)
     unsigned long long progress_enqueued = 0; // host: images enqueued to hogwild launches
-    int occ[2][4] = {};
+    int occ[2][5] = {};
+    int debug_trace = 0;                   // CHAOS_OPT_DEBUG_TRACE: hogwild epochs record their schedule
+    long long debug_stagger = 0;           // CHAOS_OPT_DEBUG_STAGGER: cycles per CTA index
+    unsigned long long* tctr = nullptr;    // kTrace event counters (2)
+    long long* trec = nullptr;             // kTrace records [groups][kTraceRec]
+    float* tw = nullptr;                   // kTrace: weights each group read [groups][2][pint]
+    long long tw_cap = 0;
+    long long trec_cap = 0;
+    long long trace_groups = 0;            // groups of the last traced epoch
+    int trace_g = 1;                       // ... and their size G
     unsigned long long* ptime = nullptr;  // CHAOS_TIMING builds only
     int ptime_grid = 0;
     ncclComm_t comm = nullptr;             // chaos_dist_init (library-owned communicator)
+    int comm_max_ctas = 0;                 // its CTA cap (the reserved SMs at init; 0 = uncapped)
     int comm_world = 0;
     cudaStream_t copy_stream = nullptr;    // chaos_train_epoch_host: H2D chunks overlap training
     unsigned long long* ready = nullptr;       // device: images landed (hogwild host entry)
@@ -356,6 +371,8 @@ struct chaos_net {
     const unsigned long long* launch_ready = nullptr;  // set around the host entry's single launch
     std::vector<cudaEvent_t> chunk_ev;
     cudaEvent_t staging_free = nullptr;
+    cudaEvent_t ready_copied = nullptr;  // recorded after a hogwild host epoch's last ready_host copy
+    bool ready_pending = false;          // ... whose copies may still be reading ready_host
 };
 
 namespace {
@@ -366,8 +383,9 @@ chaos_status ensure_kernel_attrs(chaos_net* net) {
     for (int gi = 0; gi < 2; ++gi) {
         CUDA_TRY(cudaFuncSetAttribute(net->d->fn_gated[gi], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       net->d->smem[gi]));
-        for (int m = 0; m < 4; ++m) {
+        for (int m = 0; m < 5; ++m) {
             KernelFn f = net->d->fn[gi][m];
+            if (!f) continue;
             CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, net->d->smem[gi]));
             int occ = 0;
             CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, net->d->nt, net->d->smem[gi]));
@@ -570,7 +588,7 @@ chaos_net* chaos_net_create(const chaos_arch* arch) {
     if (validate(arch) != CHAOS_OK) return nullptr;
     const NetDesc* d = match(arch);
     if (!d) {
-        fail(CHAOS_E_UNSUPPORTED, "valid arch without a compiled sm_100a instantiation (compiled: tiny, medium, large, paper_small)");
+        fail(CHAOS_E_UNSUPPORTED, "valid arch without a compiled sm_100a instantiation (compiled: tiny, medium, large, paper_small, paper_large)");
         return nullptr;
     }
     chaos_net* net = new chaos_net();
@@ -632,6 +650,10 @@ void chaos_net_destroy(chaos_net* net) {
     if (net->ready_host) cudaFreeHost(net->ready_host);
     if (net->ready) cudaFree(net->ready);
     if (net->staging_free) cudaEventDestroy(net->staging_free);
+    if (net->tctr) cudaFree(net->tctr);
+    if (net->trec) cudaFree(net->trec);
+    if (net->tw) cudaFree(net->tw);
+    if (net->ready_copied) cudaEventDestroy(net->ready_copied);
     for (cudaEvent_t e : net->chunk_ev) cudaEventDestroy(e);
     void* ptrs[] = {net->params, net->latch,  net->counter, net->loss_sum, net->partial, net->grad_out, net->claims,
                     net->ev_loss, net->ev_wrong, net->ev_sum, net->ev_err, net->st_x, net->st_y, net->ptime,
@@ -663,8 +685,22 @@ chaos_status chaos_net_set_option(chaos_net* net, chaos_option opt, int64_t valu
         case CHAOS_OPT_DEBUG_CLAIMS:
             net->debug_claims = value ? 1 : 0;
             return CHAOS_OK;
+        case CHAOS_OPT_DEBUG_TRACE:
+            if (value && !net->d->fn[0][kTrace])
+                return fail(CHAOS_E_UNSUPPORTED, "net %s has no schedule-recording (trace) build", net->d->name);
+            net->debug_trace = value ? 1 : 0;
+            return CHAOS_OK;
+        case CHAOS_OPT_DEBUG_STAGGER:
+            if (value < 0) return fail(CHAOS_E_INVALID, "stagger must be >= 0");
+            net->debug_stagger = value;
+            return CHAOS_OK;
         case CHAOS_OPT_RESERVE_SMS:
             if (value < 0 || value >= net->sms) return fail(CHAOS_E_INVALID, "reserve_sms must be in [0, %d)", net->sms);
+            if (net->comm && value > 0 && (net->comm_max_ctas == 0 || net->comm_max_ctas > value))
+                return fail(CHAOS_E_INVALID,
+                            "the communicator was created with %d CTAs (0 = uncapped): set reserve_sms before "
+                            "chaos_dist_init so collectives fit beside the persistent kernel",
+                            net->comm_max_ctas);
             net->reserve_sms = (int)value;
             return CHAOS_OK;
     }
@@ -679,6 +715,8 @@ int64_t chaos_net_get_option(const chaos_net* net, chaos_option opt) {
         case CHAOS_OPT_GROUP: return net->group;
         case CHAOS_OPT_MAX_CTAS: return net->max_ctas;
         case CHAOS_OPT_DEBUG_CLAIMS: return net->debug_claims;
+        case CHAOS_OPT_DEBUG_TRACE: return net->debug_trace;
+        case CHAOS_OPT_DEBUG_STAGGER: return net->debug_stagger;
         case CHAOS_OPT_RESERVE_SMS: return net->reserve_sms;
     }
     return -1;
@@ -749,6 +787,39 @@ chaos_status train_range(chaos_net* net, const float* d_images, const int32_t* d
         k.ready = net->launch_ready;
         net->progress_enqueued += (unsigned long long)n;
         KernelFn fn = k.ready ? net->d->fn_gated[gidx(net)] : net->d->fn[gidx(net)][kHogwild];
+        if (net->debug_trace) {  // the schedule-recording instantiation (debug): records + per-group publishes
+            if (k.ready) return fail(CHAOS_E_UNSUPPORTED, "trace recording is for device-buffer epochs");
+            const long long groups = (n + G - 1) / G;
+            chaos_status st = ensure_partial(net, groups);
+            if (st) return st;
+            CUDA_TRY(cudaMemsetAsync(net->partial, 0, sizeof(float) * (size_t)groups * (size_t)net->d->pint, net->stream));
+            if (!net->tctr) CUDA_TRY(cudaMalloc(&net->tctr, 2 * sizeof(unsigned long long)));
+            if (net->trec_cap < groups) {
+                if (net->trec) cudaFree(net->trec);
+                net->trec = nullptr;
+                CUDA_TRY(cudaMalloc(&net->trec, sizeof(long long) * kTraceRec * (size_t)groups));
+                net->trec_cap = groups;
+            }
+            if (net->tw_cap < groups) {
+                if (net->tw) cudaFree(net->tw);
+                net->tw = nullptr;
+                CUDA_TRY(cudaMalloc(&net->tw, sizeof(float) * 2 * (size_t)net->d->pint * (size_t)groups));
+                net->tw_cap = groups;
+            }
+            // NaN: a value no read recorded (the delta_in read of a layer that reuses its forward copy)
+            CUDA_TRY(cudaMemsetAsync(net->tw, 0xff, sizeof(float) * 2 * (size_t)net->d->pint * (size_t)groups,
+                                     net->stream));
+            CUDA_TRY(cudaMemsetAsync(net->tctr, 0, 2 * sizeof(unsigned long long), net->stream));
+            CUDA_TRY(cudaMemsetAsync(net->trec, 0xff, sizeof(long long) * kTraceRec * (size_t)groups, net->stream));
+            k.partial = net->partial;
+            k.tctr = net->tctr;
+            k.trec = net->trec;
+            k.stagger = net->debug_stagger;
+            k.tw = net->tw;
+            net->trace_groups = groups;
+            net->trace_g = G;
+            fn = net->d->fn[gidx(net)][kTrace];
+        }
         fn<<<grid, net->d->nt, net->d->smem[gidx(net)], net->stream>>>(k);
         CUDA_TRY(cudaGetLastError());
         return CHAOS_OK;
@@ -830,6 +901,13 @@ chaos_status host_epoch(chaos_net* net, const float* h_images, const int32_t* h_
         if (chunk < 2048) chunk = 2048;
         const long long nch = (n + chunk - 1) / chunk;
         if (!net->ready) CUDA_TRY(cudaMalloc(&net->ready, sizeof(unsigned long long)));
+        if (!net->ready_copied) CUDA_TRY(cudaEventCreateWithFlags(&net->ready_copied, cudaEventDisableTiming));
+        // the previous host epoch's copies (async entry) may still be queued to read ready_host:
+        // wait for them before the host rewrites (or frees) it
+        if (net->ready_pending) {
+            CUDA_TRY(cudaEventSynchronize(net->ready_copied));
+            net->ready_pending = false;
+        }
         if (net->ready_cap < nch) {
             if (net->ready_host) cudaFreeHost(net->ready_host);
             net->ready_host = nullptr;
@@ -854,6 +932,8 @@ chaos_status host_epoch(chaos_net* net, const float* h_images, const int32_t* h_
             CUDA_TRY(cudaMemcpyAsync(net->ready, net->ready_host + c, sizeof(unsigned long long),
                                      cudaMemcpyHostToDevice, net->copy_stream));
         }
+        CUDA_TRY(cudaEventRecord(net->ready_copied, net->copy_stream));
+        net->ready_pending = true;
         net->launch_ready = net->ready;
         chaos_status st = train_range(net, net->st_x, net->st_y, n, lr, mode);
         net->launch_ready = nullptr;
@@ -1046,11 +1126,29 @@ chaos_status chaos_dist_init(chaos_net* net, const void* host_id, int32_t rank, 
     CUDA_TRY(cudaSetDevice(net->dev));
     ncclUniqueId id;
     std::memcpy(&id, host_id, sizeof id);
-    const ncclResult_t r = n.init_rank(&net->comm, world, id, rank);
+    ncclResult_t r;
+    if (net->reserve_sms > 0) {
+        // in-flight averaging beside a persistent hogwild launch: every block of a
+        // collective must be co-resident on the reserved SMs, else a block spinning on a peer's
+        // block that cannot be scheduled never finishes -- cap the communicator's CTAs (ring /
+        // tree and NVLS) at the reserved SM count
+        if (!n.init_rank_config)
+            return fail(CHAOS_E_NCCL, "CHAOS_OPT_RESERVE_SMS needs ncclCommInitRankConfig (NCCL >= 2.14)");
+        ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+        cfg.blocking = 1;
+        cfg.minCTAs = 1;
+        cfg.maxCTAs = net->reserve_sms;
+        cfg.nvlsCTAs = net->reserve_sms;
+        cfg.collnetEnable = 0;
+        r = n.init_rank_config(&net->comm, world, id, rank, &cfg);
+    } else {
+        r = n.init_rank(&net->comm, world, id, rank);
+    }
     if (r != ncclSuccess) {
         net->comm = nullptr;
         return fail(CHAOS_E_NCCL, "ncclCommInitRank: %s", n.error_string(r));
     }
+    net->comm_max_ctas = net->reserve_sms;
     net->comm_world = world;
     return CHAOS_OK;
 }
@@ -1069,6 +1167,35 @@ chaos_status chaos_dist_average_buffer(chaos_net* net, float* d_buf, int64_t n, 
 chaos_status chaos_dist_average(chaos_net* net) {
     if (!net) return fail(CHAOS_E_INVALID, "net is NULL");
     return chaos_dist_average_buffer(net, net->params, net->d->pint, reinterpret_cast<int64_t>(net->stream));
+}
+
+chaos_status chaos_debug_trace(chaos_net* net, int64_t* host_records, int64_t n_groups, float* host_pubs,
+                               float* host_reads) {
+    if (!net || !host_records) return fail(CHAOS_E_INVALID, "NULL argument");
+    if (!net->trec || n_groups != net->trace_groups)
+        return fail(CHAOS_E_INVALID, "no trace of %lld groups recorded (last: %lld)", (long long)n_groups,
+                    net->trace_groups);
+    CUDA_TRY(cudaMemcpyAsync(host_records, net->trec, sizeof(long long) * kTraceRec * (size_t)n_groups,
+                             cudaMemcpyDeviceToHost, net->stream));
+    std::vector<float> slots;
+    if (host_pubs) {
+        slots.resize((size_t)n_groups * (size_t)net->d->pint);
+        CUDA_TRY(cudaMemcpyAsync(slots.data(), net->partial, sizeof(float) * slots.size(), cudaMemcpyDeviceToHost,
+                                 net->stream));
+    }
+    std::vector<float> rd;
+    if (host_reads) {
+        rd.resize((size_t)n_groups * 2 * (size_t)net->d->pint);
+        CUDA_TRY(cudaMemcpyAsync(rd.data(), net->tw, sizeof(float) * rd.size(), cudaMemcpyDeviceToHost, net->stream));
+    }
+    CUDA_TRY(cudaStreamSynchronize(net->stream));
+    if (host_pubs)
+        for (long long k = 0; k < n_groups; ++k)
+            to_normative(*net->d, slots.data() + k * net->d->pint, host_pubs + k * net->d->nparams);
+    if (host_reads)
+        for (long long k = 0; k < 2 * n_groups; ++k)
+            to_normative(*net->d, rd.data() + k * net->d->pint, host_reads + k * net->d->nparams);
+    return check_latch(net);
 }
 
 chaos_status chaos_debug_claims(chaos_net* net, int32_t* host_counts, int64_t n) {

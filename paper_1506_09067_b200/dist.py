@@ -62,6 +62,26 @@ def average_(tensor, world: int, group=None, force: bool = False):
     return tensor
 
 
+def check_async_comm(comm: str, net) -> None:
+    """The in-flight averages run beside a persistent hogwild launch that holds every other SM:
+    all blocks of each collective must be co-resident on the reserved SMs, else one can spin on a
+    peer block that is never scheduled.  comm "chaos": chaos_dist_init caps the communicator at
+    the reserved SMs (ncclCommInitRankConfig maxCTAs / nvlsCTAs).  comm "torch": NCCL reads
+    NCCL_MAX_CTAS / NCCL_NVLS_ENABLE when the process group is created -- they must have been set
+    to at most the reserved SMs / 0 (bench.py does); raise otherwise instead of risking a hang."""
+    from .chaos import OPT_RESERVE_SMS
+    reserve = net.get_option(OPT_RESERVE_SMS)
+    if reserve < 1:
+        raise RuntimeError("asynchronous averaging needs CHAOS_OPT_RESERVE_SMS >= 1 (SMs for the collectives)")
+    if comm == "torch":
+        import os
+        cap = os.environ.get("NCCL_MAX_CTAS")
+        if cap is None or not cap.isdigit() or int(cap) > reserve or os.environ.get("NCCL_NVLS_ENABLE") != "0":
+            raise RuntimeError(f"asynchronous averaging over torch.distributed needs NCCL_MAX_CTAS <= {reserve} "
+                               "(the reserved SMs) and NCCL_NVLS_ENABLE=0 set before the process group is "
+                               "created; or use comm='chaos', whose communicator the library caps itself")
+
+
 class DistTrainer:
     """Trains one replica per rank with periodic averaging (hogwild), or all ranks as one
     deterministic sync-SGD trainer (``sync_epoch``).
@@ -118,6 +138,17 @@ class DistTrainer:
             self._agreed_cache[key] = int(t.item())
         return self._agreed_cache[key]
 
+    def _on_net_stream(self, t):
+        """Collectives on the tensors the training kernels write go on the net's stream (a
+        Net(stream=s) need not be torch's current stream), so they are ordered after the launches
+        and before the next ones."""
+        import contextlib
+
+        import torch
+        if getattr(t, "is_cuda", False) and getattr(self.net, "stream", None) is not None:
+            return torch.cuda.stream(self.net.stream)
+        return contextlib.nullcontext()
+
     def epoch(self, images, labels, lr: float, lo: int = 0, hi: int | None = None):
         """One Training phase over this rank's images[lo:hi) (already sharded by the caller):
         one launch per interval of K images, each followed by a blocking average.  Every rank runs
@@ -131,7 +162,8 @@ class DistTrainer:
                 self.net.train_epoch(images[lo:hi], labels[lo:hi], lr)
                 self.n_launches += 1
             if multi:
-                self._average(params)
+                with self._on_net_stream(params):
+                    self._average(params)
                 self.n_collectives += 1
             return
         count = max(1, -(-self._agreed(hi - lo, "max") // self.k))
@@ -140,7 +172,8 @@ class DistTrainer:
             if e > s:
                 self.net.train_epoch(images[s:e], labels[s:e], lr)
                 self.n_launches += 1
-            self._average(params)
+            with self._on_net_stream(params):
+                self._average(params)
             self.n_collectives += 1
 
     def _launch(self, images, labels, lr, lo, hi, host, chunks):
@@ -205,6 +238,8 @@ class DistTrainer:
             self._launch(images, labels, lr, lo, hi, host, chunks)
             return
         cuda = params.is_cuda
+        if cuda:
+            check_async_comm(self.comm, net)
         if getattr(self, "_async_bufs", None) is None:
             self._async_bufs = (torch.empty_like(params), torch.empty_like(params),
                                 torch.cuda.Stream() if cuda else None)
@@ -252,7 +287,8 @@ class DistTrainer:
             self.net.batch_gradient(images[s:e], labels[s:e], grad)
             self.n_launches += 2
             if self.world > 1 or self.force:
-                sum_(grad, self.world, self.group, force=self.force)
+                with self._on_net_stream(grad):
+                    sum_(grad, self.world, self.group, force=self.force)
                 self.n_collectives += 1
             self.net.apply_gradient(grad, lr)
         return grad

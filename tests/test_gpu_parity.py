@@ -6,7 +6,6 @@ mean test loss after one epoch within rel 1e-3 (BASELINE.json north_star).
 """
 import json
 import os
-import itertools
 
 import numpy as np
 import pytest
@@ -219,57 +218,141 @@ def test_hogwild_claims_each_image_exactly_once(name, torch_cuda):
     np.testing.assert_array_equal(net.debug_claims(n), np.ones(n, np.int32))
 
 
-def interval_orders(n):
-    """All strict interval orders on n samples, as the set of predecessors of each sample.
+def run_traced(name, seed, torch_cuda, n, lr, group=None, max_ctas=None, stagger=0, data=None):
+    """One hogwild epoch of the schedule-recording build: returns (oracle, p0, data, params after,
+    records, per-group publishes, G)."""
+    from paper_1506_09067_b200 import OPT_DEBUG_STAGGER, OPT_DEBUG_TRACE, OPT_MAX_CTAS
+    o, net, p = make(name, seed, torch_cuda, group)
+    if max_ctas:
+        net.set_option(OPT_MAX_CTAS, max_ctas)
+    net.set_option(OPT_DEBUG_TRACE, 1)
+    net.set_option(OPT_DEBUG_STAGGER, stagger)
+    d = data if data is not None else sd.prototype_dataset(seed, n, 0)
+    X, Y = dev(torch_cuda, d.x_train[:n], d.y_train[:n])
+    net.train_epoch(X, Y, lr)
+    G = net.launch_info()["group"]
+    ng = -(-n // G)
+    rec, pubs, reads = net.debug_trace(ng, reads=True)
+    got = net.get_params().astype(np.float64)
+    net.close()
+    return o, p, d, got, rec, pubs.astype(np.float64), G, reads
 
-    Enumerated as the distinct read-before-publish patterns of n workers: each sample i
-    reads at time r_i and publishes at time w_i > r_i; j precedes i iff w_j < r_i."""
-    pats = set()
-    for perm in itertools.permutations(range(2 * n)):
-        r = perm[:n]
-        w = perm[n:]
-        if any(w[i] < r[i] for i in range(n)):
+
+def check_traced_epoch(o, arch, p, d, n, lr, got, rec, pubs, G, reads=None):
+    """Replay a recorded hogwild schedule in the oracle (orc_replay, SURVEY C-1 step 9).
+    (1) no lost or doubled update: final W = W0 + the sum of the groups' publishes;
+    (2) every group whose reads overlapped no publish: its publish equals the oracle's gradient
+        sum at exactly the weights it saw (W0 + the publishes it saw, per layer, forward and
+        delta_in reads separately), R9 per tensor; a mismatch is excused only where the group's
+        forward has a pool near-tie (top-2 gap < 5e-6, R9) at those weights.
+    Returns (groups checked exactly, groups with an overlapping read, near-tie excuses)."""  # noqa: D205
+    from helpers import assert_sum_of_publishes, check_read_values, min_pool_gaps, schedule_from_trace
+    blocks = o.blocks()
+    reads_rec = reads
+    groups, reads, amb = schedule_from_trace(rec, blocks, n, G)
+    assert_sum_of_publishes(got, p, pubs.sum(0), np.abs(pubs).sum(0), len(groups))
+    excused_reads = []
+    if reads_rec is not None:
+        # (3) the values each group read are W0 + publishes consistent with the schedule, and
+        # (4) EVERY group's publish -- torn reads included -- is the oracle's gradient sum at
+        #     exactly the weights it read (forward and delta_in reads separately)
+        check_read_values(rec, blocks, reads_rec, p, pubs)
+        for k, (first, cnt) in enumerate(groups):
+            wf = reads_rec[k, 0].astype(np.float64)
+            wb = np.where(np.isnan(reads_rec[k, 1]), reads_rec[k, 0], reads_rec[k, 1]).astype(np.float64)
+            g = sum(o.sample_grad2(wf, wb, d.x_train[i], d.y_train[i])[1] for i in range(first, first + cnt))
+            ok, w, wn, det = parity_report(pubs[k], -lr * g, blocks)
+            if not ok:
+                gap = min(min(min_pool_gaps(arch, o.forward(wf, d.x_train[i])[1]), default=1.0)
+                          for i in range(first, first + cnt))
+                if gap < 5e-6:
+                    excused_reads.append((k, "near-tie", w))
+                    continue
+                # reading R17 (DESIGN.md): mid-training, a group's fixed-order fp32 sums of a few
+                # hundred mixed-sign terms can cancel enough to miss R9 (derived for first steps at
+                # init); such a group is held to 10x R9 (element-wise 1e-3 with the 1e-2 floor, norm
+                # 1e-4) or to twice the error of plain fp32 on the same input (torch float32 CPU
+                # autograd at the same weights), whichever is larger -- a wrong read or a lost update
+                # is off by orders of magnitude -- and at most 2% of the groups may need it
+                import torch
+                from helpers import torch_grad
+                X32 = d.x_train[first:first + cnt]
+                _, g32, _ = torch_grad(arch, wf.astype(np.float32), X32, d.y_train[first:first + cnt],
+                                       params_bwd=wb.astype(np.float32), dtype=torch.float32)
+                _, w32, wn32, _ = parity_report(-lr * g32, -lr * g, blocks)
+                assert w <= max(10.0, 2.0 * w32) and wn <= max(10.0, 2.0 * wn32), \
+                    f"group {k} (worker {rec[k, 30]}): publish != oracle at the weights it read ({w:.3g} x tol, " \
+                    f"norm {wn:.3g}; {det}); min pool gap {gap:.2e}; torch fp32 reaches {w32:.3g} x tol, norm {wn32:.3g}"
+                excused_reads.append((k, "R17", round(w, 2), round(wn, 2), "torch-fp32", round(w32, 2), round(wn32, 2)))
+    _, ref = o.replay(p, d.x_train[:n], d.y_train[:n], groups, reads, lr, pubs_in=pubs)
+    exact, excused = 0, 0
+    for k in range(len(groups)):
+        if k in amb:
             continue
-        pats.add(tuple(frozenset(j for j in range(n) if w[j] < r[i]) for i in range(n)))
-    return sorted(pats, key=str)
-
-
-def replay(o, p, X, Y, lr, preds):
-    """Hogwild replay: sample i computed at W0 - lr*sum_{j<i} g_j."""
-    n = len(Y)
-    order = sorted(range(n), key=lambda i: len(preds[i]))
-    g = {}
-    for i in order:
-        w = p.astype(np.float64).copy()
-        for j in preds[i]:
-            w -= lr * g[j]
-        g[i] = o.sample_grad(w, X[i], Y[i])[1]
-    return p - lr * sum(g.values())
-
-
-def test_interval_order_counts():
-    assert len(interval_orders(2)) == 3
-    assert len(interval_orders(3)) == 19
+        ok, w, wn, det = parity_report(pubs[k], ref[k], blocks)
+        if not ok:
+            seenf = {r[1]: r[5] for r in reads if r[0] == k and r[2] == 0}
+            wf = p.astype(np.float64).copy()
+            starts = np.cumsum([0] + [nw + nb for _, nw, nb in blocks])
+            for l, seen in seenf.items():
+                for j in seen:
+                    wf[starts[l]:starts[l + 1]] += pubs[j][starts[l]:starts[l + 1]]
+            first, cnt = groups[k]
+            gap = min(min(min_pool_gaps(arch, o.forward(wf, d.x_train[i])[1]), default=1.0)
+                      for i in range(first, first + cnt))
+            assert gap < 5e-6, f"group {k} (worker {rec[k, 30]}): publish != replay at the weights it read " \
+                               f"({w:.3g} x tol, norm {wn:.3g}; per tensor {det}); min pool gap {gap:.2e}"
+            excused += 1
+        else:
+            exact += 1
+    if excused_reads:
+        print("groups excused at the values they read:", excused_reads)
+        assert sum(1 for e in excused_reads if e[1] == "R17") <= max(1, len(groups) // 50), excused_reads
+    return exact, len(amb), excused
 
 
 @pytest.mark.parametrize("name", ["tiny", "large"])
-def test_hogwild_three_samples_brute_force(name, torch_cuda):
-    # 3 workers x G=1 on 3 samples: the result is one of the 19 replay outcomes
-    # (or a mixed-layer read, which per-layer publishing allows: reported)
-    o, net, p = make(name, 11, torch_cuda, 1)
-    d = sd.prototype_dataset(11, 3, 0)
-    X, Y = dev(torch_cuda, d.x_train, d.y_train)
-    lr = 0.5
-    net.train_epoch(X, Y, lr)
-    got = net.get_params().astype(np.float64)
-    best = np.inf
-    for preds in interval_orders(3):
-        ref = replay(o, p, d.x_train, d.y_train, lr, preds)
-        ok, w, wn, _ = parity_report(got, ref, o.blocks())
-        best = min(best, max(w, wn))
-        if ok:
-            return
-    pytest.xfail(f"mixed-layer read (closest replay at {best:.3g} x tol)")
+@pytest.mark.parametrize("stagger", [0, 30000, 90000, 250000])
+def test_hogwild_three_workers_recorded_schedule(name, stagger, torch_cuda):
+    # 3 workers x G = 1 on 3 images, CTA b starting b * stagger cycles late: different
+    # interleavings of reads and per-layer publishes; each is replayed exactly (C-1 step 9)
+    n, lr = 3, 0.5
+    o, p, d, got, rec, pubs, G, reads = run_traced(name, 11, torch_cuda, n, lr, group=1, max_ctas=3, stagger=stagger)
+    assert G == 1
+    exact, n_amb, excused = check_traced_epoch(o, sd.ARCHS[name], p, d, n, lr, got, rec, pubs, G, reads)
+    assert exact + excused + n_amb == 3
+    print(f"{name} stagger {stagger}: workers {list(rec[:, 30])}, exact {exact}, overlapping {n_amb}, near-tie {excused}")
+    if stagger >= 90000:  # workers far enough apart that some group's reads overlap no publish
+        assert exact >= 1, (exact, n_amb, excused)
+
+
+@pytest.mark.parametrize("name", ["tiny", "large"])
+def test_hogwild_full_width_recorded_schedule(name, torch_cuda):
+    # the bench launch configuration (all SMs, default G) on 1,024 images: every group whose
+    # reads overlapped no publish is replayed exactly; the final weights hold every publish once
+    n, lr = 1024, (0.005 if name == "tiny" else 0.05)  # tiny: 148 images in flight at G = 1 (R14)
+    o, p, d, got, rec, pubs, G, reads = run_traced(name, 12, torch_cuda, n, lr)
+    exact, n_amb, excused = check_traced_epoch(o, sd.ARCHS[name], p, d, n, lr, got, rec, pubs, G, reads)
+    ng = -(-n // G)
+    print(f"{name}: {ng} groups, {exact} replayed exactly from the schedule, {n_amb} with an overlapping "
+          f"(possibly torn) read -- every group checked at the values it read; {excused} near-tie")
+    assert exact + n_amb + excused == ng
+    assert len(set(rec[:, 30])) > 64  # many workers took part
+
+
+def test_hogwild_trace_records_detect_a_wrong_schedule(torch_cuda):
+    # teeth: replaying the recorded 3-worker run with one group's reads emptied (pretending it
+    # saw no publish) must fail the per-group check whenever that group had seen one
+    n, lr = 3, 0.5
+    o, p, d, got, rec, pubs, G, _ = run_traced("tiny", 11, torch_cuda, n, lr, group=1, max_ctas=3, stagger=250000)
+    from helpers import schedule_from_trace
+    groups, reads, amb = schedule_from_trace(rec, o.blocks(), n, G)
+    saw = [k for k in range(3) if k not in amb and any(r[0] == k and r[5] for r in reads)]
+    assert saw, "with a 250k-cycle stagger a later worker sees an earlier one's publishes"
+    k = saw[0]
+    wrong = [(g, l, pp, e0, e1, [] if g == k else s) for (g, l, pp, e0, e1, s) in reads]
+    _, ref = o.replay(p, d.x_train[:n], d.y_train[:n], groups, wrong, lr, pubs_in=pubs)
+    assert not parity_report(pubs[k], ref[k], o.blocks())[0]
 
 
 def test_evaluate_matches_oracle_and_is_pure(torch_cuda):
@@ -578,6 +661,96 @@ def test_async_averaging_runs_in_flight(torch_cuda):
     ref = rec["per_epoch"][-1]
     assert abs(ne - ref["test_errors"]) / len(d.y_test) * 100 <= 0.5, (ne, ref)
     net.close()
+
+
+def test_two_replica_inflight_averaging_emulated(torch_cuda):
+    # NEXT-2 with non-zero deltas, two replicas emulated on one GPU (the 8-GPU run is the
+    # driver's): replica r is a net on its own stream with 70 CTAs (both launches co-resident, 8
+    # SMs left for the averaging kernels), training its contiguous half of the configs[3] data
+    # (strong scaling, P = 2) in ONE hogwild launch per epoch; a third stream runs the in-flight
+    # schedule of DistTrainer.epoch_async -- wait for both progress counters to pass t = K, 2K,
+    # ..., snapshot both, average (a torch mean stands in for the NCCL collective), apply
+    # avg - snapshot to each live replica -- then the exact final average.  Epoch 1 is recorded
+    # (schedule-trace build): the sum of the replicas before the final average equals 2 W0 plus
+    # every group's publish (in-flight averages preserve the sum; none lost or doubled), with
+    # non-zero deltas; after 15 epochs the averaged model passes the accuracy gate.
+    import torch
+    from paper_1506_09067_b200 import OPT_DEBUG_TRACE, OPT_MAX_CTAS, Net
+    from paper_1506_09067_b200.dist import async_targets
+    path = os.path.join(GOLD, "config3_seq.json")
+    if not os.path.exists(path):
+        pytest.skip("oracle reference run config3_seq not recorded")
+    rec = json.load(open(path))
+    w = sd.WORKLOADS[rec["workload"]]
+    d = sd.make_dataset(w)
+    arch = sd.ARCHS[rec.get("arch", w.arch)]
+    o = Oracle(arch)
+    p0 = sd.init_params(w.seed, o.blocks())
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    nets = [Net(arch, init_seed=w.seed, stream=st) for st in streams]
+    for net in nets:
+        net.set_params(p0)
+        net.set_option(OPT_MAX_CTAS, 70)
+    X, Y, Xt, Yt = dev(torch, d.x_train, d.y_train, d.x_test, d.y_test)
+    n = int(Y.shape[0])
+    half = n // 2
+    shards = [(0, half), (half, n)]
+    side = torch.cuda.Stream()
+    params = [net.device_params() for net in nets]
+    snaps = [torch.empty_like(params[0]), torch.empty_like(params[0])]
+    K = 1024
+    deltas = []
+    for e in range(w.epochs):
+        lr = w.lr0 * 0.9 ** e
+        traced = e == 0
+        for net in nets:
+            net.set_option(OPT_DEBUG_TRACE, 1 if traced else 0)
+        side.wait_stream(torch.cuda.current_stream())
+        for net in nets:
+            net.stream.wait_stream(torch.cuda.current_stream())
+        bases = [net.progress_enqueued() for net in nets]
+        for net, (lo, hi) in zip(nets, shards):
+            net.train_epoch(X[lo:hi], Y[lo:hi], lr)
+        with torch.cuda.stream(side):
+            for t in async_targets(min(hi - lo for lo, hi in shards), K):
+                for net, b in zip(nets, bases):
+                    net.progress_wait(b + t, side)
+                for net, sn in zip(nets, snaps):
+                    net.avg_snapshot(sn, side)
+                avg = (snaps[0] + snaps[1]) * 0.5
+                if traced:
+                    deltas.append(float((avg - snaps[0]).abs().max()))
+                for net, sn in zip(nets, snaps):
+                    net.avg_apply(avg, sn, side)
+        for net in nets:
+            side.wait_stream(net.stream)
+        torch.cuda.synchronize()
+        if traced:
+            G = nets[0].launch_info()["group"]
+            tot = np.zeros(o.n_params)
+            tot_abs = np.zeros(o.n_params)
+            for net, (lo, hi) in zip(nets, shards):
+                _, pubs = net.debug_trace(-(-(hi - lo) // G))[:2]
+                tot += pubs.astype(np.float64).sum(0)
+                tot_abs += np.abs(pubs.astype(np.float64)).sum(0)
+            from helpers import assert_sum_of_publishes
+            wa, wb = (net.get_params().astype(np.float64) for net in nets)
+            # n_adds: each replica's groups plus its in-flight applies; the two replicas' roundings add
+            n_adds = 2 * (-(-half // G) + len(deltas) + 1)
+            assert_sum_of_publishes(wa + wb, 2 * p0.astype(np.float64), tot, 2 * np.abs(p0) + tot_abs,
+                                    n_adds, rigorous=False)
+            assert len(deltas) == len(async_targets(half, K)) and max(deltas) > 1e-4, deltas  # non-zero deltas
+        with torch.cuda.stream(side):
+            avg = (params[0] + params[1]) * 0.5
+            params[0].copy_(avg)
+            params[1].copy_(avg)
+        side.synchronize()
+    np.testing.assert_array_equal(nets[0].get_params(), nets[1].get_params())
+    ml, ne = nets[0].evaluate(Xt, Yt)
+    ref = rec["per_epoch"][-1]
+    assert abs(ne - ref["test_errors"]) / len(d.y_test) * 100 <= 0.5, (ne, ref)
+    for net in nets:
+        net.close()
 
 
 def test_library_nccl_communicator_one_rank(torch_cuda):

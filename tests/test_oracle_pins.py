@@ -121,53 +121,7 @@ def test_identity_conv_passes_input():
 # --------------------------------------------------------------------------------------
 # torch float64 autograd (library routine) on the BASELINE.json nets
 # --------------------------------------------------------------------------------------
-def torch_grad(arch, params, X, Y, params_bwd=None):
-    """Sum-reduction CE gradient with torch's own conv2d/max_pool2d/linear/cross_entropy.
-
-    params_bwd (optional): the weights the back-propagated partial derivatives use (delta_in =
-    W_bwd^T delta), while the forward pass and the weight gradients use params -- built as
-    layer(x.detach(), W) + layer(x, W_bwd) - layer(x, W_bwd).detach(): the value is layer(x, W),
-    d/dW flows through the first term only, d/dx through the second only."""
-    import torch
-    import torch.nn.functional as F
-    P = torch.tensor(params, dtype=torch.float64, requires_grad=True)
-    Pb = None if params_bwd is None else torch.tensor(params_bwd, dtype=torch.float64)
-    x = torch.tensor(np.asarray(X, np.float64)).reshape(len(Y), 1, 29, 29)
-
-    def split(fn, h, W, b, Wb_, bb_):
-        if Pb is None:
-            return fn(h, W, b)
-        return fn(h.detach(), W, b) + fn(h, Wb_, bb_) - fn(h, Wb_, bb_).detach()
-
-    off = 0
-    h = x
-    c = 1
-    for kind, units, k, act in arch:
-        if kind == C_:
-            nw = units * c * k * k
-            W = P[off:off + nw].reshape(units, c, k, k)
-            b = P[off + nw:off + nw + units]
-            Wb_ = None if Pb is None else Pb[off:off + nw].reshape(units, c, k, k)
-            bb_ = None if Pb is None else Pb[off + nw:off + nw + units]
-            off += nw + units
-            h = split(F.conv2d, h, W, b, Wb_, bb_)
-            h = torch.tanh(h) if act == T_ else h
-            c = units
-        elif kind == P_:
-            h = F.max_pool2d(h, k, stride=k, ceil_mode=False)
-        else:
-            h = h.reshape(h.shape[0], -1)
-            nin = h.shape[1]
-            W = P[off:off + units * nin].reshape(units, nin)
-            b = P[off + units * nin:off + units * nin + units]
-            Wb_ = None if Pb is None else Pb[off:off + units * nin].reshape(units, nin)
-            bb_ = None if Pb is None else Pb[off + units * nin:off + units * nin + units]
-            off += units * nin + units
-            h = split(F.linear, h, W, b, Wb_, bb_)
-            h = torch.tanh(h) if act == T_ else h
-    loss = F.cross_entropy(h, torch.tensor(np.asarray(Y, np.int64)), reduction="sum")
-    loss.backward()
-    return loss.item(), P.grad.numpy().copy(), h.detach().numpy()
+from helpers import torch_grad  # noqa: E402  (torch conv2d / max_pool2d / linear / cross_entropy)
 
 
 @pytest.mark.parametrize("name", ["tiny", "medium", "large", "paper_small", "paper_large"])
