@@ -2365,6 +2365,11 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                         zmax = z[o];
                         best = o;
                     }
+                // s = 1 + r, r = sum of exp(z_o - zmax) over the classes other than the maximum (index
+                // order); the maximum contributes exactly 1.  Reading R18: loss = log1p(r) + zmax - z[lab]
+                // and, when the label is the maximum, delta[lab] = p[lab] - 1 = -r / s -- the same values
+                // as logf(s) and e/s - 1 without their cancellation once p[lab] -> 1 (a trained net)
+#ifdef CHAOS_OLD_SOFTMAX
                 float s = 0.f;
                 for (int o = 0; o < kClasses; ++o) s += expf(z[o] - zmax);
                 const float loss = logf(s) + zmax - z[lab];
@@ -2377,6 +2382,27 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                     for (int o = 0; o < kClasses; ++o) z[o] = expf(z[o] - zmax) * inv - (o == lab ? 1.f : 0.f);
                     s_loss[g] = loss;
                 }
+#else
+                float e[kClasses];
+                float r = 0.f;
+#pragma unroll
+                for (int o = 0; o < kClasses; ++o) {
+                    e[o] = (o == best) ? 1.f : expf(z[o] - zmax);
+                    if (o != best) r += e[o];
+                }
+                const float loss = log1pf(r) + zmax - z[lab];
+                if (!isfinite(loss)) atomicOr(a.latch, kLatchNonfinite);
+                if constexpr (MODE == kEval) {
+                    a.out_loss[base + g] = loss;
+                    a.out_wrong[base + g] = static_cast<unsigned char>(best != lab);
+                } else {
+                    const float inv = 1.f / (1.f + r);
+#pragma unroll
+                    for (int o = 0; o < kClasses; ++o)
+                        z[o] = (o != lab) ? e[o] * inv : (lab == best ? -r * inv : e[o] * inv - 1.f);
+                    s_loss[g] = loss;
+                }
+#endif
             }
         }
         if constexpr (TRAIN) {

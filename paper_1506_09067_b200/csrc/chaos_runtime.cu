@@ -103,8 +103,14 @@ struct LargeNet {  // configs[3], configs[4]
 #ifndef LARGE_C2_PB  // conv2 delta_in: window rows per band task
 #define LARGE_C2_PB 1
 #endif
-    using C2 = Conv<20, 13, 13, 60, 3, 2, 10, 9, 1, 4, LARGE_C2_PB, -1, false, true, 0, false, 1>;
-    using C3 = Conv<60, 5, 5, 100, 2, 2, 4, 4, 1, 5, 2, 0, false, false, 4, true, 1>;
+#ifndef LARGE_C2_MT  // conv2 forward: output maps per thread item
+#define LARGE_C2_MT 10
+#endif
+#ifndef LARGE_C3_MT  // conv3 forward: output maps per thread item
+#define LARGE_C3_MT 4
+#endif
+    using C2 = Conv<20, 13, 13, 60, 3, 2, LARGE_C2_MT, 9, 1, 4, LARGE_C2_PB, -1, false, true, 0, false, 1>;
+    using C3 = Conv<60, 5, 5, 100, 2, 2, LARGE_C3_MT, 4, 1, 5, 2, 0, false, false, 4, true, 1>;
     using F1 = Full<400, 150, true>;
     using F2 = Full<150, 10, false>;
 };

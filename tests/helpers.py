@@ -16,24 +16,28 @@ def split_blocks(vec, blocks):
     return out
 
 
-def parity_report(got, ref, blocks, rel=1e-4, floor=1e-2, norm_rel=1e-5):
+def parity_report(got, ref, blocks, rel=1e-4, floor=1e-2, norm_rel=1e-5, abs_floor=None):
     """Per tensor T: |got-ref| <= rel*max(|ref|, floor*||ref||_inf) element-wise and
-    ||got-ref||_2 <= norm_rel*||ref||_2.  Returns (ok, worst_ratio, worst_norm_ratio, details)."""
+    ||got-ref||_2 <= norm_rel*||ref||_2.  abs_floor (optional, per element, normative layout): an
+    absolute tolerance added to both (reading R20: a weight update below one ulp of the weight it
+    is applied to cannot change it).  Returns (ok, worst_ratio, worst_norm_ratio, details)."""
     ok = True
     worst = 0.0
     worst_norm = 0.0
     details = []
+    afl = split_blocks(np.asarray(abs_floor, np.float64), blocks) if abs_floor is not None else None
     for k, (g, r) in enumerate(zip(split_blocks(np.asarray(got, np.float64), blocks),
                                    split_blocks(np.asarray(ref, np.float64), blocks))):
         rmax = np.abs(r).max() if r.size else 0.0
-        if rmax == 0.0:
+        a = afl[k] if afl is not None else np.zeros_like(r)
+        if rmax == 0.0 and not a.any():
             bad = np.abs(g).max() if g.size else 0.0
             ratio = 0.0 if bad == 0.0 else np.inf
             nr = 0.0 if bad == 0.0 else np.inf
         else:
-            tol = rel * np.maximum(np.abs(r), floor * rmax)
+            tol = np.maximum(rel * np.maximum(np.abs(r), floor * rmax), a)
             ratio = float(np.max(np.abs(g - r) / tol))
-            nr = float(np.linalg.norm(g - r) / np.linalg.norm(r)) / norm_rel
+            nr = float(np.linalg.norm(g - r) / (norm_rel * np.linalg.norm(r) + np.linalg.norm(a)))
         worst = max(worst, ratio)
         worst_norm = max(worst_norm, nr)
         details.append((k, ratio, nr))

@@ -18,8 +18,9 @@ pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden", "oracle_runs")
 NETS = ["tiny", "medium", "large", "paper_small", "paper_large"]
 # Element-wise tolerance of multi-step weight comparisons (R9 / R16): BASELINE.json's
-# rel 1e-4 for its nets; the Table I large net (not a BASELINE config) sums up to 2,160 fp32
-# products per output (9x the large net's 240), so its bound scales by sqrt(9): 3e-4
+# rel 1e-4 for its nets; the Table I large net (not a BASELINE config) 3e-4: plain fp32 (torch
+# CPU float32) itself reaches 1.22x the 1e-4 bound on the 3-step B = 64 trajectory of
+# test_sync_steps (profiles/r3/tolerance_table.md, scripts/tolerance_table.py)
 REL = {"paper_large": 3e-4}
 
 
@@ -83,8 +84,10 @@ def test_forward_logits(name, group, torch_cuda):
 
 @pytest.mark.parametrize("name", NETS)
 @pytest.mark.parametrize("n", [1, 13])
-def test_gradients(name, n, torch_cuda):
-    o, net, p = make(name, 5, torch_cuda)
+@pytest.mark.parametrize("group", [None, 4])
+def test_gradients(name, n, group, torch_cuda):
+    # default G and G = 4 (the tiny / Table I small nets default to G = 1), each against the oracle
+    o, net, p = make(name, 5, torch_cuda, group)
     d = sd.prototype_dataset(5, n, 0)
     X, Y = dev(torch_cuda, d.x_train, d.y_train)
     g = net.compute_gradients(X, Y)
@@ -108,25 +111,92 @@ def test_gradients_group1_equal_default_group(name, torch_cuda):
 
 @pytest.mark.parametrize("name", NETS)
 def test_sync_steps(name, torch_cuda):
-    # 3 sync batches (B=64, last one partial: 150 = 64+64+22), weights after the steps.  The Table
-    # I large net has ~8k pool windows per image, so most 64-image trajectories cross an argmax
-    # near-tie (top-2 gap < 5e-6, R9) where fp32 and fp64 may pick differently: for it a verified
-    # tie-free trajectory (scripted search: seed 26, 40 images, B = 16 -> 16+16+8, min gap 9.5e-6)
+    # 3 sync batches (B=64, last one partial: 150 = 64+64+22) on the same trajectory for every net.
+    # (a) Each step from the oracle's weights at its start, against the oracle's step (R9 / R16 for
+    #     the Table I large net): a step whose batch has a pool near-tie at those weights (top-2
+    #     gap < 1e-5 relative, SURVEY C-15) may take the other argmax in fp32 -- reported, not
+    #     failed (at least one step per net must be checked).
+    # (b) The whole 3-step GPU trajectory against the oracle's, when the trajectory is tie-free.
+    from helpers import min_pool_gaps
     from paper_1506_09067_b200 import OPT_SYNC_BATCH, SYNC
-    seed, n, batch = (26, 40, 16) if name == "paper_large" else (7, 150, 64)
+    seed, n, batch = 7, 150, 64
     o, net, p = make(name, seed, torch_cuda)
     net.set_option(OPT_SYNC_BATCH, batch)
     d = sd.prototype_dataset(seed, n, 0)
-    X, Y = dev(torch_cuda, d.x_train, d.y_train)
     lr = 0.05
-    net.train_epoch(X, Y, lr, SYNC)
-    got = net.get_params()
-    ref, _ = o.train_sync(p, d.x_train, d.y_train, lr, batch)
-    # the weights move by lr*g: compare the step (ref - p) as well as the weights
-    assert_parity(got, ref, o.blocks(), rel=REL.get(name, 1e-4))
-    step_ok, w, wn, _ = parity_report(got.astype(np.float64) - p, ref - p, o.blocks(), rel=1e-3, floor=1e-2,
-                                      norm_rel=1e-4)
-    assert step_ok, (w, wn)
+    rel = REL.get(name, 1e-4)
+    arch = sd.ARCHS[name]
+    w = p.astype(np.float64)
+    checked, attributed, min_gap = 0, [], 1.0
+    for s0 in range(0, n, batch):
+        xs, ys = d.x_train[s0:s0 + batch], d.y_train[s0:s0 + batch]
+        w32 = w.astype(np.float32)
+        gap = min(min(min_pool_gaps(arch, o.forward(w32, x)[1]), default=1.0) for x in xs)
+        min_gap = min(min_gap, gap)
+        ref, _ = o.train_sync(w32, xs, ys, lr, batch)
+        net.set_params(w32)
+        X, Y = dev(torch_cuda, xs, ys)
+        net.train_epoch(X, Y, lr, SYNC)
+        got = net.get_params().astype(np.float64)
+        ok_w = parity_report(got, ref, o.blocks(), rel=rel)[0]
+        ok_s, ws, wns, _ = parity_report(got - w32, ref - w32, o.blocks(), rel=1e-3, floor=1e-2, norm_rel=1e-4)
+        if ok_w and ok_s:
+            checked += 1
+        elif gap < 1e-5:
+            attributed.append((s0, gap, ws))
+        else:
+            assert False, f"step at image {s0}: {parity_report(got, ref, o.blocks(), rel=rel)[1:3]}, step {ws}, {wns}"
+        w = ref
+    assert checked >= 1, attributed
+    if attributed:
+        print(f"{name}: steps attributed to pool near-ties (start image, gap, step x tol): {attributed}")
+    if min_gap >= 1e-5:
+        _, net2, _ = make(name, seed, torch_cuda)
+        net2.set_option(OPT_SYNC_BATCH, batch)
+        X, Y = dev(torch_cuda, d.x_train, d.y_train)
+        net2.train_epoch(X, Y, lr, SYNC)
+        got = net2.get_params()
+        ref, _ = o.train_sync(p, d.x_train, d.y_train, lr, batch)
+        # the weights move by lr*g: compare the step (ref - p) as well as the weights
+        assert_parity(got, ref, o.blocks(), rel=rel)
+        step_ok, ws, wn, _ = parity_report(got.astype(np.float64) - p, ref - p, o.blocks(), rel=1e-3, floor=1e-2,
+                                           norm_rel=1e-4)
+        assert step_ok, (ws, wn)
+
+
+@pytest.mark.parametrize("name", NETS)
+@pytest.mark.parametrize("group", [None, 1])
+def test_exact_pool_ties(name, group, torch_cuda):
+    # every pool window ties exactly (SURVEY C-14, first maximum in row-major order):
+    # (a) all-zero weights -- every activation is 0; closed form: the output bias gradient is
+    #     sum(0.1 - onehot), every other gradient exactly 0;
+    # (b) constant images with random weights -- every conv output is constant over its map, so
+    #     every window of every pool layer ties; gradients against the oracle (R9)
+    o, net, p = make(name, 19, torch_cuda, group)
+    d = sd.prototype_dataset(19, 9, 0)
+    X, Y = dev(torch_cuda, d.x_train, d.y_train)
+    net.set_params(np.zeros(o.n_params, np.float32))
+    g = net.compute_gradients(X, Y)
+    expect = np.zeros(o.n_params)
+    for y in d.y_train:
+        expect[-10:] += 0.1
+        expect[-10 + y] -= 1.0
+    np.testing.assert_allclose(g[-10:], expect[-10:], rtol=1e-6, atol=1e-6)
+    assert np.count_nonzero(g[:-10]) == 0
+    net.set_params(p)
+    xc = np.empty_like(d.x_train)
+    for i in range(9):
+        xc[i] = np.float32((i - 4) / 4.5)  # constant per image, in [-1, 1] (one image all zero)
+    X, = dev(torch_cuda, xc)
+    g = net.compute_gradients(X, Y)
+    ref = sum(o.sample_grad(p, xc[i], d.y_train[i])[1] for i in range(9))
+    assert_parity(g, ref, o.blocks())
+    logits = net.forward(X).cpu().numpy()
+    for i in range(9):
+        r, _, am = o.forward(p, xc[i])
+        assert not am.any()  # the oracle's argmax is the first position of every window
+        tol = 1e-4 * np.maximum(np.abs(r), 1e-2 * np.abs(r).max())
+        assert np.all(np.abs(logits[i] - r) <= tol)
 
 
 @pytest.mark.parametrize("name", NETS)
@@ -261,7 +331,8 @@ def check_traced_epoch(o, arch, p, d, n, lr, got, rec, pubs, G, reads=None):
             wf = reads_rec[k, 0].astype(np.float64)
             wb = np.where(np.isnan(reads_rec[k, 1]), reads_rec[k, 0], reads_rec[k, 1]).astype(np.float64)
             g = sum(o.sample_grad2(wf, wb, d.x_train[i], d.y_train[i])[1] for i in range(first, first + cnt))
-            ok, w, wn, det = parity_report(pubs[k], -lr * g, blocks)
+            ulp = 2.0 ** -24 * np.abs(wf)  # R20: below one ulp of the weight it updates, an update is moot
+            ok, w, wn, det = parity_report(pubs[k], -lr * g, blocks, abs_floor=ulp)
             if not ok:
                 gap = min(min(min_pool_gaps(arch, o.forward(wf, d.x_train[i])[1]), default=1.0)
                           for i in range(first, first + cnt))
@@ -279,7 +350,7 @@ def check_traced_epoch(o, arch, p, d, n, lr, got, rec, pubs, G, reads=None):
                 X32 = d.x_train[first:first + cnt]
                 _, g32, _ = torch_grad(arch, wf.astype(np.float32), X32, d.y_train[first:first + cnt],
                                        params_bwd=wb.astype(np.float32), dtype=torch.float32)
-                _, w32, wn32, _ = parity_report(-lr * g32, -lr * g, blocks)
+                _, w32, wn32, _ = parity_report(-lr * g32, -lr * g, blocks, abs_floor=ulp)
                 assert w <= max(10.0, 2.0 * w32) and wn <= max(10.0, 2.0 * wn32), \
                     f"group {k} (worker {rec[k, 30]}): publish != oracle at the weights it read ({w:.3g} x tol, " \
                     f"norm {wn:.3g}; {det}); min pool gap {gap:.2e}; torch fp32 reaches {w32:.3g} x tol, norm {wn32:.3g}"
@@ -289,7 +360,12 @@ def check_traced_epoch(o, arch, p, d, n, lr, got, rec, pubs, G, reads=None):
     for k in range(len(groups)):
         if k in amb:
             continue
-        ok, w, wn, det = parity_report(pubs[k], ref[k], blocks)
+        if reads_rec is not None:
+            seen0 = reads_rec[k, 0].astype(np.float64)
+        else:
+            seen0 = p.astype(np.float64) + sum((pubs[j] for j in set().union(*[set(r[5]) for r in reads if r[0] == k])),
+                                               np.zeros(len(p)))
+        ok, w, wn, det = parity_report(pubs[k], ref[k], blocks, abs_floor=2.0 ** -24 * np.abs(seen0))
         if not ok:
             seenf = {r[1]: r[5] for r in reads if r[0] == k and r[2] == 0}
             wf = p.astype(np.float64).copy()
@@ -462,7 +538,15 @@ def test_hogwild_accuracy_gate(run, torch_cuda):
         curve.append(net.evaluate(Xt, Yt))
     ref = rec["per_epoch"][-1]
     n = len(d.y_test)
+    print(run, "hogwild (CE, errors) per epoch:", [(round(c, 5), e) for c, e in curve])
+    print(run, "oracle seq (CE, errors) per epoch:", [(round(r["test_mean_loss"], 5), r["test_errors"])
+                                                     for r in rec["per_epoch"]])
     assert abs(curve[-1][1] - ref["test_errors"]) / n * 100 <= 0.5, (curve, ref)
+    # the learning curve, epoch by epoch (R19): test errors within 0.5 pp of the oracle's
+    # sequential SGD and mean test cross-entropy within a factor 1.3 of it at every epoch
+    for (ce, ne), r in zip(curve, rec["per_epoch"]):
+        assert abs(ne - r["test_errors"]) / n * 100 <= 0.5, (curve, rec["per_epoch"])
+        assert r["test_mean_loss"] / 1.3 <= ce <= 1.3 * r["test_mean_loss"], (curve, rec["per_epoch"])
 
 
 def test_batch_gradient_apply_equals_sync_epoch_bitwise(torch_cuda):
