@@ -117,7 +117,7 @@ struct Conv {
     static_assert(KK % TT == 0, "TT must divide K*K");
     static_assert(RB % KP == 0 || NB == 1, "bands must start on a window row");
     static_assert(PH >= 1 && PW >= 1, "pool larger than the conv output");
-    static constexpr int GW_SCRATCH = (GS > 1 ? GS * WFL : 0) + BLK;  // floats to assemble gW (+ splits)
+    static constexpr int GW_SCRATCH = (GS > 1 ? GS * WFL + GS * M : 0) + BLK;  // floats to assemble gW (+ splits)
 };
 
 // Fully connected layer IN -> OUT, tanh or identity (logits).
@@ -739,6 +739,8 @@ __device__ __forceinline__ void conv_gw(const KArgs& a, int slot, const float* _
                 else
                     fin[L::WFL + m] = sc * accb;
             }
+        } else {
+            if (n == 0 && tg == 0) scr[GS * L::WFL + L::BLK + s * M + m] = accb;  // bias partial of split s
         }
     }
     if constexpr (SCRATCH) {
@@ -753,10 +755,10 @@ __device__ __forceinline__ void conv_gw(const KArgs& a, int slot, const float* _
                 for (int k = 0; k < GS; ++k) s += scr[k * L::WFL + widx];
                 fin[widx] = sc * s;
             }
-            for (int m = threadIdx.x; m < M; m += NT) {  // bias: fixed-order sum by one thread per map
+            for (int m = threadIdx.x; m < M; m += NT) {  // bias: the splits' partial sums, fixed order
                 float s = 0.f;
-                for (int g = 0; g < cnt; ++g)
-                    for (int pp = 0; pp < P; ++pp) s += dp[g * L::OUT_SZ + m * P + pp];
+#pragma unroll
+                for (int k = 0; k < GS; ++k) s += scr[GS * L::WFL + L::BLK + k * M + m];
                 fin[L::WFL + m] = sc * s;
             }
         }
@@ -1661,6 +1663,201 @@ __device__ __forceinline__ void conv_din_winp(const float* __restrict__ wsm, con
 }
 
 // ------------------------------------------------------------------------------------
+// PHASE(conv_bwd_sparse) the whole backward of a small conv layer (KP == 2, lanes over input
+// maps), argmax-sparse: for a given (image, output map, window) the argmax phase is the same for
+// every lane, so one warp-uniform two-level branch selects it and only the argmax position's K*K
+// products are computed (not the 4 phases of the dense conv_din_win / conv_gw_win).
+//  delta_in: warps [0, DW), one per (image, 32 input maps): dout[g][n][y][x] = (1 - in^2) *
+//            sum_m sum_w W[m][n][i][j] d[g][m][w] at (y, x) = window origin + phase + (i, j)
+//  gW:       then every warp takes tasks (4 output maps, 32 input maps) from a shared counter:
+//            gW[n][i][j][m] = sum_g sum_w d[g][m][w] in[g][n][origin + phase + (i, j)], gb = sum d,
+//            published from registers (16-B vector reductions / slot stores).  The order of every
+//            sum is fixed (g, w, then m or the task's own order): deterministic, whichever warp runs
+//            a task.  out must not alias in / dp.  ctr: one int of shared memory, 0 on entry.
+// ------------------------------------------------------------------------------------
+template <class L, int NT, int MODE>
+__device__ __forceinline__ void conv_bwd_sparse(const KArgs& a, int slot, const float* __restrict__ wsm,
+                                                const float* __restrict__ dp, const uint8_t* __restrict__ am,
+                                                const float* __restrict__ in, float* __restrict__ out, int woff,
+                                                int cnt, float sc, int* ctr) {
+    constexpr int K = L::K, KP = L::KP, KK = L::KK, PW = L::PW, P = L::P, M = L::M, C = L::C;
+    constexpr int H = L::H, W = L::W, HW = H * W, HR = L::HR, WR = L::WR, BS = KP + K - 1;
+    constexpr int NCW = (C + 31) / 32, NMG = M / 4, NTASK = NMG * NCW;
+    static_assert(KP == 2 && M % 4 == 0 && L::MP == M, "2x2 pooling, 4 maps per vector");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // ---- delta_in
+    if (warp < cnt * NCW) {
+        const int cw = warp % NCW, g = warp / NCW;
+        const int n = cw * 32 + lane;
+        const bool act = n < C;
+        const float* wn = wsm + (act ? n : 0) * KK * L::MP;
+        const float* dpg = dp + g * L::OUT_SZ;
+        const uint8_t* amg = am + g * L::OUT_SZ;
+        float acc[HR][WR];
+#pragma unroll
+        for (int y = 0; y < HR; ++y)
+#pragma unroll
+            for (int x = 0; x < WR; ++x) acc[y][x] = 0.f;
+#pragma unroll 1
+        for (int m4 = 0; m4 < M; m4 += 4) {
+            float4 w4[KK];
+#pragma unroll
+            for (int tp = 0; tp < KK; ++tp) w4[tp] = *reinterpret_cast<const float4*>(wn + tp * L::MP + m4);
+            float dv[4][P];
+            int av[4][P];
+#pragma unroll
+            for (int mm = 0; mm < 4; ++mm) {
+                if constexpr (P == 4) {  // one map's 4 windows: a 16-B delta load and a 4-byte phase load
+                    const float4 d4 = *reinterpret_cast<const float4*>(dpg + (m4 + mm) * P);
+                    const uint32_t a4 = *reinterpret_cast<const uint32_t*>(amg + (m4 + mm) * P);
+                    dv[mm][0] = d4.x;
+                    dv[mm][1] = d4.y;
+                    dv[mm][2] = d4.z;
+                    dv[mm][3] = d4.w;
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) av[mm][w] = (a4 >> (8 * w)) & 0xffu;
+                } else {
+#pragma unroll
+                    for (int w = 0; w < P; ++w) {
+                        dv[mm][w] = dpg[(m4 + mm) * P + w];
+                        av[mm][w] = amg[(m4 + mm) * P + w];
+                    }
+                }
+            }
+#pragma unroll
+            for (int mm = 0; mm < 4; ++mm) {
+                float wv[KK];
+#pragma unroll
+                for (int tp = 0; tp < KK; ++tp)
+                    wv[tp] = mm == 0 ? w4[tp].x : mm == 1 ? w4[tp].y : mm == 2 ? w4[tp].z : w4[tp].w;
+#pragma unroll
+                for (int w = 0; w < P; ++w) {
+                    const int pr = w / PW, pc = w % PW;
+                    const float d = dv[mm][w];
+                    const int ph = av[mm][w];
+#define CHAOS_DIN_PH(AA, BB)                                                                    \
+    _Pragma("unroll") for (int i = 0; i < K; ++i) _Pragma("unroll") for (int j = 0; j < K; ++j) \
+        acc[pr * KP + (AA) + i][pc * KP + (BB) + j] =                                           \
+            fmaf(wv[i * K + j], d, acc[pr * KP + (AA) + i][pc * KP + (BB) + j]);
+                    if (ph < 2) {  // warp-uniform: one argmax phase per (image, map, window)
+                        if (ph == 0) {
+                            CHAOS_DIN_PH(0, 0)
+                        } else {
+                            CHAOS_DIN_PH(0, 1)
+                        }
+                    } else {
+                        if (ph == 2) {
+                            CHAOS_DIN_PH(1, 0)
+                        } else {
+                            CHAOS_DIN_PH(1, 1)
+                        }
+                    }
+#undef CHAOS_DIN_PH
+                }
+            }
+        }
+        if (act) {
+            const float* ib = in + g * L::IN_SZ + n * HW;
+            float* ob = out + g * L::IN_SZ + n * HW;
+#pragma unroll
+            for (int y = 0; y < H; ++y)
+#pragma unroll
+                for (int x = 0; x < W; ++x) {
+                    const float v = ib[y * W + x];
+                    ob[y * W + x] = (y < HR && x < WR ? acc[y < HR ? y : 0][x < WR ? x : 0] : 0.f) * (1.f - v * v);
+                }
+        }
+    }
+    // ---- weight gradient: tasks (4 output maps, 32 input maps) from the shared counter
+    for (;;) {
+        int task = 0;
+        if (lane == 0) task = atomicAdd(ctr, 1);
+        task = __shfl_sync(0xffffffffu, task, 0);
+        if (task >= NTASK) break;
+        const int cw = task % NCW, m0 = (task / NCW) * 4;
+        const int n = cw * 32 + lane;
+        const bool act = n < C;
+        float acc[4][KK];
+        float accb[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            accb[q] = 0.f;
+#pragma unroll
+            for (int t = 0; t < KK; ++t) acc[q][t] = 0.f;
+        }
+#pragma unroll 1
+        for (int g = 0; g < cnt; ++g) {
+            const float* ing = in + g * L::IN_SZ + (act ? n : 0) * HW;
+            const float* dpg = dp + g * L::OUT_SZ + m0 * P;
+            const uint8_t* amg = am + g * L::OUT_SZ + m0 * P;
+            float dvs[4 * P];
+            int avs[4 * P];
+            if constexpr (P == 4) {  // the task's 4 maps x 4 windows: four 16-B delta loads, one 16-B phase load
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float4 d4 = reinterpret_cast<const float4*>(dpg)[q];
+                    dvs[4 * q] = d4.x;
+                    dvs[4 * q + 1] = d4.y;
+                    dvs[4 * q + 2] = d4.z;
+                    dvs[4 * q + 3] = d4.w;
+                }
+                const uint4 a16 = *reinterpret_cast<const uint4*>(amg);
+                const uint32_t aw[4] = {a16.x, a16.y, a16.z, a16.w};
+#pragma unroll
+                for (int e = 0; e < 16; ++e) avs[e] = (aw[e / 4] >> (8 * (e % 4))) & 0xffu;
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4 * P; ++e) {
+                    dvs[e] = dpg[e];
+                    avs[e] = amg[e];
+                }
+            }
+#pragma unroll
+            for (int w = 0; w < P; ++w) {
+                const int pr = w / PW, pc = w % PW;
+                float blk[BS][BS];
+#pragma unroll
+                for (int u = 0; u < BS; ++u)
+#pragma unroll
+                    for (int v = 0; v < BS; ++v) blk[u][v] = ing[(pr * KP + u) * W + pc * KP + v];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float d = dvs[q * P + w];
+                    const int ph = avs[q * P + w];
+                    accb[q] += d;
+#define CHAOS_GW_PH(AA, BB)                                                                     \
+    _Pragma("unroll") for (int i = 0; i < K; ++i) _Pragma("unroll") for (int j = 0; j < K; ++j) \
+        acc[q][i * K + j] = fmaf(d, blk[(AA) + i][(BB) + j], acc[q][i * K + j]);
+                    if (ph < 2) {  // warp-uniform
+                        if (ph == 0) {
+                            CHAOS_GW_PH(0, 0)
+                        } else {
+                            CHAOS_GW_PH(0, 1)
+                        }
+                    } else {
+                        if (ph == 2) {
+                            CHAOS_GW_PH(1, 0)
+                        } else {
+                            CHAOS_GW_PH(1, 1)
+                        }
+                    }
+#undef CHAOS_GW_PH
+                }
+            }
+        }
+        if (act) {
+#pragma unroll
+            for (int t = 0; t < KK; ++t)
+                publish_vec4<MODE>(a, slot, woff + (n * KK + t) * L::MP + m0,
+                                   make_float4(sc * acc[0][t], sc * acc[1][t], sc * acc[2][t], sc * acc[3][t]));
+            if (n == 0)
+                publish_vec4<MODE>(a, slot, woff + L::WFL + m0,
+                                   make_float4(sc * accb[0], sc * accb[1], sc * accb[2], sc * accb[3]));
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
 // PHASE(fc_fwd2) fully connected forward, IN % 4 == 0: one warp per NR output rows, lanes
 // over 16-B column quads; every weight load of the NR rows is issued before the first FMA
 // (__ldcg: on-demand reads of the shared store from L2), activations are LDS.128 broadcasts
@@ -2157,9 +2354,14 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
 #ifndef CHAOS_C3_DINP  // conv3 delta_in: the software-pipelined conv_din_winp
 #define CHAOS_C3_DINP 1
 #endif
+#ifndef CHAOS_C3_SPARSE  // conv3 backward: argmax-sparse conv_bwd_sparse (warp-uniform phase branches)
+#define CHAOS_C3_SPARSE 1
+#endif
 #ifndef CHAOS_C2_PAR  // conv2 backward: delta_in (window-row bands, PB >= 2) beside conv_gw_m on the other warps
 #define CHAOS_C2_PAR 0
 #endif
+    constexpr bool C3_SPARSE = CHAOS_C3_SPARSE && NCONV >= 3 && !BIG && C3::KP == 2 && C3::M % 4 == 0 &&
+                               C3::MP == C3::M && G * ((C3::C + 31) / 32) <= NT / 32;
     constexpr int C2_WTP = (CHAOS_C2_WTP && NCONV == 3 && !BIG && C2::DIN3 && C2::GWIN == 0) ? (C2::ROWS | 1) : 0;
     constexpr int FRCH = FCSTAGE ? (S::WBUF / (2 * F1::IN)) : 1;
     static_assert(!FCSTAGE || FRCH >= 1, "FC1 chunk must hold a row");
@@ -2349,60 +2551,58 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
         __syncthreads();
         if constexpr (NFULL == 2) TR_RE(4, 0);
         PTIME(5);
-        // ---------------- a4: softmax cross-entropy, output delta
-        if (threadIdx.x < cnt) {
-            const int g = threadIdx.x;
-            float* z = zz + g * kZStride;
-            const int lab = s_lab[g];
-            if constexpr (MODE == kForward) {
+        // ---------------- a4: softmax cross-entropy, output delta.  16 lanes per image (class o =
+        // lane % 16), two images per warp: the maximum, the sum and the loss are shuffle trees in a
+        // fixed order (deterministic), every exp in parallel.  Reading R18: with r = the sum of
+        // exp(z_o - zmax) over the classes other than the first maximum (which contributes exactly
+        // 1), loss = log1p(r) + zmax - z[lab] and, when the label is that maximum,
+        // delta[lab] = p[lab] - 1 = -r / (1 + r): the values of log(s) and p - onehot without their
+        // cancellation once p[lab] -> 1 (a trained net)
+        if constexpr (MODE == kForward) {
+            if (threadIdx.x < cnt) {
+                const int g = threadIdx.x;
                 for (int o = 0; o < kClasses; ++o)
-                    a.out_logits[(static_cast<long long>(base) + g) * kClasses + o] = z[o];
-            } else {
-                float zmax = z[0];
-                int best = 0;
-                for (int o = 1; o < kClasses; ++o)
-                    if (z[o] > zmax) {
-                        zmax = z[o];
-                        best = o;
-                    }
-                // s = 1 + r, r = sum of exp(z_o - zmax) over the classes other than the maximum (index
-                // order); the maximum contributes exactly 1.  Reading R18: loss = log1p(r) + zmax - z[lab]
-                // and, when the label is the maximum, delta[lab] = p[lab] - 1 = -r / s -- the same values
-                // as logf(s) and e/s - 1 without their cancellation once p[lab] -> 1 (a trained net)
-#ifdef CHAOS_OLD_SOFTMAX
-                float s = 0.f;
-                for (int o = 0; o < kClasses; ++o) s += expf(z[o] - zmax);
-                const float loss = logf(s) + zmax - z[lab];
+                    a.out_logits[(static_cast<long long>(base) + g) * kClasses + o] = zz[g * kZStride + o];
+            }
+        } else if (threadIdx.x < 32 * ((G + 1) / 2)) {
+            static_assert(kClasses <= 16 && kZStride >= kClasses, "16 lanes per image");
+            const int g = threadIdx.x >> 4, o = threadIdx.x & 15;
+            const bool on = g < cnt && o < kClasses;
+            float* z = zz + (g < cnt ? g : 0) * kZStride;
+            const int lab = s_lab[g < cnt ? g : 0];
+            const float zo = on ? z[o] : -INFINITY;
+            // first maximum: the largest value, ties to the lowest class
+            float zmax = zo;
+            int best = on ? o : 16;
+#pragma unroll
+            for (int k = 8; k >= 1; k >>= 1) {
+                const float zv = __shfl_xor_sync(0xffffffffu, zmax, k);
+                const int bv = __shfl_xor_sync(0xffffffffu, best, k);
+                if (zv > zmax || (zv == zmax && bv < best)) {
+                    zmax = zv;
+                    best = bv;
+                }
+            }
+            const float e = (on && o != best) ? expf(zo - zmax) : 0.f;
+            float r = e;
+#pragma unroll
+            for (int k = 8; k >= 1; k >>= 1) r += __shfl_xor_sync(0xffffffffu, r, k);
+            const float zlab = __shfl_sync(0xffffffffu, zo, (threadIdx.x & 16) + lab);
+            const float loss = log1pf(r) + zmax - zlab;
+            if (on && o == 0) {
                 if (!isfinite(loss)) atomicOr(a.latch, kLatchNonfinite);
                 if constexpr (MODE == kEval) {
                     a.out_loss[base + g] = loss;
                     a.out_wrong[base + g] = static_cast<unsigned char>(best != lab);
                 } else {
-                    const float inv = 1.f / s;
-                    for (int o = 0; o < kClasses; ++o) z[o] = expf(z[o] - zmax) * inv - (o == lab ? 1.f : 0.f);
                     s_loss[g] = loss;
                 }
-#else
-                float e[kClasses];
-                float r = 0.f;
-#pragma unroll
-                for (int o = 0; o < kClasses; ++o) {
-                    e[o] = (o == best) ? 1.f : expf(z[o] - zmax);
-                    if (o != best) r += e[o];
-                }
-                const float loss = log1pf(r) + zmax - z[lab];
-                if (!isfinite(loss)) atomicOr(a.latch, kLatchNonfinite);
-                if constexpr (MODE == kEval) {
-                    a.out_loss[base + g] = loss;
-                    a.out_wrong[base + g] = static_cast<unsigned char>(best != lab);
-                } else {
+            }
+            if constexpr (MODE != kEval) {
+                if (on) {
                     const float inv = 1.f / (1.f + r);
-#pragma unroll
-                    for (int o = 0; o < kClasses; ++o)
-                        z[o] = (o != lab) ? e[o] * inv : (lab == best ? -r * inv : e[o] * inv - 1.f);
-                    s_loss[g] = loss;
+                    z[o] = (o != lab) ? (o == best ? inv : e * inv) : (lab == best ? -r * inv : e * inv - 1.f);
                 }
-#endif
             }
         }
         if constexpr (TRAIN) {
@@ -2519,7 +2719,14 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 }
                 TR_PB(2);
                 // otherwise W3 is still staged from the forward pass (the exact snapshot it used)
-                if constexpr (C3::GWIN > 0) {
+                if constexpr (C3_SPARSE) {
+                    int* ctr = reinterpret_cast<int*>(smem + 72);  // header word (kHdrBytes), reset here
+                    if (threadIdx.x == 0) *ctr = 0;
+                    __syncthreads();
+                    conv_bwd_sparse<C3, NT, MODE>(a, slot, wb, a3, am3, a2, sS, O::c3w, cnt, sc, ctr);
+                    __syncthreads();
+                    PTIME(9);
+                } else if constexpr (C3::GWIN > 0) {
                     // delta_in (latency-bound, one warp per (image, 32 maps)) and the dense
                     // weight gradient (issue-bound, published from registers) side by side
                     constexpr int DW = G * C3::NBAND * ((C3::C + 31) / 32);

@@ -10,6 +10,7 @@ traffic.json (dram read+write bytes per launch of the captured kernel, used by b
 """
 import csv
 import io
+import re
 import json
 import os
 import shutil
@@ -30,6 +31,17 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
         "lts__t_requests_op_red.sum", "lts__t_sectors_op_red.sum", "sm__cycles_elapsed.avg", "smsp__cycles_active.avg",
         "launch__grid_size", "launch__block_size"]
+
+
+D7 = (r"^derived__(sm|smsp)__sass_thread_inst_executed_op_(ffma|fadd|fmul)_pred_on"
+      r"|^smsp__sass_thread_inst_executed_op_(ffma|fadd|fmul)_pred_on\.sum$"
+      r"|^l1tex__data_pipe_lsu_wavefronts_mem_shared(_op_ld|_op_st)?\.sum(\.pct_of_peak_sustained_elapsed)?$"
+      r"|^l1tex__data_bank_conflicts_pipe_lsu_mem_shared(_op_ld|_op_st)?\.sum$"
+      r"|^lts__t_(sectors|bytes|requests)\.sum(\.per_second|\.pct_of_peak_sustained_elapsed)?$"
+      r"|^lts__t_(sectors|requests)_srcunit_tex_op_red\.sum$|^lts__t_(sectors|requests)_op_red\.sum$"
+      r"|^l1tex__t_requests_pipe_lsu_mem_global_op_red\.sum$|^l1tex__t_sectors_pipe_lsu_mem_global_op_red\.sum$"
+      r"|^dram__bytes\.sum\.per_second$|^sm__pipe_fma_cycles_active\.avg\.pct_of_peak_sustained_(active|elapsed)$"
+      r"|^sm__pipe_fmaheavy_cycles_active|^sm__inst_executed_pipe_(fma|fmalite|fmaheavy|lsu|alu)\.avg\.pct")
 
 
 def main(tag):
@@ -68,6 +80,13 @@ def main(tag):
                     f.write(f"{k:70s} {m[k][0]:>10s} {m[k][1]}\n")
             for k in sorted(m):
                 if k.startswith("smsp__average_warps_issue_stalled") and k.endswith("_per_issue_active.ratio"):
+                    f.write(f"{k:70s} {m[k][0]:>10s} {m[k][1]}\n")
+            # SURVEY D-7 counters (names as this ncu build reports them): executed FP32 work per cycle
+            # (derived ..._x2 = thread FFMA x 2 + FADD + FMUL per cycle), shared-memory pipe
+            # utilisation, L2 throughput and the RED traffic of the hogwild publishes
+            f.write("# D-7\n")
+            for k in sorted(m):
+                if re.search(D7, k):
                     f.write(f"{k:70s} {m[k][0]:>10s} {m[k][1]}\n")
 
         def val(k):
