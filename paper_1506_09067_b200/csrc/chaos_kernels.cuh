@@ -2043,7 +2043,10 @@ __device__ __forceinline__ void fc_fwd3(const float* __restrict__ Wg, const floa
             LA.wait();
         if constexpr (MODE == kTrace) trace_dump(*ta, slot, 0, woff + c * RCH * F::IN, cb, rows(c) * F::IN);
         // RPW rows per warp pass: each activation quad loaded from shared memory feeds RPW rows
-        constexpr int RPW = 2;
+#ifndef CHAOS_FC1_RPW
+#define CHAOS_FC1_RPW 3
+#endif
+        constexpr int RPW = CHAOS_FC1_RPW;
         for (int r0 = warp * RPW; r0 < rows(c); r0 += NW * RPW) {
             float acc[RPW][G];
 #pragma unroll
@@ -2634,7 +2637,10 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                     static_assert(NRG >= 1 && (NRG - 1) * G * F1::IN <= S::SFL, "row-group partials must fit in S");
                     fc_bwd2<F1, G, NT, MODE, NRG>(a, slot, O::f1w, O::f1b, alast, hh, F1::OUT, sS, bsc, cnt, sc);
                 } else if constexpr (FCSTAGE) {
-                    constexpr int NRG = NT / (F1::IN / 4) < 4 ? NT / (F1::IN / 4) : 4;
+#ifndef CHAOS_FC1_NRG  // FC1 backward: row groups (threads per column quad)
+#define CHAOS_FC1_NRG 4
+#endif
+                    constexpr int NRG = NT / (F1::IN / 4) < CHAOS_FC1_NRG ? NT / (F1::IN / 4) : CHAOS_FC1_NRG;
                     static_assert((NRG - 1) * G * F1::IN <= S::SFL, "row-group partials must fit in S");
                     fence_async_smem();
                     wait_publish_reads();  // the FC2 publish has read its buffers; WB is free
