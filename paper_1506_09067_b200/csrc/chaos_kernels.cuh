@@ -75,6 +75,16 @@ template <class N>
 struct BigW<N, std::void_t<decltype(N::BIGW)>> {
     static constexpr bool value = N::BIGW;
 };
+// Nets whose conv2 forward runs with map groups fastest over the lanes (conv_fwd MGF) declare
+// MGF2 = true (measured per net)
+template <class N, class = void>
+struct MgfC2 {
+    static constexpr bool value = false;
+};
+template <class N>
+struct MgfC2<N, std::void_t<decltype(N::MGF2)>> {
+    static constexpr bool value = N::MGF2;
+};
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 
 // Convolution block: conv (valid, stride 1, C->M maps, KxK) -> tanh -> KPxKP max-pool (floor).
@@ -500,7 +510,10 @@ __device__ __forceinline__ float warp_sum(float v) {
 // one pooled window x one image; the KP*KP conv outputs of the window stay in registers,
 // the weights of the MT maps are warp-uniform vector loads from the staged block.
 // ------------------------------------------------------------------------------------
-template <class L, int NT>
+// MGF: map groups fastest over the lanes (a warp's lanes read a few windows' patches -- broadcasts,
+// distinct banks -- and the map groups' weight vectors) instead of windows fastest (neighbouring
+// windows 2 columns apart share banks)
+template <class L, int NT, bool MGF = false>
 __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const float* __restrict__ wsm,
                                          float* __restrict__ out, uint8_t* __restrict__ am, int cnt) {
     constexpr int MT = L::MT, KP = L::KP, K = L::K, PW = L::PW, P = L::P, MG = L::M / MT;
@@ -512,10 +525,10 @@ __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const flo
     const int total = MG * cnt * P * NSPL;
     for (int it = threadIdx.x; it < total; it += NT) {
         const int half = it % NSPL;
-        const int p = (it / NSPL) % P;
-        const int t = (it / NSPL) / P;
-        const int g = t % cnt;
-        const int mg = t / cnt;
+        const int p = MGF ? ((it / NSPL) / MG) % P : (it / NSPL) % P;
+        const int t = MGF ? 0 : (it / NSPL) / P;
+        const int g = MGF ? ((it / NSPL) / MG) / P : t % cnt;
+        const int mg = MGF ? (it / NSPL) % MG : t / cnt;
         const int pr = p / PW, pc = p - (p / PW) * PW;
         float acc[MT][KP * KP];
         {
@@ -2357,6 +2370,15 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
 #ifndef CHAOS_C3_DINP  // conv3 delta_in: the software-pipelined conv_din_winp
 #define CHAOS_C3_DINP 1
 #endif
+#ifndef CHAOS_MGF_C1  // conv forwards with map groups fastest over the lanes (conv_fwd MGF)
+#define CHAOS_MGF_C1 0
+#endif
+#ifndef CHAOS_MGF_C2
+#define CHAOS_MGF_C2 0
+#endif
+#ifndef CHAOS_MGF_C3
+#define CHAOS_MGF_C3 0
+#endif
 #ifndef CHAOS_C3_SPARSE  // conv3 backward: argmax-sparse conv_bwd_sparse (warp-uniform phase branches)
 #define CHAOS_C3_SPARSE 1
 #endif
@@ -2484,7 +2506,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
         PTIME(1);
 
         // ---------------- a2: conv -> tanh -> pool, layer by layer
-        conv_fwd<C1, NT>(sS, wb, a1, am1, cnt);
+        conv_fwd<C1, NT, CHAOS_MGF_C1>(sS, wb, a1, am1, cnt);
         float* alast = a1;
         if constexpr (NCONV >= 2) {
             fence_async_smem();
@@ -2495,7 +2517,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             L1.wait();
             TR_RE(1, 0);
             if constexpr (!BIG) TR_DUMP(0, O::c2w, wb + W2OFF, C2::BLK);
-            conv_fwd<C2, NT>(a1, wb + W2OFF, a2, am2, cnt);
+            conv_fwd<C2, NT, CHAOS_MGF_C2 || MgfC2<Net>::value>(a1, wb + W2OFF, a2, am2, cnt);
             alast = a2;
         }
         if constexpr (NCONV >= 3 && BIG) {
@@ -2513,7 +2535,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             L3.wait();
             TR_RE(2, 0);
             TR_DUMP(0, O::c3w, wb, C3::BLK);
-            conv_fwd<C3, NT>(a2, wb, a3, am3, cnt);
+            conv_fwd<C3, NT, CHAOS_MGF_C3>(a2, wb, a3, am3, cnt);
             alast = a3;
         }
         fence_async_smem();  // WB (read by the conv forward) is refilled by the async proxy next
@@ -2603,8 +2625,16 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             }
             if constexpr (MODE != kEval) {
                 if (on) {
+#if defined(CHAOS_EXPERIMENT_RCP)
+                    const float inv = __frcp_rn(1.f + r);
+#else
                     const float inv = 1.f / (1.f + r);
+#endif
+#if defined(CHAOS_EXPERIMENT_NODELTA)
+                    z[o] = e;
+#else
                     z[o] = (o != lab) ? (o == best ? inv : e * inv) : (lab == best ? -r * inv : e * inv - 1.f);
+#endif
                 }
             }
         }
@@ -2638,7 +2668,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                     fc_bwd2<F1, G, NT, MODE, NRG>(a, slot, O::f1w, O::f1b, alast, hh, F1::OUT, sS, bsc, cnt, sc);
                 } else if constexpr (FCSTAGE) {
 #ifndef CHAOS_FC1_NRG  // FC1 backward: row groups (threads per column quad)
-#define CHAOS_FC1_NRG 4
+#define CHAOS_FC1_NRG 5
 #endif
                     constexpr int NRG = NT / (F1::IN / 4) < CHAOS_FC1_NRG ? NT / (F1::IN / 4) : CHAOS_FC1_NRG;
                     static_assert((NRG - 1) * G * F1::IN <= S::SFL, "row-group partials must fit in S");
@@ -2792,14 +2822,20 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 L1.wait();
                 TR_RE(1, 1);
                 TR_DUMP(1, O::c2w, wb, C2::BLK);
-                if constexpr (C2_WTP > 0) {
-                    // transposed copy [m][C*K*K] (odd pitch) for the delta_in's lanes over input maps;
-                    // ordered before its reads by the barrier after the weight gradient
-                    static_assert(round4(C2::BLK) + C2::M * C2_WTP <= S::WBUF, "transposed W2 must fit in WB");
+                // transposed W2 copy [m][C*K*K] (odd pitch) for the delta_in's lanes over input maps, made
+                // by the warps the weight gradient leaves idle (or here when it uses them all); ordered
+                // before the delta_in's reads by the barrier after the weight gradient
+                constexpr int GWW = (C2::M * (C2::C / (CHAOS_C2_GWM > 0 ? CHAOS_C2_GWM : 1)) + 31) / 32;
+                constexpr bool WT_OVERLAP = C2_WTP > 0 && C2::MS < 0 && CHAOS_C2_GWM > 0 && GWW < NT / 32 &&
+                                            !CHAOS_C2_PAR;
+                auto transpose_w2 = [&](int t0, int nthr) {
+                    static_assert(C2_WTP == 0 || round4(C2::BLK) + C2::M * C2_WTP <= S::WBUF,
+                                  "transposed W2 must fit in WB");
                     float* wbt = wb + round4(C2::BLK);
-                    for (int e = threadIdx.x; e < C2::ROWS * C2::M; e += NT)
+                    for (int e = static_cast<int>(threadIdx.x) - t0; e < C2::ROWS * C2::M; e += nthr)
                         wbt[(e % C2::M) * C2_WTP + e / C2::M] = wb[(e / C2::M) * C2::MP + e % C2::M];
-                }
+                };
+                if constexpr (C2_WTP > 0 && !WT_OVERLAP) transpose_w2(0, NT);
                 PTIME(11);
                 TR_PB(1);
                 if constexpr (CHAOS_C2_PAR && C2::MS < 0 && CHAOS_C2_GWM > 0 && C2::NBAND > 1 && C2::GWIN == 0) {
@@ -2840,7 +2876,12 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                     PTIME(12);
                     PTIME(13);
                 } else {
-                if constexpr (C2::MS < 0 && CHAOS_C2_GWM > 0)  // lanes over output maps, NPT input maps per thread
+                if constexpr (WT_OVERLAP) {  // the gradient on warps [0, GWW), the W2 transpose on the others
+                    if (threadIdx.x < GWW * 32)
+                        conv_gw_m<C2, NT, MODE, CHAOS_C2_GWM, 0, GWW>(a, slot, a1, sS, am2, O::c2w, cnt, sc);
+                    else
+                        transpose_w2(GWW * 32, NT - GWW * 32);
+                } else if constexpr (C2::MS < 0 && CHAOS_C2_GWM > 0)  // lanes over output maps, NPT maps per thread
                     conv_gw_m<C2, NT, MODE, CHAOS_C2_GWM>(a, slot, a1, sS, am2, O::c2w, cnt, sc);
                 else if constexpr (C2::MS < 0)  // generic, lanes over output maps, published from registers
                     conv_gw<C2, NT, MODE, false>(a, slot, a1, sS, am2, nullptr, O::c2w, cnt, sc);
