@@ -6,7 +6,7 @@
 //   D[p][m] = sum_k A[p][k] B[m][k],  p = conv position (22x22 = 484 -> M = 512 = 4 tiles of 128),
 //   k = (input map n, tap i, tap j) (20 x 25 = 500 -> K = 512), m = output map (60 -> N = 64).
 //
-// One CTA per image.  A is the im2col of the image, built slab by slab (KS = 32 of K) in shared
+// One CTA per image.  A is the im2col of the image, built slab by slab (KS = 16 of K) in shared
 // memory in the canonical K-major no-swizzle layout (8-row x 16-byte core matrices: SBO = 128 B
 // between 8-row groups, LBO = the K-chunk stride); B likewise.  Precision modes: 1 = one TF32 pass
 // (10-bit mantissas), 3 = 3xTF32 (a = a_hi + a_lo: a_hi b_hi + a_hi b_lo + a_lo b_hi).  One thread
@@ -23,14 +23,23 @@
 #include <vector>
 #include <cuda_runtime.h>
 
+#ifndef LARGE_NET  // Table I large net conv2 (default) or, with -DLARGE_NET, configs[3]'s conv2
 constexpr int C = 20, H = 26, W = 26, M = 60, K = 5, OH = H - K + 1, OW = W - K + 1;  // 22 x 22
 constexpr int NPOS = OH * OW, KDIM = C * K * K;                                     // 484, 500
-constexpr int MP = 512, NP = 64, KP = 512, KS = 32, NSLAB = KP / KS, MT = MP / 128;
+constexpr int MP = 512, NP = 64, KP = 512, KS = 16, NSLAB = KP / KS, MT = MP / 128;
+#else  // 20 x 13 x 13 -> 60 maps, 3x3: the 10 x 10 outputs the floor pool uses (one image per CTA here)
+constexpr int C = 20, H = 13, W = 13, M = 60, K = 3, OH = 10, OW = 10;
+constexpr int NPOS = OH * OW, KDIM = C * K * K;                                     // 100, 180
+constexpr int MP = 128, NP = 64, KP = 192, KS = 16, NSLAB = KP / KS, MT = MP / 128;
+#endif
 constexpr int NT = 512;
-// shared memory: A slab per precision part [tile][kc][rowgroup][8][16 B] and B slab
-constexpr int A_TILE_BYTES = (KS * 4 / 16) * 16 * 128;  // 8 kc x 16 rowgroups x 128 B = 16 KB
-constexpr int A_BYTES = MT * A_TILE_BYTES;                // 64 KB
-constexpr int B_BYTES = (KS * 4 / 16) * (NP / 8) * 128;   // 8 kc x 8 rowgroups x 128 B = 8 KB
+// shared memory: A slab per precision part [tile][kc][rowgroup][8][16 B] and B slab; the image
+constexpr int A_TILE_BYTES = (KS * 4 / 16) * 16 * 128;  // 4 kc x 16 rowgroups x 128 B = 8 KB
+constexpr int A_BYTES = MT * A_TILE_BYTES;                // 32 KB
+constexpr int B_BYTES = (KS * 4 / 16) * (NP / 8) * 128;   // 4 kc x 8 rowgroups x 128 B = 4 KB
+constexpr int X_BYTES = C * H * W * 4;                    // 54,080 B
+constexpr int NPART = 3;                                  // tf32 parts of each operand (x = p0 + p1 + p2)
+constexpr int SMEM_BYTES = NPART * (A_BYTES + B_BYTES) + X_BYTES + 64;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -51,19 +60,40 @@ __device__ __forceinline__ int kmaj_off(int r, int k, int R) {
     return (k >> 2) * (R / 8) * 128 + (r >> 3) * 128 + (r & 7) * 16 + (k & 3) * 4;
 }
 
+__device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                 "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// prec: 1 = one TF32 pass; 3 = 3xTF32 (p0 q0 + p0 q1 + p1 q0); 6 = three-way split, every term of
+// order <= 2 (p0q0, p0q1, p1q0, p0q2, p1q1, p2q0: the parts hold 3 x 11 mantissa bits >= fp32's 24)
 __global__ void __launch_bounds__(NT, 1)
 tc_conv2(const float* __restrict__ X, const float* __restrict__ Wt, const float* __restrict__ bias,
          float* __restrict__ out, int prec, long long* cycles) {
     extern __shared__ __align__(1024) unsigned char sm[];
-    unsigned char* Ahi = sm;
-    unsigned char* Alo = sm + A_BYTES;
-    unsigned char* Bhi = sm + 2 * A_BYTES;
-    unsigned char* Blo = Bhi + B_BYTES;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(Blo + B_BYTES);
+    unsigned char* Ap[NPART];
+    unsigned char* Bp[NPART];
+    for (int q = 0; q < NPART; ++q) {
+        Ap[q] = sm + q * A_BYTES;
+        Bp[q] = sm + NPART * A_BYTES + q * B_BYTES;
+    }
+    float* xs = reinterpret_cast<float*>(sm + NPART * (A_BYTES + B_BYTES));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + NPART * (A_BYTES + B_BYTES) + X_BYTES);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
     const float* x = X + (size_t)blockIdx.x * C * H * W;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // prec 13: 3xTF32 with every slab accumulated afresh in TMEM and the slab sums added in fp32
+    // registers (round to nearest) -- isolates the tensor core's own accumulation error
+    const bool chunked = prec == 13;
+    if (chunked) prec = 3;
+    const int nparts = prec == 6 ? 3 : (prec == 3 ? 2 : 1);
+    float racc[MT][16];
+    for (int t = 0; t < MT; ++t)
+        for (int q = 0; q < 16; ++q) racc[t][q] = 0.f;
     long long t0 = clock64(), t_build = 0, t_mma = 0;
+    for (int e = tid; e < C * H * W / 4; e += NT)  // the image, once (16-B loads)
+        reinterpret_cast<float4*>(xs)[e] = reinterpret_cast<const float4*>(x)[e];
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "n"(MT * NP));
@@ -82,27 +112,47 @@ tc_conv2(const float* __restrict__ X, const float* __restrict__ Wt, const float*
     uint32_t phase = 0;
     for (int s = 0; s < NSLAB; ++s) {
         long long tb = clock64();
-        // im2col slab: A[p][k0 + kk] for p < 512, kk < 32 (hi and lo parts)
-        for (int e = tid; e < MP * KS; e += NT) {
-            const int p = e / KS, kk = e % KS, k = s * KS + kk;
-            float v = 0.f;
-            if (p < NPOS && k < KDIM) {
-                const int n = k / 25, i = (k % 25) / 5, j = k % 5, y = p / OW, xx = p % OW;
-                v = x[(n * H + y + i) * W + xx + j];
+        // im2col slab, one 16-B chunk (4 consecutive k of one row) per item: item = (kc, row) with
+        // rows fastest, so consecutive threads store consecutive 16-B chunks of a core-matrix column
+        for (int e = tid; e < (KS / 4) * MP; e += NT) {
+            const int p = e % MP, kc = e / MP;
+            uint32_t part[NPART][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int k = s * KS + kc * 4 + u;
+                float v = 0.f;
+                if (p < NPOS && k < KDIM) {
+                    const int n = k / (K * K), r25 = k - n * (K * K), i = r25 / K, j = r25 - i * K, y = p / OW, xx = p - y * OW;
+                    v = xs[(n * H + y + i) * W + xx + j];
+                }
+                float rem = v;
+#pragma unroll
+                for (int q = 0; q < NPART; ++q) {
+                    part[q][u] = tf32_hi(rem);
+                    rem -= __uint_as_float(part[q][u]);
+                }
             }
-            const uint32_t hi = tf32_hi(v);
-            const uint32_t lo = tf32_hi(v - __uint_as_float(hi));
             const int t = p >> 7, r = p & 127;
-            *reinterpret_cast<uint32_t*>(Ahi + t * A_TILE_BYTES + kmaj_off(r, kk, 128)) = hi;
-            *reinterpret_cast<uint32_t*>(Alo + t * A_TILE_BYTES + kmaj_off(r, kk, 128)) = lo;
+            const int off = t * A_TILE_BYTES + kc * 16 * 128 + (r >> 3) * 128 + (r & 7) * 16;
+            for (int q = 0; q < nparts; ++q)
+                *reinterpret_cast<uint4*>(Ap[q] + off) = make_uint4(part[q][0], part[q][1], part[q][2], part[q][3]);
         }
-        for (int e = tid; e < NP * KS; e += NT) {
-            const int m = e / KS, kk = e % KS, k = s * KS + kk;
-            const float v = (m < M && k < KDIM) ? Wt[m * KDIM + k] : 0.f;
-            const uint32_t hi = tf32_hi(v);
-            const uint32_t lo = tf32_hi(v - __uint_as_float(hi));
-            *reinterpret_cast<uint32_t*>(Bhi + kmaj_off(m, kk, NP)) = hi;
-            *reinterpret_cast<uint32_t*>(Blo + kmaj_off(m, kk, NP)) = lo;
+        for (int e = tid; e < (KS / 4) * NP; e += NT) {
+            const int m = e % NP, kc = e / NP;
+            uint32_t part[NPART][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int k = s * KS + kc * 4 + u;
+                float rem = (m < M && k < KDIM) ? Wt[m * KDIM + k] : 0.f;
+#pragma unroll
+                for (int q = 0; q < NPART; ++q) {
+                    part[q][u] = tf32_hi(rem);
+                    rem -= __uint_as_float(part[q][u]);
+                }
+            }
+            const int off = kc * (NP / 8) * 128 + (m >> 3) * 128 + (m & 7) * 16;
+            for (int q = 0; q < nparts; ++q)
+                *reinterpret_cast<uint4*>(Bp[q] + off) = make_uint4(part[q][0], part[q][1], part[q][2], part[q][3]);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
         asm volatile("tcgen05.fence::before_thread_sync;");
@@ -112,24 +162,20 @@ tc_conv2(const float* __restrict__ X, const float* __restrict__ Wt, const float*
         t_build += tm - tb;
         if (tid == 0) {
             const uint32_t a_lbo = 16 * 128, b_lbo = (NP / 8) * 128;  // next 16-B K chunk
+            // (A part, B part) pairs in increasing magnitude order of their products' weight
+            const int pa6[6] = {2, 1, 0, 1, 0, 0}, pb6[6] = {0, 1, 2, 0, 1, 0};
+            const int pa3[3] = {1, 0, 0}, pb3[3] = {0, 1, 0};
+            const int nt = prec == 6 ? 6 : (prec == 3 ? 3 : 1);
             for (int t = 0; t < MT; ++t) {
                 for (int ks = 0; ks < KS / 8; ++ks) {  // K = 8 tf32 = 2 chunks per instruction
                     const uint32_t aoff = t * A_TILE_BYTES + ks * 2 * a_lbo, boff = ks * 2 * b_lbo;
-                    const uint64_t ah = sdesc(smem_u32(Ahi) + aoff, a_lbo, 128), al = sdesc(smem_u32(Alo) + aoff, a_lbo, 128);
-                    const uint64_t bh = sdesc(smem_u32(Bhi) + boff, b_lbo, 128), bl = sdesc(smem_u32(Blo) + boff, b_lbo, 128);
                     const uint32_t d = tmem + t * NP;
-                    const uint32_t acc0 = (s > 0 || ks > 0) ? 1u : 0u;
-                    // hi x hi first (initialises), then the two cross terms (3xTF32)
-                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-                                 "l"(ah), "l"(bh), "r"(idesc), "r"(acc0));
-                    if (prec == 3) {
-                        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                                     "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-                                     "l"(ah), "l"(bl), "r"(idesc), "r"(1u));
-                        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                                     "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-                                     "l"(al), "l"(bh), "r"(idesc), "r"(1u));
+                    for (int term = 0; term < nt; ++term) {
+                        const int qa = prec == 6 ? pa6[term] : (prec == 3 ? pa3[term] : 0);
+                        const int qb = prec == 6 ? pb6[term] : (prec == 3 ? pb3[term] : 0);
+                        const uint32_t acc = ((s > 0 && !chunked) || ks > 0 || term > 0) ? 1u : 0u;
+                        mma_tf32(d, sdesc(smem_u32(Ap[qa]) + aoff, a_lbo, 128), sdesc(smem_u32(Bp[qb]) + boff, b_lbo, 128),
+                                 idesc, acc);
                     }
                 }
             }
@@ -147,11 +193,36 @@ tc_conv2(const float* __restrict__ X, const float* __restrict__ Wt, const float*
             phase ^= 1u;
         }
         asm volatile("tcgen05.fence::after_thread_sync;");
+        if (chunked) {  // warp w: TMEM lanes 32 (w % 4) .., columns 16 (w / 4) .. of every tile
+            for (int t = 0; t < MT; ++t) {
+                uint32_t v[16];
+                const uint32_t taddr = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + t * NP + 16 * (warp >> 2);
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                             : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                               "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+                               "=r"(v[14]), "=r"(v[15])
+                             : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;");
+                for (int q = 0; q < 16; ++q) racc[t][q] += __uint_as_float(v[q]);
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncthreads();  // every warp has read the slab sums before the next slab's MMAs overwrite them
+            asm volatile("tcgen05.fence::after_thread_sync;");
+        }
         t_mma += clock64() - tm;
+    }
+    if (chunked) {
+        for (int t = 0; t < MT; ++t) {
+            const int p = t * 128 + 32 * (warp & 3) + lane;
+            for (int q = 0; q < 16; ++q) {
+                const int m = 16 * (warp >> 2) + q;
+                if (p < NPOS && m < M) out[((size_t)blockIdx.x * M + m) * NPOS + p] = racc[t][q] + bias[m];
+            }
+        }
     }
     // epilogue: warp w (< 4) reads TMEM lanes [32w, 32w + 32) = rows of each M tile
     long long te = clock64();
-    if (warp < 4) {
+    if (warp < 4 && !chunked) {
         for (int t = 0; t < MT; ++t) {
             for (int c0 = 0; c0 < NP; c0 += 16) {
                 uint32_t v[16];
@@ -238,7 +309,7 @@ int main(int argc, char** argv) {
     CK(cudaMemcpy(dX, X.data(), X.size() * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dW, Wt.data(), Wt.size() * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice));
-    const int smem = 2 * A_BYTES + 2 * B_BYTES + 64;
+    const int smem = SMEM_BYTES;
     CK(cudaFuncSetAttribute(tc_conv2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
@@ -262,6 +333,34 @@ int main(int argc, char** argv) {
     }
     std::vector<long long> c3(nimg * 4);
     CK(cudaMemcpy(c3.data(), dc, c3.size() * 8, cudaMemcpyDeviceToHost));
+    float *dO6;
+    CK(cudaMalloc(&dO6, osz * 4));
+    float ms6 = 0;
+    for (int rep = 0; rep < 2; ++rep) {
+        cudaEventRecord(e0);
+        tc_conv2<<<nimg, NT, smem>>>(dX, dW, dB, dO6, 6, rep ? dc : nullptr);
+        cudaEventRecord(e1);
+        CK(cudaEventSynchronize(e1));
+        cudaEventElapsedTime(&ms6, e0, e1);
+    }
+    std::vector<long long> c6(nimg * 4);
+    CK(cudaMemcpy(c6.data(), dc, c6.size() * 8, cudaMemcpyDeviceToHost));
+    float *dO13;
+    CK(cudaMalloc(&dO13, osz * 4));
+    float ms13 = 0;
+    std::vector<long long> c13(nimg * 4);
+    for (int rep = 0; rep < 2; ++rep) {
+        cudaEventRecord(e0);
+        tc_conv2<<<nimg, NT, smem>>>(dX, dW, dB, dO13, 13, rep ? dc : nullptr);
+        cudaEventRecord(e1);
+        CK(cudaEventSynchronize(e1));
+        cudaEventElapsedTime(&ms13, e0, e1);
+    }
+    CK(cudaMemcpy(c13.data(), dc, c13.size() * 8, cudaMemcpyDeviceToHost));
+    std::vector<float> O13(osz);
+    CK(cudaMemcpy(O13.data(), dO13, osz * 4, cudaMemcpyDeviceToHost));
+    std::vector<float> O6(osz);
+    CK(cudaMemcpy(O6.data(), dO6, osz * 4, cudaMemcpyDeviceToHost));
     for (int rep = 0; rep < 2; ++rep) {
         cudaEventRecord(e0);
         ffma_conv2<<<nimg, 384>>>(dX, dW, dB, dOf, rep ? dcf : nullptr);
@@ -277,7 +376,7 @@ int main(int argc, char** argv) {
     CK(cudaMemcpy(O3.data(), dO3, osz * 4, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(Of.data(), dOf, osz * 4, cudaMemcpyDeviceToHost));
     // float64 reference on a sample of images: worst |err| / max(|ref|, 1e-2 max|ref|) (the R9 form)
-    double w1 = 0, w3 = 0, wf = 0, n1 = 0, n3 = 0, nf = 0, nr = 0;
+    double w1 = 0, w3 = 0, w6 = 0, w13 = 0, wf = 0, n1 = 0, n3 = 0, n6 = 0, n13 = 0, nf = 0, nr = 0;
     const int ncheck = nimg < 8 ? nimg : 8;
     for (int b = 0; b < ncheck; ++b) {
         std::vector<double> ref(M * NPOS);
@@ -299,6 +398,10 @@ int main(int argc, char** argv) {
             const size_t o = (size_t)b * M * NPOS + e;
             w1 = std::fmax(w1, std::fabs(O1[o] - r) / tol);
             w3 = std::fmax(w3, std::fabs(O3[o] - r) / tol);
+            w6 = std::fmax(w6, std::fabs(O6[o] - r) / tol);
+            w13 = std::fmax(w13, std::fabs(O13[o] - r) / tol);
+            n13 += (O13[o] - r) * (O13[o] - r);
+            n6 += (O6[o] - r) * (O6[o] - r);
             wf = std::fmax(wf, std::fabs(Of[o] - r) / tol);
             n1 += (O1[o] - r) * (O1[o] - r);
             n3 += (O3[o] - r) * (O3[o] - r);
@@ -312,7 +415,7 @@ int main(int argc, char** argv) {
         std::sort(x.begin(), x.end());
         return x[x.size() / 2];
     };
-    printf("conv2 forward of the Table I large net (20x26x26 -> 60x22x22, 5x5; %d images, one CTA each)\n", nimg);
+    printf("conv2 forward (%dx%dx%d -> %dx%dx%d used, %dx%d; K = %d; %d images, one CTA each)\n", C, H, W, M, OH, OW, K, K, KDIM, nimg);
     printf("  %-28s %10s %10s %10s %10s | %12s %12s\n", "path", "build cyc", "mma cyc", "epi cyc", "total cyc",
            "max rel err", "norm rel err");
     printf("  %-28s %10lld %10lld %10lld %10lld | %12.3g %12.3g   (%.3f ms for all images)\n",
@@ -320,6 +423,10 @@ int main(int argc, char** argv) {
            std::sqrt(n1 / nr), ms[0]);
     printf("  %-28s %10lld %10lld %10lld %10lld | %12.3g %12.3g   (%.3f ms)\n", "tcgen05 kind::tf32 x3 (3xTF32)",
            med(c3, 4, 0), med(c3, 4, 1), med(c3, 4, 2), med(c3, 4, 3), w3, std::sqrt(n3 / nr), ms[1]);
+    printf("  %-28s %10lld %10lld %10lld %10lld | %12.3g %12.3g   (%.3f ms)\n", "tcgen05 kind::tf32 x6 (3-way split)",
+           med(c6, 4, 0), med(c6, 4, 1), med(c6, 4, 2), med(c6, 4, 3), w6, std::sqrt(n6 / nr), ms6);
+    printf("  %-28s %10lld %10lld %10lld %10lld | %12.3g %12.3g   (%.3f ms)\n", "3xTF32, slab sums in fp32 regs",
+           med(c13, 4, 0), med(c13, 4, 1), med(c13, 4, 2), med(c13, 4, 3), w13, std::sqrt(n13 / nr), ms13);
     printf("  %-28s %10s %10s %10s %10lld | %12.3g %12.3g   (%.3f ms, 384 threads, naive loop order)\n",
            "FFMA direct (fp32)", "-", "-", "-", med(cf, 1, 0), wf, std::sqrt(nf / nr), ms[2]);
     printf("  errors vs float64: max |err| / max(|ref|, 1e-2 max|ref|) (R9 form; bound 1e-4), norm-wise (bound 1e-5)\n");
