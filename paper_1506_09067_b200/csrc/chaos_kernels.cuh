@@ -36,7 +36,7 @@ namespace chaos {
 
 constexpr int kClasses = 10;
 constexpr int kZStride = 16;  // logits / output-delta row stride in shared memory
-constexpr int kHdrBytes = 256;
+constexpr int kHdrBytes = 512;  // mbarriers, claim word, labels, losses; [256, 512): tensor-core mbarriers
 constexpr int kBiasScratch = 256;  // floats: FC bias-gradient scratch
 
 // kTrace: hogwild (kHogwild semantics) that also records, per claimed group and weighted layer,
@@ -77,6 +77,15 @@ struct BigW<N, std::void_t<decltype(N::BIGW)>> {
 };
 // Nets whose conv2 forward runs with map groups fastest over the lanes (conv_fwd MGF) declare
 // MGF2 = true (measured per net)
+// Nets whose conv2 forward runs on the tensor cores (conv_fwd_tc2) declare TC2 = true
+template <class N, class = void>
+struct TcC2 {
+    static constexpr bool value = false;
+};
+template <class N>
+struct TcC2<N, std::void_t<decltype(N::TC2)>> {
+    static constexpr bool value = N::TC2;
+};
 template <class N, class = void>
 struct MgfC2 {
     static constexpr bool value = false;
@@ -586,6 +595,227 @@ __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const flo
             if constexpr (KP > 1) am[o] = static_cast<uint8_t>(arg);
         }
     }
+}
+
+// ------------------------------------------------------------------------------------
+// PHASE(conv_fwd_tc2) conv -> tanh -> max-pool forward of a 3x3 / 2x2-pool layer on the
+// 5th-generation tensor cores: the implicit GEMM
+//   Z_q[row][m] = sum_k A_q[row][k] Wt[k][m],  one 128-row tile per pool phase q, row = (image g,
+//   pool window w), k = (input map n, tap i, tap j)
+// as tcgen05.mma kind::tf32, M = 128 rows per tile, N = 64 maps, K = 8 per instruction, with
+// 3xTF32 operands (x = x_hi + x_lo, terms hi*hi + hi*lo + lo*hi) and the accumulation split into
+// two TMEM chains (K < 96 and K >= 96) added in fp32 registers: long tensor-core accumulation
+// chains lose accuracy, short ones are more accurate than the FFMA path
+// (scripts/microbench/tc_conv2.cu, profiles/r3/tcgen05_conv2.txt).
+// Producer warps (all but the last) build the im2col operand slabs (K = 8 per stage) in shared
+// memory in the canonical K-major no-swizzle layout (8-row x 16-byte core matrices) -- two stages,
+// full / empty mbarriers; one thread of the last warp issues the MMAs and commits each stage back
+// to its producers (the two chains' stages alternate, so consecutive MMAs feed independent
+// accumulators).  Then warps 0-15 read the accumulators (tcgen05.ld, TMEM lane quarter = warp % 4:
+// 32 windows; warp / 4: 16 maps), add the chains and the bias, max-pool over the 4 phase tiles in
+// registers (first maximum in phase order, R4), apply tanh and write the pooled activations and
+// argmaxes.
+// ------------------------------------------------------------------------------------
+// round to TF32 (10 explicit mantissa bits), nearest, ties away from zero (= cvt.rna.tf32.f32) with
+// two integer ops on the sign-magnitude bits instead of the conversion unit (finite inputs)
+__device__ __forceinline__ uint32_t tf32_rna(float x) { return (__float_as_uint(x) + 0x1000u) & 0xffffe000u; }
+// canonical K-major SWIZZLE_NONE shared-memory matrix descriptor (sm_100 version 1)
+__device__ __forceinline__ uint64_t umma_sdesc(uint32_t addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+    return (uint64_t)((addr >> 4) & 0x3fffu) | ((uint64_t)((lbo_bytes >> 4) & 0x3fffu) << 16) |
+           ((uint64_t)((sbo_bytes >> 4) & 0x3fffu) << 32) | (1ull << 46);
+}
+__device__ __forceinline__ void umma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                 "l"(a), "l"(b), "r"(idesc), "r"(acc)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+constexpr int kTcStageBytes = 20480;  // A (hi, lo: 2 x 8 KB) + B (hi, lo: 2 x 2 KB) of one K = 8 slab
+constexpr int kTcCols = 512;          // TMEM columns: 2 chains x 4 tiles x 64 maps
+
+// Four operand stages of kTcStageBytes: two at stg (followed by a small offset table) and one each at
+// stg2 / stg3 (dead shared-memory regions of the caller; stg3 may be `out`, written only after the
+// last MMA has read it).  tcbar: 2 * NS + 1 mbarriers (full[NS], empty[NS], done).
+template <class L, int NT, int G>
+__device__ __forceinline__ void conv_fwd_tc2(const float* __restrict__ in, const float* __restrict__ wsm,
+                                             float* __restrict__ out, uint8_t* __restrict__ am, int cnt,
+                                             uint32_t tmem, unsigned char* stg, unsigned char* stg2, unsigned char* stg3,
+                                             uint64_t* tcbar, uint32_t& done_phase,
+                                             unsigned long long* tslot = nullptr) {
+    // tslot (instrumented builds): [0] += producer thread 0's waits for free stages, [1] += the MMA
+    // thread's waits for filled stages
+    constexpr int K = L::K, KK = L::KK, C = L::C, M = L::M, W = L::W, HW = L::H * L::W, P = L::P, PW = L::PW;
+    constexpr int ROWS = G * P * 4, KD = C * KK, NSL = (KD + 15) / 16 * 2, PROW = 256, NPASS = 2;
+    constexpr int A_PART = 2 * (PROW / 8) * 128, B_PART = 2 * 8 * 128;
+    constexpr int NPW = NT / 32 - 1;  // producer warps; the last warp issues the MMAs
+    static_assert(L::KP == 2 && K == 3 && M <= 64 && ROWS <= NPASS * PROW && 2 * A_PART + 2 * B_PART == kTcStageBytes,
+                  "3x3 conv, 2x2 pool, <= 64 maps, 4 tiles of 128 rows");
+    static_assert(2 * PROW + 64 <= NPW * 32, "one producer thread per A chunk and per B row");
+    static_assert(NSL % 2 == 0, "two accumulation chains of equal length");
+    constexpr int NS = 4;         // operand stages in flight
+    uint64_t* full = tcbar;       // [NS]: producer warps arrive
+    uint64_t* empty = tcbar + NS; // [NS]: the MMA commit arrives
+    uint64_t* done = tcbar + 2 * NS;  // all MMAs complete
+    auto stage = [&](int b) -> unsigned char* { return b < 2 ? stg + b * kTcStageBytes : (b == 2 ? stg2 : stg3); };
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // k -> input offset n*H*W + i*W + j (-1 beyond K), 16-B aligned groups of 4 (4 consecutive k
+    // of one 16-B chunk with one vector load); placed after the two stages
+    int* koff = reinterpret_cast<int*>(stg + 2 * kTcStageBytes);
+    for (int k = threadIdx.x; k < NSL * 8; k += NT) {
+        const int n = k / KK, t = k - n * KK, i = t / K, j = t - i * K;
+        koff[k] = k < KD ? n * HW + i * W + j : -1;
+    }
+    __syncthreads();
+    if (warp < NPW) {
+        // fixed roles: threads [0, 2*PROW) build A chunk (row r, kc); the next 64 build B rows (both kc)
+        const int tid = threadIdx.x;
+        const bool isA = tid < 2 * PROW, isB = !isA && tid < 2 * PROW + 64;
+        const int r = tid % PROW, kc = (tid / PROW) & 1, mB = tid - 2 * PROW;
+        const float* ib = nullptr;
+#pragma unroll 1
+        for (int f = 0; f < NPASS * NSL; ++f) {
+            const int b = f % NS, u = f / NS, h = f / NSL, jj = f % NSL;
+            // alternate the two accumulation chains (K < 96, K >= 96) so consecutive stages feed
+            // independent accumulators (4 in flight instead of 2)
+            const int sl = (jj & 1) ? NSL / 2 + (jj >> 1) : (jj >> 1);
+            if (jj == 0 && isA) {  // this pass's row: tile = pool phase, row = (image, window) -> patch origin
+                const int ph = 2 * h + r / 128, Rw = r % 128, g = Rw / P;
+                ib = nullptr;
+                if (Rw < G * P && g < cnt) {
+                    const int w = Rw % P;
+                    ib = in + g * L::IN_SZ + (2 * (w / PW) + (ph >> 1)) * W + 2 * (w % PW) + (ph & 1);
+                }
+            }
+#ifdef CHAOS_TIMING
+            const long long tw0 = clock64();
+#endif
+            if (u > 0) mbar_wait(empty + b, static_cast<uint32_t>(u - 1) & 1u);
+#ifdef CHAOS_TIMING
+            if (threadIdx.x == 0 && tslot) tslot[0] += clock64() - tw0;
+#endif
+            unsigned char* st = stage(b);
+            if (isA) {
+                const int4 ko = reinterpret_cast<const int4*>(koff)[sl * 2 + kc];
+                const int kq[4] = {ko.x, ko.y, ko.z, ko.w};
+                uint32_t hi[4], lo[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float v = (ib && kq[q] >= 0) ? ib[kq[q]] : 0.f;
+                    hi[q] = tf32_rna(v);
+                    lo[q] = tf32_rna(v - __uint_as_float(hi[q]));
+                }
+                const int off = kc * (PROW / 8) * 128 + (r >> 3) * 128 + (r & 7) * 16;
+                *reinterpret_cast<uint4*>(st + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                *reinterpret_cast<uint4*>(st + A_PART + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+            } else if (isB) {
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    uint32_t hi[4], lo[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int k = sl * 8 + c * 4 + q;
+                        const float v = (mB < M && k < KD) ? wsm[k * L::MP + mB] : 0.f;
+                        hi[q] = tf32_rna(v);
+                        lo[q] = tf32_rna(v - __uint_as_float(hi[q]));
+                    }
+                    const int off = c * 8 * 128 + (mB >> 3) * 128 + (mB & 7) * 16;
+                    *reinterpret_cast<uint4*>(st + 2 * A_PART + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                    *reinterpret_cast<uint4*>(st + 2 * A_PART + B_PART + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                }
+            }
+            fence_async_smem();  // these generic writes -> the tensor core's (async proxy) reads
+            __syncwarp();
+            if (lane == 0) mbar_arrive(full + b);
+        }
+    } else if (lane == 0) {
+        // kind::tf32, D f32, A and B TF32, both K-major, N = 64, M = 128
+        constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+#pragma unroll 1
+        for (int f = 0; f < NPASS * NSL; ++f) {
+            const int b = f % NS, u = f / NS, h = f / NSL, jj = f % NSL;
+            // alternate the two accumulation chains (K < 96, K >= 96) so consecutive stages feed
+            // independent accumulators (4 in flight instead of 2)
+            const int sl = (jj & 1) ? NSL / 2 + (jj >> 1) : (jj >> 1);
+#ifdef CHAOS_TIMING
+            const long long tw0 = clock64();
+#endif
+            mbar_wait(full + b, static_cast<uint32_t>(u) & 1u);
+#ifdef CHAOS_TIMING
+            if (tslot) tslot[1] += clock64() - tw0;
+#endif
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t sb = smem_u32(stage(b));
+            const int chain = sl < NSL / 2 ? 0 : 1, first = (sl % (NSL / 2)) == 0;
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                const uint32_t d = tmem + chain * 256 + (2 * h + t) * 64;
+                const uint32_t a0 = sb + t * 16 * 128, a1 = a0 + A_PART;
+                const uint32_t b0 = sb + 2 * A_PART, b1 = b0 + B_PART;
+                const uint32_t alb = (PROW / 8) * 128, blb = 8 * 128;
+                umma_tf32(d, umma_sdesc(a0, alb, 128), umma_sdesc(b0, blb, 128), idesc, first ? 0u : 1u);
+                umma_tf32(d, umma_sdesc(a0, alb, 128), umma_sdesc(b1, blb, 128), idesc, 1u);
+                umma_tf32(d, umma_sdesc(a1, alb, 128), umma_sdesc(b0, blb, 128), idesc, 1u);
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             smem_u32(empty + b))
+                         : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(done))
+                     : "memory");
+    }
+    mbar_wait(done, done_phase);
+    done_phase ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#ifdef CHAOS_TIMING
+    const long long te0 = clock64();
+#endif
+    if (warp < 16) {  // TMEM lane quarter = warp % 4 (windows), 16 output maps per warp = warp / 4
+        const int qd = warp & 3, cb = warp >> 2;
+        const int Rw = 32 * qd + lane, g = Rw / P, w = Rw % P;
+        const bool valid = Rw < G * P && g < cnt;
+#pragma unroll 1
+        for (int c0 = 16 * cb; c0 < 16 * cb + 16; c0 += 8) {
+            uint32_t v[4][2][8];  // [phase tile][chain][column]
+            const uint32_t ta = tmem + (static_cast<uint32_t>(32 * qd) << 16) + c0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int ch = 0; ch < 2; ++ch)
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                                 : "=r"(v[q][ch][0]), "=r"(v[q][ch][1]), "=r"(v[q][ch][2]), "=r"(v[q][ch][3]),
+                                   "=r"(v[q][ch][4]), "=r"(v[q][ch][5]), "=r"(v[q][ch][6]), "=r"(v[q][ch][7])
+                                 : "r"(ta + ch * 256 + q * 64));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const int m = c0 + c;
+                const float bm = m < M ? wsm[L::WFL + m] : 0.f;
+                float best = (__uint_as_float(v[0][0][c]) + __uint_as_float(v[0][1][c])) + bm;
+                int arg = 0;
+#pragma unroll
+                for (int q = 1; q < 4; ++q) {  // first strict maximum in phase order wins (R4)
+                    const float zq = (__uint_as_float(v[q][0][c]) + __uint_as_float(v[q][1][c])) + bm;
+                    if (zq > best) {
+                        best = zq;
+                        arg = q;
+                    }
+                }
+                if (valid && m < M) {
+                    const int o = g * L::OUT_SZ + m * P + w;
+                    out[o] = tanhf(best);
+                    am[o] = static_cast<uint8_t>(arg);
+                }
+            }
+        }
+    }
+#ifdef CHAOS_TIMING
+    if (threadIdx.x == 0 && tslot) tslot[2] += clock64() - te0;  // the epilogue (warp 0's view)
+#endif
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
 
 // ------------------------------------------------------------------------------------
@@ -2385,6 +2615,12 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
 #ifndef CHAOS_C2_PAR  // conv2 backward: delta_in (window-row bands, PB >= 2) beside conv_gw_m on the other warps
 #define CHAOS_C2_PAR 0
 #endif
+#ifndef CHAOS_C2_TC  // conv2 forward on the tensor cores (conv_fwd_tc2) for nets that declare TC2:
+#define CHAOS_C2_TC 0  // experimental, parity-green, measured slower (DESIGN.md §6 "tensor cores")
+#endif
+    // (G images fill the S and A2 regions enough to hold one operand stage each; else the FFMA path)
+    constexpr bool TC2 = CHAOS_C2_TC && TcC2<Net>::value && NCONV >= 3 && !BIG && S::SFL * 4 >= kTcStageBytes &&
+                         G * C2::OUT_SZ * 4 >= kTcStageBytes;
     constexpr bool C3_SPARSE = CHAOS_C3_SPARSE && NCONV >= 3 && !BIG && C3::KP == 2 && C3::M % 4 == 0 &&
                                C3::MP == C3::M && G * ((C3::C + 31) / 32) <= NT / 32;
     constexpr int C2_WTP = (CHAOS_C2_WTP && NCONV == 3 && !BIG && C2::DIN3 && C2::GWIN == 0) ? (C2::ROWS | 1) : 0;
@@ -2422,11 +2658,37 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
     (void)am2;
     (void)am3;
 
+    // tensor-core conv2 (conv_fwd_tc2): 9 more mbarriers in the header (full[4], empty[4], done) and
+    // the whole TMEM (512 columns, one CTA per SM), allocated once for the kernel's lifetime
+    uint64_t* tcbar = reinterpret_cast<uint64_t*>(smem + 256);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 48);
+    uint32_t tc_done_phase = 0;
+    (void)tcbar;
+    (void)tc_done_phase;
     if (threadIdx.x == 0) {
         for (int k = 0; k < 6; ++k) mbar_init(bars + k, 1);
+        if constexpr (TC2) {
+            for (int k = 0; k < 4; ++k) {
+                mbar_init(tcbar + k, NT / 32 - 1);  // full: one arrival per producer warp
+                mbar_init(tcbar + 4 + k, 1);        // empty: the MMA commit
+            }
+            mbar_init(tcbar + 8, 1);  // done
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if constexpr (TC2) {
+        if (threadIdx.x < 32) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "n"(kTcCols)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    }
     __syncthreads();
+    if constexpr (TC2) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = TC2 ? *tmem_slot : 0u;
+    (void)tmem;
     Loader L0{bars + 0, 0u}, L1{bars + 1, 0u}, L2{bars + 2, 0u}, L3{bars + 3, 0u};
     Loader L4{bars + 4, 0u}, L5{bars + 5, 0u};  // FC1 weight chunks (double buffer)
     (void)L4;
@@ -2512,12 +2774,22 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             fence_async_smem();
             __syncthreads();
             PTIME(2);
-            if constexpr (NCONV >= 3 && !BIG) TR_RB(2, 0);
-            if constexpr (NCONV >= 3 && !BIG) L2.issue(wb, P + O::c3w, W3A);  // W1 region is dead: W3's first half
+            if constexpr (NCONV >= 3 && !BIG && !TC2) TR_RB(2, 0);
+            if constexpr (NCONV >= 3 && !BIG && !TC2)
+                L2.issue(wb, P + O::c3w, W3A);  // W1 region is dead: W3's first half
             L1.wait();
             TR_RE(1, 0);
             if constexpr (!BIG) TR_DUMP(0, O::c2w, wb + W2OFF, C2::BLK);
-            conv_fwd<C2, NT, CHAOS_MGF_C2 || MgfC2<Net>::value>(a1, wb + W2OFF, a2, am2, cnt);
+            if constexpr (TC2) {  // the W1 region [0, 20 KB x 2) holds the operand stages; W3 comes after
+                static_assert(2 * kTcStageBytes + 4 * 256 <= W2OFF * 4, "tensor-core stages must not overlap W2");
+                static_assert(S::SFL * 4 >= kTcStageBytes && G * C2::OUT_SZ * 4 >= kTcStageBytes,
+                              "S and A2 each hold one operand stage");
+                conv_fwd_tc2<C2, NT, G>(a1, wb + W2OFF, a2, am2, cnt, tmem, reinterpret_cast<unsigned char*>(wb),
+                                        reinterpret_cast<unsigned char*>(sS), reinterpret_cast<unsigned char*>(a2), tcbar,
+                                        tc_done_phase, a.ptime ? a.ptime + blockIdx.x * kPhases + 17 : nullptr);
+            } else {
+                conv_fwd<C2, NT, CHAOS_MGF_C2 || MgfC2<Net>::value>(a1, wb + W2OFF, a2, am2, cnt);
+            }
             alast = a2;
         }
         if constexpr (NCONV >= 3 && BIG) {
@@ -2530,6 +2802,10 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             fence_async_smem();
             __syncthreads();
             PTIME(3);
+            if constexpr (TC2) {
+                TR_RB(2, 0);
+                L2.issue(wb, P + O::c3w, W3A);
+            }
             L3.issue(wb + W3A, P + O::c3w + W3A, C3::BLK - W3A);
             L2.wait();
             L3.wait();
@@ -2625,16 +2901,8 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
             }
             if constexpr (MODE != kEval) {
                 if (on) {
-#if defined(CHAOS_EXPERIMENT_RCP)
-                    const float inv = __frcp_rn(1.f + r);
-#else
                     const float inv = 1.f / (1.f + r);
-#endif
-#if defined(CHAOS_EXPERIMENT_NODELTA)
-                    z[o] = e;
-#else
                     z[o] = (o != lab) ? (o == best ? inv : e * inv) : (lab == best ? -r * inv : e * inv - 1.f);
-#endif
                 }
             }
         }
@@ -2942,6 +3210,13 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
         PTIME(15);
     }
     if (threadIdx.x == 0) bulk_wait_all<0>();
+    if constexpr (TC2) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (threadIdx.x < 32)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTcCols) : "memory");
+    }
     if constexpr (is_hog(MODE))
         if (threadIdx.x == 0 && pending_progress && a.progress)
             atomicAdd(a.progress, static_cast<unsigned long long>(pending_progress));

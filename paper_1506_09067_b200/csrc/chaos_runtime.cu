@@ -93,6 +93,7 @@ struct LargeNet {  // configs[3], configs[4]
     static constexpr int NCONV = 3, NFULL = 2, GDEF = 4, GINIT = 4, INFLIGHT = 592, NT = 640, SFL = 6400;
     static constexpr bool TRACE = true;
     static constexpr bool MGF2 = true;  // conv2 forward: map groups fastest over the lanes (+0.3%)
+    static constexpr bool TC2 = true;   // conv2 forward on the tensor cores when built with CHAOS_C2_TC
     //                C   H   W   M   K  KP  MT  TT  GS  RB  PB  MS  (0)  DIN3  GWIN  DWIN  NSPL
 #ifndef LARGE_C1_MT  // tile sweeps (scripts): -DLARGE_C1_MT=.. -DLARGE_C1_GS=..
 #define LARGE_C1_MT 10
