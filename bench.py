@@ -199,11 +199,15 @@ def main():
     ap.add_argument("--force-dist", action="store_true",
                     help="run the multi-GPU leg (NCCL process group, configs[4] shards, averaging every K) "
                          "even with one rank -- exercises the N>1 code path on one GPU")
-    ap.add_argument("--avg", default="async", choices=["interval", "async"],
+    ap.add_argument("--avg", default="async", choices=["interval", "async", "fused"],
                     help="multi-GPU hogwild averaging: 'interval' = one launch per K images, then a blocking "
                          "NCCL average; 'async' = one launch per shard with in-flight averages every K images on "
-                         "a second stream (SURVEY NEXT-2)")
+                         "a second stream (SURVEY NEXT-2); 'fused' = the persistent kernel averages the replicas "
+                         "itself every K images through peer memory (CUDA IPC / NVLink), no reserved SMs")
     ap.add_argument("--reserve-sms", type=int, default=4, help="--avg async: SMs left to the comm kernels")
+    ap.add_argument("--pavg-comm", type=int, default=None,
+                    help="--avg fused: comm CTAs per GPU running the in-kernel rounds (default 1 for N <= 2, "
+                         "else 2; 0 = the training CTAs run them between image groups)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: 60,000 images per GPU per step (configs[4] shards for N > 1); strong: the "
                          "60,000 configs[3] images split over the N GPUs (SURVEY D-5 headline)")
@@ -253,6 +257,7 @@ def main():
     torch.cuda.set_stream(stream)
     net = Net(sd.ARCHS[args.arch], init_seed=w.seed, stream=stream)
     use_async = distributed and args.mode == "hogwild" and args.avg == "async"
+    use_fused = distributed and args.mode == "hogwild" and args.avg == "fused"
     if use_async:
         net.set_option(OPT_RESERVE_SMS, args.reserve_sms)
     info = net.launch_info()
@@ -263,10 +268,14 @@ def main():
     trainer = DistTrainer(net, rank, world, args.k, force_collective=args.force_dist,
                           comm=args.comm if args.mode == "hogwild" else "torch")
     grad_buf = torch.zeros_like(net.device_params()) if args.mode == "sync" else None
+    if use_fused:
+        trainer.setup_fused(args.pavg_comm)
 
     def step(Xs, Ys, lr_s):
         if args.mode == "sync":
             trainer.sync_epoch(Xs, Ys, lr_s, args.sync_batch, grad_buf)
+        elif use_fused:
+            trainer.epoch_fused(Xs, Ys, lr_s)
         elif use_async:
             trainer.epoch_async(Xs, Ys, lr_s)
         else:
@@ -340,8 +349,8 @@ def main():
             if host_entry:
                 net.train_epoch_host(Xh, Yh, lr_s)
                 net.last_train_loss()
-            elif use_async:
-                trainer.epoch_async(X, Y, lr_s, host=(Xh, Yh))
+            elif use_async or use_fused:
+                (trainer.epoch_fused if use_fused else trainer.epoch_async)(X, Y, lr_s, host=(Xh, Yh))
                 out_h.copy_(net.device_params()[:1], non_blocking=True)
                 torch.cuda.current_stream().synchronize()
             else:
@@ -365,6 +374,8 @@ def main():
                "path": "chaos_train_epoch_host (C ABI, host buffers)" if host_entry
                else "DistTrainer.epoch_async(host=...) -> chaos_train_epoch_host_async: one launch gated "
                     "by the copy stream's landed-images counter, in-flight averages beside it" if use_async
+               else "DistTrainer.epoch_fused(host=...) -> chaos_train_epoch_host_async: one gated launch "
+                    "averaging in-kernel through peer memory" if use_fused
                else "pinned H2D copy + step on the training stream"}
 
     # per-interval all-reduce time (SURVEY D-6): the K-interval average of the parameters alone,
@@ -411,6 +422,8 @@ def main():
                                  f"{world} GPUs per step (strong scaling)")
                                 + ("" if not distributed else f"; {'configs[4] generator, ' if args.scaling == 'weak' else ''}NCCL average every {args.k}"
                                    + (f" images in flight (async, {args.reserve_sms} SMs reserved)" if use_async
+                                      else " claimed images in-kernel through peer memory (fused), exact NCCL "
+                                           "average at the end of the step" if use_fused
                                       else " images (blocking)")))
                    if args.mode == "hogwild" else
                    (f"configs[3] {args.arch} net, deterministic sync SGD, global batch {args.sync_batch}, "
@@ -447,6 +460,10 @@ def main():
     if args.force_dist:
         line["config"]["force_dist"] = True
         line["collectives"] = trainer.n_collectives
+    if use_fused:
+        line["fused_rounds"] = trainer.n_fused_rounds
+        line["config"]["pavg_comm_ctas"] = trainer.comm_ctas
+        line["roofline"]["kernel"] = line["roofline"]["kernel"][:-1] + ",PAVG>"
     print(json.dumps(line), flush=True)
     if distributed:
         dist.destroy_process_group()

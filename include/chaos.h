@@ -93,7 +93,10 @@ typedef enum {
                                     set it before chaos_dist_init, which caps the communicator's CTAs at it */
     CHAOS_OPT_DEBUG_TRACE = 6,   /* 1 => hogwild epochs record their schedule (chaos_debug_trace); tiny and
                                     large nets; CHAOS_E_UNSUPPORTED elsewhere */
-    CHAOS_OPT_DEBUG_STAGGER = 7  /* trace epochs: CTA b starts b * value cycles late (varied interleavings) */
+    CHAOS_OPT_DEBUG_STAGGER = 7, /* trace epochs: CTA b starts b * value cycles late (varied interleavings) */
+    CHAOS_OPT_PAVG_COMM_CTAS = 8 /* fused averaging (chaos_pavg_*): 0 (default) = the training CTAs run the
+                                    rounds between image groups; c in [1, 16] = c extra CTAs of the launch
+                                    (SMs of their own) run them and the training CTAs never stall on one */
 } chaos_option;
 
 typedef struct chaos_net chaos_net;
@@ -197,6 +200,58 @@ chaos_status chaos_dist_unique_id(void* host_id);
 chaos_status chaos_dist_init(chaos_net* net, const void* host_id, int32_t rank, int32_t world);
 chaos_status chaos_dist_average(chaos_net* net);
 chaos_status chaos_dist_average_buffer(chaos_net* net, float* d_buf, int64_t n, int64_t stream);
+
+/* Fused in-kernel cross-replica averaging (the fused variant; PAPER.md:138-140
+ * "arbitrary order of synchronization" carried across replicas, PAPER.md:412 CHAOS on several
+ * devices).  The persistent hogwild kernel averages the replicas itself, between image
+ * groups, through peer memory -- no collective launch, no reserved SMs.  The weight vector is cut
+ * into nslice slices; CTA c owns slices c, c + ctas, ...  Round t of a launch is due once t*k of the
+ * replica's images are claimed; then each CTA copies its slices of the live weights into its own
+ * snapshot ring (4 buffers), publishes a per-slice flag, and -- once every replica's flag for the
+ * slice has reached the round -- reads all R snapshots (NVLink loads through CUDA-IPC mappings, or
+ * same-device buffers) and adds (fixed-order mean - own snapshot) to its live weights with
+ * reductions, keeping the hogwild updates made meanwhile; every replica computes the same mean, so
+ * each round preserves the replicas' sum up to the rounding of the deltas.  A launch returns only
+ * after all its rounds are applied on every replica; every replica must run the same launches
+ * with the same armed rounds (collective), so the caller agrees the count (e.g. from the shortest
+ * shard).  The final exact average after a launch is the caller's (chaos_dist_average / NCCL).
+ * chaos_pavg_setup: allocates this replica's exchange buffer (cudaMalloc, zeroed: snapshot ring +
+ *   flags + checksums) for rank in [0, world), world <= 8, interval k >= 1 images, nslice slices
+ *   (0 = the SM count; every replica must use the same value and the same arch).  Once per net.
+ * chaos_pavg_exchange: the device pointer of rank `peer`'s exchange buffer as this net maps it (its
+ *   own for peer == rank; same-process peers, tests) and the buffer size.
+ * chaos_pavg_ipc_handle: writes its CUDA IPC handle (CHAOS_IPC_HANDLE_BYTES bytes) to host_handle,
+ *   to be sent to the other ranks (e.g. a torch.distributed all-gather).
+ * chaos_pavg_open_peer: maps rank `peer`'s exchange buffer from its IPC handle (another process,
+ *   another GPU: peer access enabled lazily); closed with the net.
+ * chaos_pavg_set_peer: uses an exchange buffer of this process (another net) for rank `peer`.
+ * chaos_pavg_arm: the net's next hogwild launch (device or host entry) runs `rounds` averaging
+ *   rounds; every peer table entry must be set by then (CHAOS_E_INVALID otherwise).
+ * chaos_pavg_rounds_done: rounds launched so far (round numbers are absolute and monotonic).
+ * chaos_pavg_set_check: debug: every snapshot is checksummed and every read of it verified in the
+ *   kernel; a mismatch (a torn or stale peer read) latches CHAOS_E_CUDA.  Also (re)starts two
+ *   device sums over this replica's applied deltas, per weight: the signed sum and the sum of
+ *   magnitudes (summed over the replicas, the signed one is 0 up to rounding: every round preserves
+ *   the replicas' sum).
+ * chaos_pavg_debug_sums: copies those two sums (internal layout, n = chaos_net_device_params_len)
+ *   to the host; synchronizing; returns latched errors.
+ * chaos_train_epoch_replicas: one-GPU emulation of R replicas (this build: the large net): ONE
+ *   cooperative hogwild launch, CTAs split evenly, replica r = nets[r] trains its own images
+ *   d_images[r] / d_labels[r] (n[r] >= 1 images) into its own weights, with the fused averaging when
+ *   armed (nets[r] set up as rank r of R, with each other's exchange buffers).  Asynchronous on
+ *   nets[0]'s stream; the other nets' streams wait for it. */
+#define CHAOS_IPC_HANDLE_BYTES 64
+chaos_status chaos_pavg_setup(chaos_net* net, int32_t rank, int32_t world, int64_t k, int32_t nslice);
+chaos_status chaos_pavg_exchange(chaos_net* net, int32_t peer, void** d_ptr, int64_t* bytes);
+chaos_status chaos_pavg_ipc_handle(chaos_net* net, void* host_handle);
+chaos_status chaos_pavg_open_peer(chaos_net* net, int32_t peer, const void* host_handle);
+chaos_status chaos_pavg_set_peer(chaos_net* net, int32_t peer, void* d_exchange);
+chaos_status chaos_pavg_arm(chaos_net* net, int64_t rounds);
+int64_t chaos_pavg_rounds_done(const chaos_net* net);
+chaos_status chaos_pavg_set_check(chaos_net* net, int32_t on);
+chaos_status chaos_pavg_debug_sums(chaos_net* net, float* host_dsum, float* host_dabs, int64_t n);
+chaos_status chaos_train_epoch_replicas(chaos_net* const* nets, int32_t R, const float* const* d_images,
+                                        const int32_t* const* d_labels, const int64_t* n, float lr);
 
 /* Debug (controlled hogwild / arbitrary order of synchronization; checked by
  * replaying the recorded schedule in the oracle): after a hogwild epoch

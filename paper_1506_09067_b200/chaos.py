@@ -20,7 +20,7 @@ CHAOS_CONV, CHAOS_MAXPOOL, CHAOS_FULL = 1, 2, 3
 CHAOS_TANH, CHAOS_IDENTITY = 0, 1
 HOGWILD, SYNC = 0, 1
 OPT_STREAM, OPT_SYNC_BATCH, OPT_GROUP, OPT_MAX_CTAS, OPT_DEBUG_CLAIMS, OPT_RESERVE_SMS = 0, 1, 2, 3, 4, 5
-OPT_DEBUG_TRACE, OPT_DEBUG_STAGGER = 6, 7
+OPT_DEBUG_TRACE, OPT_DEBUG_STAGGER, OPT_PAVG_COMM_CTAS = 6, 7, 8
 TRACE_REC = 32  # int64 per group in chaos_debug_trace records
 STATUS = {0: "CHAOS_OK", -1: "CHAOS_E_INVALID", -2: "CHAOS_E_ARCH", -3: "CHAOS_E_UNSUPPORTED",
           -4: "CHAOS_E_LABEL", -5: "CHAOS_E_NONFINITE", -6: "CHAOS_E_CUDA", -7: "CHAOS_E_NCCL"}
@@ -33,7 +33,11 @@ EXPORTS = ["chaos_net_create", "chaos_net_destroy", "chaos_net_set_option", "cha
            "chaos_net_launch_info", "chaos_last_error", "chaos_last_status", "chaos_debug_phase_times",
            "chaos_batch_gradient", "chaos_apply_gradient", "chaos_progress_enqueued", "chaos_progress_wait",
            "chaos_avg_snapshot", "chaos_avg_apply", "chaos_dist_unique_id", "chaos_dist_init",
-           "chaos_dist_average", "chaos_dist_average_buffer", "chaos_train_epoch_host_async", "chaos_debug_trace"]
+           "chaos_dist_average", "chaos_dist_average_buffer", "chaos_train_epoch_host_async", "chaos_debug_trace",
+           "chaos_pavg_setup", "chaos_pavg_exchange", "chaos_pavg_ipc_handle", "chaos_pavg_open_peer",
+           "chaos_pavg_set_peer", "chaos_pavg_arm", "chaos_pavg_rounds_done", "chaos_pavg_set_check",
+           "chaos_pavg_debug_sums", "chaos_train_epoch_replicas"]
+IPC_HANDLE_BYTES = 64
 
 
 class ChaosError(RuntimeError):
@@ -96,6 +100,17 @@ def lib():
             "chaos_dist_init": ([vp, vp, C.c_int32, C.c_int32], C.c_int),
             "chaos_dist_average": ([vp], C.c_int),
             "chaos_dist_average_buffer": ([vp, vp, C.c_int64, C.c_int64], C.c_int),
+            "chaos_pavg_setup": ([vp, C.c_int32, C.c_int32, C.c_int64, C.c_int32], C.c_int),
+            "chaos_pavg_exchange": ([vp, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)], C.c_int),
+            "chaos_pavg_debug_sums": ([vp, fp, fp, C.c_int64], C.c_int),
+            "chaos_pavg_ipc_handle": ([vp, vp], C.c_int),
+            "chaos_pavg_open_peer": ([vp, C.c_int32, vp], C.c_int),
+            "chaos_pavg_set_peer": ([vp, C.c_int32, vp], C.c_int),
+            "chaos_pavg_arm": ([vp, C.c_int64], C.c_int),
+            "chaos_pavg_rounds_done": ([vp], C.c_int64),
+            "chaos_pavg_set_check": ([vp, C.c_int32], C.c_int),
+            "chaos_train_epoch_replicas": ([C.POINTER(C.c_void_p), C.c_int32, C.POINTER(C.c_void_p),
+                                            C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.c_float], C.c_int),
         }
         for name, (args, res) in sig.items():
             if os.environ.get("CHAOS_LIB") and not hasattr(L, name):
@@ -341,6 +356,71 @@ class Net:
     def dist_average_buffer(self, buf, stream):
         """chaos_dist_average_buffer: in-place average of a CUDA float32 tensor on `stream`."""
         _check(lib().chaos_dist_average_buffer(self._h, _ptr(buf), int(buf.numel()), stream.cuda_stream))
+
+    # ---- fused in-kernel cross-replica averaging (chaos_pavg_*; include/chaos.h)
+    def pavg_setup(self, rank, world, k, nslice=0):
+        """chaos_pavg_setup: this replica's exchange buffer (rank of world, interval k images)."""
+        _check(lib().chaos_pavg_setup(self._h, int(rank), int(world), int(k), int(nslice)))
+        self._pavg_rank = int(rank)
+
+    def pavg_exchange(self, peer=None):
+        """chaos_pavg_exchange: (device pointer, bytes) of rank `peer`'s exchange buffer as this net
+        maps it (default: its own)."""
+        p, b = C.c_void_p(), C.c_int64()
+        if peer is None:
+            peer = self._pavg_rank
+        _check(lib().chaos_pavg_exchange(self._h, int(peer), C.byref(p), C.byref(b)))
+        return int(p.value), int(b.value)
+
+    def pavg_debug_sums(self):
+        """chaos_pavg_debug_sums: (signed sum, magnitude sum) of the applied deltas (internal layout)."""
+        n = int(lib().chaos_net_device_params_len(self._h))
+        ds, da = np.zeros(n, np.float32), np.zeros(n, np.float32)
+        fpp = C.POINTER(C.c_float)
+        _check(lib().chaos_pavg_debug_sums(self._h, ds.ctypes.data_as(fpp), da.ctypes.data_as(fpp), n))
+        return ds, da
+
+    def pavg_ipc_handle(self) -> bytes:
+        """chaos_pavg_ipc_handle: the exchange buffer's CUDA IPC handle (64 bytes)."""
+        buf = C.create_string_buffer(IPC_HANDLE_BYTES)
+        _check(lib().chaos_pavg_ipc_handle(self._h, buf))
+        return buf.raw
+
+    def pavg_open_peer(self, peer, handle: bytes):
+        """chaos_pavg_open_peer: map rank `peer`'s exchange buffer (another process / GPU)."""
+        if len(handle) != IPC_HANDLE_BYTES:
+            raise ValueError(f"expected the {IPC_HANDLE_BYTES}-byte handle of pavg_ipc_handle()")
+        _check(lib().chaos_pavg_open_peer(self._h, int(peer), C.create_string_buffer(handle, IPC_HANDLE_BYTES)))
+
+    def pavg_set_peer(self, peer, other):
+        """chaos_pavg_set_peer: another Net of this process (same device) is rank `peer`."""
+        ptr, _ = other.pavg_exchange()
+        _check(lib().chaos_pavg_set_peer(self._h, int(peer), C.c_void_p(ptr)))
+
+    def pavg_arm(self, rounds):
+        """chaos_pavg_arm: the next hogwild launch runs `rounds` in-kernel averaging rounds."""
+        _check(lib().chaos_pavg_arm(self._h, int(rounds)))
+
+    def pavg_rounds_done(self) -> int:
+        return int(lib().chaos_pavg_rounds_done(self._h))
+
+    def pavg_set_check(self, on=True):
+        """chaos_pavg_set_check: debug checksums of every snapshot and every peer read of it."""
+        _check(lib().chaos_pavg_set_check(self._h, 1 if on else 0))
+
+    @staticmethod
+    def train_epoch_replicas(nets, images, labels, lr):
+        """chaos_train_epoch_replicas: one-GPU emulation, replica r = nets[r] trains images[r] /
+        labels[r] (CUDA tensors) in ONE cooperative launch (asynchronous on nets[0]'s stream)."""
+        R = len(nets)
+        if not (len(images) == len(labels) == R):
+            raise ValueError("one images / labels tensor per replica")
+        ns = [_check_batch(x, y, nets[0].n_in, nets[0].device, True) for x, y in zip(images, labels)]
+        hs = (C.c_void_p * R)(*[n._h.value for n in nets])
+        xs = (C.c_void_p * R)(*[x.data_ptr() for x in images])
+        ys = (C.c_void_p * R)(*[y.data_ptr() for y in labels])
+        nn = (C.c_int64 * R)(*ns)
+        _check(lib().chaos_train_epoch_replicas(hs, R, xs, ys, nn, float(lr)))
 
     def debug_trace(self, n_groups, pubs=True, reads=False):
         """chaos_debug_trace: (records int64 [n_groups][32], publishes float32 [n_groups][n_params]

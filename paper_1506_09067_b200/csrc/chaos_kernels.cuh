@@ -49,7 +49,7 @@ __host__ __device__ constexpr bool is_hog(int mode) { return mode == kHogwild ||
 // read (done count at its start / started count at its end), 4/5 the delta_in read (-1: the
 // forward read's values serve); [30] = worker (CTA), [31] = the worker's iteration.
 constexpr int kTraceRec = 32;
-enum Latch : int { kLatchLabel = 1, kLatchNonfinite = 2 };
+enum Latch : int { kLatchLabel = 1, kLatchNonfinite = 2, kLatchPavg = 4 };
 
 __host__ __device__ constexpr int round4(int x) { return (x + 3) / 4 * 4; }
 
@@ -233,6 +233,40 @@ struct KArgs {
     long long stagger;            // kTrace: CTA b starts after b * stagger cycles
     float* tw;                    // kTrace: the weight values each group read, [group][2][pint]
                                   // (internal layout; [.][0] forward reads, [.][1] delta_in reads)
+    const struct PavgArgs* pavg;  // hogwild: fused in-kernel cross-replica averaging (null: off)
+    long long pavg_round0;        // averaging rounds run by this replica's earlier launches
+    long long pavg_rounds;        // rounds in this launch: round t is due once t * pavg_k images are claimed
+    long long pavg_k;
+    int pavg_comm;                // > 0: the last pavg_comm CTAs of the replica's launch are comm CTAs
+                                  // (they run the rounds; the training CTAs never stall on one)
+    const KArgs* reps;            // one-GPU replica emulation (REP instantiation): per-replica arguments
+    int rep_ctas;                 // ... and CTAs per replica (CTA b runs replica b / rep_ctas)
+};
+
+// Fused cross-replica averaging (fused variant): the replicas'
+// weight vectors are cut into nslice slices; CTA c of a replica's launch owns slices c, c + ctas, ...
+// and, once round t is due, copies its slices of the live weights into its snapshot ring (buffer
+// t % kPavgBufs), publishes flag = t; when every peer's flag for the slice has reached t it reads
+// all R snapshots (peer memory: NVLink loads through CUDA-IPC mappings; same-device buffers in the
+// one-GPU emulation), adds avg - own snapshot to its live weights (red.add, so the hogwild updates
+// made meanwhile are kept: "arbitrary order of synchronization", carried across
+// replicas) and publishes done = t.  Round t may overwrite a buffer only after every peer's done
+// has reached t - kPavgBufs.  Round numbers are absolute (round0 + t) and monotonic across launches,
+// so flags are never reset.  Every replica computes the same avg (fixed order q = 0..R-1, then / R),
+// so each round preserves the sum of the replicas up to the rounding of the deltas.
+constexpr int kPavgMaxR = 8;       // replicas per average
+constexpr int kPavgBufs = 4;       // snapshot ring depth
+struct PavgArgs {
+    int R, rank, nslice, slice_fl;       // slice_fl: floats per slice (multiple of 4)
+    long long pint;                      // floats of the weight vector
+    int check;                           // debug: checksum every snapshot and verify every read of it
+    float* snap[kPavgMaxR];              // replica q's ring [kPavgBufs][nslice * slice_fl]
+    unsigned* flag[kPavgMaxR];           // [nslice] last round whose snapshot of the slice q published
+    unsigned* done[kPavgMaxR];           // [nslice] last round whose peer snapshots q consumed
+    unsigned long long* cks[kPavgMaxR];  // [nslice][kPavgBufs] checksum of q's snapshot (check mode)
+    int* latch;                          // check mode: kLatchPavg on a mismatch
+    float* dsum;                         // check mode: [pint] sum of this replica's applied deltas
+    float* dabs;                         // ... and of their magnitudes
 };
 
 // Phase timing (instrumented build only, -DCHAOS_TIMING): thread 0 adds the clock64 cycles
@@ -2561,11 +2595,216 @@ __device__ __forceinline__ void wait_landed(const unsigned long long* ready, uns
 }
 
 // ------------------------------------------------------------------------------------
-// PHASE(worker) The worker kernel: hogwild training, sync-batch gradients, evaluation, forward.
+// PHASE(pavg) fused cross-replica averaging, serviced by the hogwild worker between image groups
+// (see PavgArgs).  Loads of peer data are relaxed at system scope (never served by a stale L1
+// line); flags are published with a system-scope fence after a CTA barrier (cumulative) and read
+// with relaxed loads followed by a system-scope fence before the barrier that releases the reads.
 // ------------------------------------------------------------------------------------
-// GATED (hogwild from host buffers only): claims wait for the copy stream's landed-images counter.
-template <class Net, int G, int NT, int MODE, bool GATED = false>
-__global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
+__device__ __forceinline__ unsigned ld_relaxed_sys(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ float4 ld_relaxed_sys4(const float* p) {
+    float4 v;
+    asm volatile("ld.relaxed.sys.global.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_sys(unsigned* p, unsigned v) {
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ unsigned long long bits4(float4 v) {
+    return static_cast<unsigned long long>(__float_as_uint(v.x)) + __float_as_uint(v.y) + __float_as_uint(v.z) +
+           __float_as_uint(v.w);
+}
+
+// Warp 0: do all R replicas' words w[q][s] for this CTA's slices s reach `need`?  (parallel loads)
+__device__ __forceinline__ bool pavg_all_reached(unsigned* const* w, int R, int cta, int ncta, int nslice,
+                                                 unsigned need, bool plus_bufs) {
+    const int lane = threadIdx.x & 31;
+    const int nsl = (nslice - cta + ncta - 1) / ncta;  // slices of this CTA
+    bool ok = true;
+    for (int e = lane; e < nsl * R; e += 32) {
+        const int s = cta + (e / R) * ncta, q = e % R;
+        const unsigned v = ld_relaxed_sys(w[q] + s);
+        ok = ok && (plus_bufs ? v + kPavgBufs >= need : v >= need);
+    }
+    return __all_sync(0xffffffffu, ok);
+}
+
+// Run every averaging action this CTA can take now: apply rounds whose snapshots all peers have
+// published, snapshot rounds that are due (due = rounds whose t * K images are claimed), and, when
+// `final` (no images left to claim), wait until all the launch's rounds are applied.  All threads
+// call it converged.  cta / ncta: this CTA's index among the replica's CTAs that own slices (the
+// training CTAs, or the comm CTAs).  ctl: 4 ints + 8 64-bit sums of shared memory; ctl[0] / ctl[1]
+// = rounds snapshotted / applied by this CTA in this launch (0 at the launch start).
+template <int NT>
+__device__ __noinline__ void pavg_service(float* params, const PavgArgs* pp, unsigned r0, int rounds, int cta,
+                                          int ncta, int due, bool final, int* ctl) {
+    const PavgArgs& p = *pp;
+    const int R = p.R, me = p.rank, nslice = p.nslice, sfl = p.slice_fl;
+    unsigned long long* sums = reinterpret_cast<unsigned long long*>(ctl + 4);
+    for (;;) {
+        if (threadIdx.x < 32) {
+            const int ts = ctl[0], tap = ctl[1];
+            int act = 0;  // 0 leave, 1 snapshot, 2 apply, 3 wait
+            if (tap < ts) {  // the oldest snapshotted round: have all peers published it?
+                if (pavg_all_reached(p.flag, R, cta, ncta, nslice, r0 + static_cast<unsigned>(tap) + 1u, false)) act = 2;
+            } else if (ts < due) {
+                // next snapshot: only once this CTA's previous round is applied (rounds are sequential
+                // per slice: a snapshot taken before an earlier round's apply would re-apply its
+                // correction), and its ring buffer must be consumed by every peer
+                const unsigned t = r0 + static_cast<unsigned>(ts) + 1u;
+                const bool ok = t <= static_cast<unsigned>(kPavgBufs) ||
+                                pavg_all_reached(p.done, R, cta, ncta, nslice, t, true);
+                act = ok ? 1 : (final ? 3 : 0);  // blocked mid-launch: train on, retry at the next group
+            }
+            if (act == 0 && final && tap < rounds) act = 3;
+            if (threadIdx.x == 0) {
+                if (act == 1 || act == 2) fence_sys();  // acquire: the words just read precede what follows
+                ctl[2] = act;
+                sums[0] = 0ull;
+                if (p.check)
+                    for (int q = 1; q < kPavgMaxR; ++q) sums[q] = 0ull;
+            }
+        }
+        __syncthreads();
+        const int act = ctl[2];
+        if (act == 0) break;
+        if (act == 3) {
+            if (threadIdx.x == 0) __nanosleep(500);
+        } else if (act == 1) {
+            const unsigned t = r0 + static_cast<unsigned>(ctl[0]) + 1u;
+            const int b = static_cast<int>(t % kPavgBufs);
+            for (int s = cta; s < nslice; s += ncta) {
+                const long long off = static_cast<long long>(s) * sfl;
+                const int nq = static_cast<int>(min(static_cast<long long>(sfl), p.pint - off)) / 4;
+                const float4* src = reinterpret_cast<const float4*>(params + off);
+                float4* dst = reinterpret_cast<float4*>(p.snap[me] + (static_cast<long long>(b) * nslice + s) * sfl);
+                unsigned long long ck = 0ull;
+                for (int i = threadIdx.x; i < nq; i += NT) {
+                    const float4 v = __ldcg(src + i);  // the live weights (the REDs land in L2)
+                    dst[i] = v;
+                    ck += bits4(v);
+                }
+                if (p.check) {  // per slice: block sum, written before the flag
+                    atomicAdd(sums, ck);
+                    __syncthreads();
+                    if (threadIdx.x == 0) {
+                        p.cks[me][s * kPavgBufs + b] = sums[0];
+                        sums[0] = 0ull;
+                    }
+                    __syncthreads();
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                fence_sys();  // release (cumulative over the CTA's stores ordered by the barrier)
+                for (int s = cta; s < nslice; s += ncta) st_relaxed_sys(p.flag[me] + s, t);
+                ++ctl[0];
+            }
+        } else {  // act == 2
+            const unsigned t = r0 + static_cast<unsigned>(ctl[1]) + 1u;
+            const int b = static_cast<int>(t % kPavgBufs);
+            for (int s = cta; s < nslice; s += ncta) {
+                const long long off = static_cast<long long>(s) * sfl;
+                const int nq = static_cast<int>(min(static_cast<long long>(sfl), p.pint - off)) / 4;
+                const long long soff = (static_cast<long long>(b) * nslice + s) * sfl;
+                for (int i = threadIdx.x; i < nq; i += NT) {
+                    float4 sum = make_float4(0.f, 0.f, 0.f, 0.f), mine = sum;
+                    for (int q = 0; q < R; ++q) {  // fixed order q = 0..R-1 on every replica
+                        const float4 v = ld_relaxed_sys4(p.snap[q] + soff + 4 * i);
+                        if (p.check) atomicAdd(sums + q, bits4(v));  // debug only: shared-memory atomics
+                        if (q == 0) {
+                            sum = v;
+                        } else {
+                            sum.x += v.x;
+                            sum.y += v.y;
+                            sum.z += v.z;
+                            sum.w += v.w;
+                        }
+                        if (q == me) mine = v;
+                    }
+                    const float rf = static_cast<float>(R);
+                    const float4 dl = make_float4(sum.x / rf - mine.x, sum.y / rf - mine.y, sum.z / rf - mine.z,
+                                                  sum.w / rf - mine.w);
+                    red_add4(params + off + 4 * i, dl);
+                    if (p.check) {
+                        red_add4(p.dsum + off + 4 * i, dl);
+                        red_add4(p.dabs + off + 4 * i, make_float4(fabsf(dl.x), fabsf(dl.y), fabsf(dl.z), fabsf(dl.w)));
+                    }
+                }
+                if (p.check) {
+                    __syncthreads();
+                    if (threadIdx.x == 0) {
+                        for (int q = 0; q < R; ++q)
+                            if (sums[q] != *reinterpret_cast<volatile unsigned long long*>(p.cks[q] + s * kPavgBufs + b))
+                                atomicOr(p.latch, kLatchPavg);
+                        for (int q = 0; q < kPavgMaxR; ++q) sums[q] = 0ull;
+                    }
+                    __syncthreads();
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                fence_sys();  // the peer reads above complete before done is seen
+                for (int s = cta; s < nslice; s += ncta) st_relaxed_sys(p.done[me] + s, t);
+                ++ctl[1];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// A comm CTA (KArgs.pavg_comm > 0): trains nothing; polls the replica's claim counter and runs the
+// averaging rounds of its slices (the slices are split over the comm CTAs only) until all of the
+// launch's rounds are applied.  The training CTAs never stall on a round.
+template <int NT>
+__device__ __forceinline__ void pavg_comm_loop(const KArgs& a, int ccta, int* ctl) {
+    const int rounds = static_cast<int>(a.pavg_rounds);
+    for (;;) {
+        if (threadIdx.x == 0) {
+            const unsigned long long c = *reinterpret_cast<const volatile unsigned long long*>(a.counter);
+            const bool fin = c >= static_cast<unsigned long long>(a.n);
+            ctl[3] = static_cast<int>(fin ? a.pavg_rounds : min(a.pavg_rounds, static_cast<long long>(c) / a.pavg_k));
+            ctl[2] = fin ? 1 : 0;  // (service overwrites ctl[2] after reading this copy)
+        }
+        __syncthreads();
+        const int due = ctl[3];
+        const bool fin = ctl[2] != 0;
+        __syncthreads();
+        pavg_service<NT>(a.params, a.pavg, static_cast<unsigned>(a.pavg_round0), rounds, ccta, a.pavg_comm, due, fin,
+                         ctl);
+        if (ctl[1] >= rounds) break;
+        if (threadIdx.x == 0) __nanosleep(1000);
+        __syncthreads();
+    }
+}
+
+// REP (one-GPU emulation of replicas, hogwild only): CTA b runs replica b / a0.rep_ctas with that
+// replica's arguments a0.reps[b / a0.rep_ctas].
+template <bool REP>
+__device__ __forceinline__ const KArgs& replica_args(const KArgs& a0) {
+    if constexpr (REP)
+        return a0.reps[blockIdx.x / a0.rep_ctas];
+    else
+        return a0;
+}
+// PAVG: the fused cross-replica averaging is compiled in (a separate instantiation: its mere presence
+// costs the plain hogwild kernel ~1.4% -- measured, profiles/r4)
+template <class Net, int G, int NT, int MODE, bool GATED = false, bool REP = false, bool PAVG = REP>
+__global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a0) {
+    static_assert(!REP || MODE == kHogwild, "replica emulation is hogwild only");
+    static_assert(!PAVG || MODE == kHogwild, "fused averaging is hogwild only");
+    const KArgs& a = replica_args<REP>(a0);
+    const int cta = REP ? static_cast<int>(blockIdx.x) % a0.rep_ctas : static_cast<int>(blockIdx.x);
+    const int ncta = REP ? a0.rep_ctas : static_cast<int>(gridDim.x);
+    (void)cta;
+    (void)ncta;
     using C1 = typename Net::C1;
     using C2 = typename Net::C2;
     using C3 = typename Net::C3;
@@ -2637,6 +2876,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
     int* s_base = reinterpret_cast<int*>(smem + 64);
     int* s_lab = reinterpret_cast<int*>(smem + 80);                // G labels (<= 16)
     float* s_loss = reinterpret_cast<float*>(smem + 80 + 4 * 16);  // G losses
+    int* pctl = reinterpret_cast<int*>(smem + 384);  // fused averaging: 4 control ints + 8 64-bit sums
     float* fa = reinterpret_cast<float*>(smem + kHdrBytes);
     float* sS = fa + S::S;
     float* a1 = fa + S::A1;
@@ -2666,6 +2906,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
     (void)tcbar;
     (void)tc_done_phase;
     if (threadIdx.x == 0) {
+        pctl[0] = pctl[1] = pctl[3] = 0;
         for (int k = 0; k < 6; ++k) mbar_init(bars + k, 1);
         if constexpr (TC2) {
             for (int k = 0; k < 4; ++k) {
@@ -2689,6 +2930,13 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
     if constexpr (TC2) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = TC2 ? *tmem_slot : 0u;
     (void)tmem;
+    if constexpr (PAVG) {
+        static_assert(!TC2, "comm CTAs return before the TMEM teardown");
+        if (a.pavg && a.pavg_comm > 0 && cta >= ncta - a.pavg_comm) {
+            pavg_comm_loop<NT>(a, cta - (ncta - a.pavg_comm), pctl);
+            return;
+        }
+    }
     Loader L0{bars + 0, 0u}, L1{bars + 1, 0u}, L2{bars + 2, 0u}, L3{bars + 3, 0u};
     Loader L4{bars + 4, 0u}, L5{bars + 5, 0u};  // FC1 weight chunks (double buffer)
     (void)L4;
@@ -2715,10 +2963,17 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a) {
                 base = (static_cast<long long>(blockIdx.x) + iter * gridDim.x) * G;
             }
             *s_base = base < a.n ? static_cast<int>(base) : -1;
+            if constexpr (PAVG)  // fused averaging: rounds whose t * K images are claimed
+                if (a.pavg && a.pavg_comm == 0)
+                    pctl[3] = static_cast<int>(base < a.n ? min(a.pavg_rounds, base / a.pavg_k) : a.pavg_rounds);
         }
         fence_proxy_async();  // earlier generic smem / global accesses precede the async proxy
         __syncthreads();
         const int base = *s_base;
+        if constexpr (PAVG)
+            if (a.pavg && a.pavg_comm == 0)
+                pavg_service<NT>(a.params, a.pavg, static_cast<unsigned>(a.pavg_round0), static_cast<int>(a.pavg_rounds),
+                                 cta, ncta, pctl[3], base < 0, pctl);
         PTIME(0);
         if (base < 0) break;
         const int slot = static_cast<int>(base / G);

@@ -94,6 +94,7 @@ struct LargeNet {  // configs[3], configs[4]
     static constexpr bool TRACE = true;
     static constexpr bool MGF2 = true;  // conv2 forward: map groups fastest over the lanes (+0.3%)
     static constexpr bool TC2 = true;   // conv2 forward on the tensor cores when built with CHAOS_C2_TC
+    static constexpr bool REPL = true;  // replica-emulation build (fused cross-replica averaging tests)
     //                C   H   W   M   K  KP  MT  TT  GS  RB  PB  MS  (0)  DIN3  GWIN  DWIN  NSPL
 #ifndef LARGE_C1_MT  // tile sweeps (scripts): -DLARGE_C1_MT=.. -DLARGE_C1_GS=..
 #define LARGE_C1_MT 10
@@ -137,6 +138,17 @@ struct PaperLargeNet {  // Table I large: conv
 
 using KernelFn = void (*)(KArgs);
 
+// Nets with a one-GPU replica-emulation build of the hogwild worker (REPL = true: the fused
+// cross-replica averaging is tested on one GPU with R replicas in one cooperative launch)
+template <class N, class = void>
+struct Repl {
+    static constexpr bool value = false;
+};
+template <class N>
+struct Repl<N, std::void_t<decltype(N::REPL)>> {
+    static constexpr bool value = N::REPL;
+};
+
 struct Block {  // one weighted layer, host view
     bool conv;
     int C, K, M, MP;  // conv
@@ -161,6 +173,8 @@ struct NetDesc {
     // [gi][mode]: gi 0 -> G=1, gi 1 -> G=gdef
     KernelFn fn[2][5] = {};  // [gi][mode]; kTrace only for nets with trace points (else nullptr)
     KernelFn fn_gated[2] = {};  // hogwild from host buffers (claims gated by the landed counter)
+    KernelFn fn_rep = nullptr;  // hogwild, G = gdef, replica emulation (nets with REPL)
+    KernelFn fn_pavg[2] = {};   // hogwild, G = gdef, fused averaging compiled in: [gated] (nets with REPL)
     int smem[2] = {0, 0};
     double flops_per_sample = 0;  // algorithmic
 };
@@ -208,6 +222,11 @@ void fill_kernels(NetDesc& d, int gi) {
     d.fn[gi][kForward] = chaos_worker<Net, G, Net::NT, kForward>;
     if constexpr (Net::TRACE) d.fn[gi][kTrace] = chaos_worker<Net, G, Net::NT, kTrace>;
     d.fn_gated[gi] = chaos_worker<Net, G, Net::NT, kHogwild, true>;
+    if constexpr (Repl<Net>::value && G == Net::GDEF) {
+        d.fn_rep = chaos_worker<Net, G, Net::NT, kHogwild, false, true>;
+        d.fn_pavg[0] = chaos_worker<Net, G, Net::NT, kHogwild, false, false, true>;
+        d.fn_pavg[1] = chaos_worker<Net, G, Net::NT, kHogwild, true, false, true>;
+    }
     d.smem[gi] = SLayout<Net, G>::BYTES;
 }
 
@@ -381,6 +400,18 @@ struct chaos_net {
     cudaEvent_t staging_free = nullptr;
     cudaEvent_t ready_copied = nullptr;  // recorded after a hogwild host epoch's last ready_host copy
     bool ready_pending = false;          // ... whose copies may still be reading ready_host
+    // fused in-kernel cross-replica averaging (chaos_pavg_*)
+    void* px = nullptr;                  // own exchange buffer: snapshot ring, flags, done, checksums
+    size_t px_bytes = 0;
+    size_t px_off_flag = 0, px_off_done = 0, px_off_cks = 0;
+    PavgArgs px_host{};                  // peer table (host copy)
+    PavgArgs* px_dev = nullptr;          // ... device copy
+    bool px_dirty = true;
+    void* px_mapped[kPavgMaxR] = {};     // IPC mappings to close
+    int px_peers_set = 0;                // bitmask of peers with a table entry
+    long long px_k = 0, px_round0 = 0, px_arm = 0;
+    int px_comm = 0;                     // CHAOS_OPT_PAVG_COMM_CTAS
+    KArgs* rep_dev = nullptr;            // replica emulation: per-replica arguments (device)
 };
 
 namespace {
@@ -388,6 +419,8 @@ namespace {
 int gidx(const chaos_net* net) { return net->group == 1 ? 0 : 1; }
 
 chaos_status ensure_kernel_attrs(chaos_net* net) {
+    for (KernelFn f : {net->d->fn_rep, net->d->fn_pavg[0], net->d->fn_pavg[1]})
+        if (f) CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, net->d->smem[1]));
     for (int gi = 0; gi < 2; ++gi) {
         CUDA_TRY(cudaFuncSetAttribute(net->d->fn_gated[gi], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       net->d->smem[gi]));
@@ -421,6 +454,8 @@ chaos_status check_latch(chaos_net* net) {
         CUDA_TRY(cudaMemsetAsync(net->latch, 0, sizeof(int), net->stream));
         CUDA_TRY(cudaStreamSynchronize(net->stream));
         if (h & kLatchLabel) return fail(CHAOS_E_LABEL, "device: a label outside [0, %d)", kClasses);
+        if (h & kLatchPavg)
+            return fail(CHAOS_E_CUDA, "device: fused averaging read a peer snapshot whose checksum does not match");
         return fail(CHAOS_E_NONFINITE, "device: non-finite loss");
     }
     return CHAOS_OK;
@@ -663,6 +698,13 @@ void chaos_net_destroy(chaos_net* net) {
     if (net->tw) cudaFree(net->tw);
     if (net->ready_copied) cudaEventDestroy(net->ready_copied);
     for (cudaEvent_t e : net->chunk_ev) cudaEventDestroy(e);
+    for (void* m : net->px_mapped)
+        if (m) cudaIpcCloseMemHandle(m);
+    if (net->px) cudaFree(net->px);
+    if (net->px_dev) cudaFree(net->px_dev);
+    if (net->px_host.dsum) cudaFree(net->px_host.dsum);
+    if (net->px_host.dabs) cudaFree(net->px_host.dabs);
+    if (net->rep_dev) cudaFree(net->rep_dev);
     void* ptrs[] = {net->params, net->latch,  net->counter, net->loss_sum, net->partial, net->grad_out, net->claims,
                     net->ev_loss, net->ev_wrong, net->ev_sum, net->ev_err, net->st_x, net->st_y, net->ptime,
                     net->progress};
@@ -702,6 +744,10 @@ chaos_status chaos_net_set_option(chaos_net* net, chaos_option opt, int64_t valu
             if (value < 0) return fail(CHAOS_E_INVALID, "stagger must be >= 0");
             net->debug_stagger = value;
             return CHAOS_OK;
+        case CHAOS_OPT_PAVG_COMM_CTAS:
+            if (value < 0 || value > 16) return fail(CHAOS_E_INVALID, "pavg comm CTAs must be in [0, 16]");
+            net->px_comm = (int)value;
+            return CHAOS_OK;
         case CHAOS_OPT_RESERVE_SMS:
             if (value < 0 || value >= net->sms) return fail(CHAOS_E_INVALID, "reserve_sms must be in [0, %d)", net->sms);
             if (net->comm && value > 0 && (net->comm_max_ctas == 0 || net->comm_max_ctas > value))
@@ -726,6 +772,7 @@ int64_t chaos_net_get_option(const chaos_net* net, chaos_option opt) {
         case CHAOS_OPT_DEBUG_TRACE: return net->debug_trace;
         case CHAOS_OPT_DEBUG_STAGGER: return net->debug_stagger;
         case CHAOS_OPT_RESERVE_SMS: return net->reserve_sms;
+        case CHAOS_OPT_PAVG_COMM_CTAS: return net->px_comm;
     }
     return -1;
 }
@@ -757,6 +804,27 @@ chaos_status chaos_net_set_params(chaos_net* net, const float* host_src, int64_t
 }  // extern "C"
 
 namespace {
+// Fused averaging arguments of the next hogwild launch (the armed rounds are consumed).
+chaos_status pavg_args(chaos_net* net, KArgs& k) {
+    const PavgArgs& h = net->px_host;
+    if (!net->px) return fail(CHAOS_E_INVALID, "chaos_pavg_arm without chaos_pavg_setup");
+    if (net->px_peers_set != (1 << h.R) - 1)
+        return fail(CHAOS_E_INVALID, "fused averaging: exchange buffers of %d replicas expected, peer mask 0x%x",
+                    h.R, net->px_peers_set);
+    if (net->px_dirty) {
+        CUDA_TRY(cudaMemcpyAsync(net->px_dev, &net->px_host, sizeof(PavgArgs), cudaMemcpyHostToDevice, net->stream));
+        net->px_dirty = false;
+    }
+    k.pavg = net->px_dev;
+    k.pavg_round0 = net->px_round0;
+    k.pavg_rounds = net->px_arm;
+    k.pavg_k = net->px_k;
+    k.pavg_comm = net->px_comm;
+    net->px_round0 += net->px_arm;
+    net->px_arm = 0;
+    return CHAOS_OK;
+}
+
 // One Training phase launch over images [0, n) (n > 0, arguments validated), accumulating into
 // the net's training-loss sum; asynchronous on the net's stream.
 chaos_status train_range(chaos_net* net, const float* d_images, const int32_t* d_labels, int64_t n, float lr,
@@ -780,21 +848,34 @@ chaos_status train_range(chaos_net* net, const float* d_images, const int32_t* d
             k.claims = net->claims;
         }
         CUDA_TRY(cudaMemsetAsync(net->counter, 0, sizeof(unsigned long long), net->stream));
-        const int grid = grid_for(net, kHogwild, (n + G - 1) / G);
+        int grid = grid_for(net, kHogwild, (n + G - 1) / G);
 #ifdef CHAOS_TIMING
-        if (net->ptime_grid < grid) {
+        if (net->ptime_grid < grid + net->px_comm) {
             if (net->ptime) cudaFree(net->ptime);
             net->ptime = nullptr;
-            CUDA_TRY(cudaMalloc(&net->ptime, sizeof(unsigned long long) * kPhases * grid));
-            net->ptime_grid = grid;
+            CUDA_TRY(cudaMalloc(&net->ptime, sizeof(unsigned long long) * kPhases * (grid + net->px_comm)));
+            net->ptime_grid = grid + net->px_comm;
         }
         CUDA_TRY(cudaMemsetAsync(net->ptime, 0, sizeof(unsigned long long) * kPhases * net->ptime_grid, net->stream));
         k.ptime = net->ptime;
 #endif
         k.progress = net->progress;
         k.ready = net->launch_ready;
+        if (net->px_arm > 0) {
+            if (net->debug_trace) return fail(CHAOS_E_UNSUPPORTED, "fused averaging is not traced");
+            if (!net->d->fn_pavg[0] || net->group != net->d->gdef)
+                return fail(CHAOS_E_UNSUPPORTED, "fused averaging is compiled for the large net at its default G");
+            chaos_status st = pavg_args(net, k);
+            if (st) return st;
+            if (net->px_comm > 0) {  // comm CTAs on SMs of their own, after the training CTAs
+                const int train = std::min(grid, net->sms - net->reserve_sms - net->px_comm);
+                if (train < 1) return fail(CHAOS_E_INVALID, "no SM left for training beside %d comm CTAs", net->px_comm);
+                grid = train + net->px_comm;
+            }
+        }
         net->progress_enqueued += (unsigned long long)n;
         KernelFn fn = k.ready ? net->d->fn_gated[gidx(net)] : net->d->fn[gidx(net)][kHogwild];
+        if (k.pavg) fn = net->d->fn_pavg[k.ready ? 1 : 0];
         if (net->debug_trace) {  // the schedule-recording instantiation (debug): records + per-group publishes
             if (k.ready) return fail(CHAOS_E_UNSUPPORTED, "trace recording is for device-buffer epochs");
             const long long groups = (n + G - 1) / G;
@@ -1230,6 +1311,202 @@ chaos_status chaos_debug_phase_times(chaos_net* net, uint64_t* host_cycles, int3
     (void)n;
     return fail(CHAOS_E_UNSUPPORTED, "phase timing needs the instrumented build (libchaos_timing.so, -DCHAOS_TIMING)");
 #endif
+}
+
+chaos_status chaos_pavg_setup(chaos_net* net, int32_t rank, int32_t world, int64_t k, int32_t nslice) {
+    if (!net) return fail(CHAOS_E_INVALID, "net is NULL");
+    if (world < 1 || world > kPavgMaxR || rank < 0 || rank >= world)
+        return fail(CHAOS_E_INVALID, "rank %d / world %d (world in [1, %d])", rank, world, kPavgMaxR);
+    if (k < 1) return fail(CHAOS_E_INVALID, "averaging interval k must be >= 1");
+    if (nslice == 0) nslice = net->sms;
+    if (nslice < 1) return fail(CHAOS_E_INVALID, "nslice must be >= 1 (0 = the SM count)");
+    if (net->px) return fail(CHAOS_E_INVALID, "chaos_pavg_setup already called for this net");
+    const long long pint = net->d->pint;
+    const int sfl = (int)(((pint + nslice - 1) / nslice + 3) / 4 * 4);
+    auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+    const size_t snap = sizeof(float) * (size_t)kPavgBufs * (size_t)nslice * (size_t)sfl;
+    net->px_off_flag = up(snap);
+    net->px_off_done = net->px_off_flag + up(sizeof(unsigned) * (size_t)nslice);
+    net->px_off_cks = net->px_off_done + up(sizeof(unsigned) * (size_t)nslice);
+    net->px_bytes = net->px_off_cks + up(sizeof(unsigned long long) * (size_t)nslice * kPavgBufs);
+    CUDA_TRY(cudaMalloc(&net->px, net->px_bytes));
+    CUDA_TRY(cudaMemset(net->px, 0, net->px_bytes));  // flags / done start at round 0
+    CUDA_TRY(cudaMalloc(&net->px_dev, sizeof(PavgArgs)));
+    PavgArgs& h = net->px_host;
+    h = PavgArgs{};
+    h.R = world;
+    h.rank = rank;
+    h.nslice = nslice;
+    h.slice_fl = sfl;
+    h.pint = pint;
+    h.latch = net->latch;
+    net->px_k = k;
+    net->px_round0 = 0;
+    net->px_arm = 0;
+    net->px_peers_set = 0;
+    net->px_dirty = true;
+    return chaos_pavg_set_peer(net, rank, net->px);
+}
+
+chaos_status chaos_pavg_exchange(chaos_net* net, int32_t peer, void** d_ptr, int64_t* bytes) {
+    if (!net || !d_ptr || !bytes) return fail(CHAOS_E_INVALID, "NULL argument");
+    if (!net->px) return fail(CHAOS_E_INVALID, "chaos_pavg_setup has not been called");
+    if (peer < 0 || peer >= net->px_host.R || !(net->px_peers_set & (1 << peer)))
+        return fail(CHAOS_E_INVALID, "no exchange buffer for rank %d", peer);
+    *d_ptr = net->px_host.snap[peer];
+    *bytes = (int64_t)net->px_bytes;
+    return CHAOS_OK;
+}
+
+chaos_status chaos_pavg_debug_sums(chaos_net* net, float* host_dsum, float* host_dabs, int64_t n) {
+    if (!net || !host_dsum || !host_dabs) return fail(CHAOS_E_INVALID, "NULL argument");
+    if (!net->px || !net->px_host.dsum) return fail(CHAOS_E_INVALID, "chaos_pavg_set_check has not been called");
+    if (n != net->d->pint) return fail(CHAOS_E_INVALID, "n=%lld != chaos_net_device_params_len=%lld", (long long)n,
+                                       net->d->pint);
+    CUDA_TRY(cudaMemcpyAsync(host_dsum, net->px_host.dsum, sizeof(float) * n, cudaMemcpyDeviceToHost, net->stream));
+    CUDA_TRY(cudaMemcpyAsync(host_dabs, net->px_host.dabs, sizeof(float) * n, cudaMemcpyDeviceToHost, net->stream));
+    CUDA_TRY(cudaStreamSynchronize(net->stream));
+    return check_latch(net);
+}
+
+chaos_status chaos_pavg_ipc_handle(chaos_net* net, void* host_handle) {
+    if (!net || !host_handle) return fail(CHAOS_E_INVALID, "NULL argument");
+    if (!net->px) return fail(CHAOS_E_INVALID, "chaos_pavg_setup has not been called");
+    static_assert(sizeof(cudaIpcMemHandle_t) == CHAOS_IPC_HANDLE_BYTES, "IPC handle size");
+    cudaIpcMemHandle_t hd;
+    CUDA_TRY(cudaIpcGetMemHandle(&hd, net->px));
+    std::memcpy(host_handle, &hd, sizeof hd);
+    return CHAOS_OK;
+}
+
+chaos_status chaos_pavg_set_peer(chaos_net* net, int32_t peer, void* d_exchange) {
+    if (!net || !d_exchange) return fail(CHAOS_E_INVALID, "NULL argument");
+    if (!net->px) return fail(CHAOS_E_INVALID, "chaos_pavg_setup has not been called");
+    PavgArgs& h = net->px_host;
+    if (peer < 0 || peer >= h.R) return fail(CHAOS_E_INVALID, "peer %d outside [0, %d)", peer, h.R);
+    if (reinterpret_cast<uintptr_t>(d_exchange) & 255) return fail(CHAOS_E_INVALID, "exchange buffer not 256-B aligned");
+    char* b = static_cast<char*>(d_exchange);
+    h.snap[peer] = reinterpret_cast<float*>(b);
+    h.flag[peer] = reinterpret_cast<unsigned*>(b + net->px_off_flag);
+    h.done[peer] = reinterpret_cast<unsigned*>(b + net->px_off_done);
+    h.cks[peer] = reinterpret_cast<unsigned long long*>(b + net->px_off_cks);
+    net->px_peers_set |= 1 << peer;
+    net->px_dirty = true;
+    return CHAOS_OK;
+}
+
+chaos_status chaos_pavg_open_peer(chaos_net* net, int32_t peer, const void* host_handle) {
+    if (!net || !host_handle) return fail(CHAOS_E_INVALID, "NULL argument");
+    if (!net->px) return fail(CHAOS_E_INVALID, "chaos_pavg_setup has not been called");
+    if (peer < 0 || peer >= net->px_host.R || peer == net->px_host.rank)
+        return fail(CHAOS_E_INVALID, "peer %d: not another rank of [0, %d)", peer, net->px_host.R);
+    if (net->px_mapped[peer]) return fail(CHAOS_E_INVALID, "peer %d already opened", peer);
+    cudaIpcMemHandle_t hd;
+    std::memcpy(&hd, host_handle, sizeof hd);
+    void* p = nullptr;
+    CUDA_TRY(cudaSetDevice(net->dev));
+    CUDA_TRY(cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess));
+    net->px_mapped[peer] = p;
+    return chaos_pavg_set_peer(net, peer, p);
+}
+
+chaos_status chaos_pavg_arm(chaos_net* net, int64_t rounds) {
+    if (!net) return fail(CHAOS_E_INVALID, "net is NULL");
+    if (!net->px) return fail(CHAOS_E_INVALID, "chaos_pavg_setup has not been called");
+    if (rounds < 0 || rounds > (1 << 20)) return fail(CHAOS_E_INVALID, "rounds must be in [0, 2^20]");
+    net->px_arm = rounds;
+    return CHAOS_OK;
+}
+
+int64_t chaos_pavg_rounds_done(const chaos_net* net) { return net ? net->px_round0 : -1; }
+
+chaos_status chaos_pavg_set_check(chaos_net* net, int32_t on) {
+    if (!net) return fail(CHAOS_E_INVALID, "net is NULL");
+    if (!net->px) return fail(CHAOS_E_INVALID, "chaos_pavg_setup has not been called");
+    net->px_host.check = on ? 1 : 0;
+    if (on) {  // (re)start the delta sums
+        const size_t b = sizeof(float) * (size_t)net->d->pint;
+        if (!net->px_host.dsum) {
+            CUDA_TRY(cudaMalloc(&net->px_host.dsum, b));
+            CUDA_TRY(cudaMalloc(&net->px_host.dabs, b));
+        }
+        CUDA_TRY(cudaMemsetAsync(net->px_host.dsum, 0, b, net->stream));
+        CUDA_TRY(cudaMemsetAsync(net->px_host.dabs, 0, b, net->stream));
+    }
+    net->px_dirty = true;
+    return CHAOS_OK;
+}
+
+chaos_status chaos_train_epoch_replicas(chaos_net* const* nets, int32_t R, const float* const* d_images,
+                                        const int32_t* const* d_labels, const int64_t* n, float lr) {
+    if (!nets || !d_images || !d_labels || !n) return fail(CHAOS_E_INVALID, "NULL argument");
+    if (R < 1 || R > kPavgMaxR) return fail(CHAOS_E_INVALID, "R must be in [1, %d]", kPavgMaxR);
+    if (!std::isfinite(lr)) return fail(CHAOS_E_INVALID, "lr is not finite");
+    chaos_net* n0 = nets[0];
+    if (!n0) return fail(CHAOS_E_INVALID, "nets[0] is NULL");
+    if (!n0->d->fn_rep) return fail(CHAOS_E_UNSUPPORTED, "net %s has no replica-emulation build", n0->d->name);
+    if (n0->group != n0->d->gdef) return fail(CHAOS_E_INVALID, "replica emulation runs at the net's default G");
+    const int G = n0->group;
+    const int comm = n0->px_arm > 0 ? n0->px_comm : 0;
+    int cta = (n0->sms - n0->reserve_sms) / R - comm;  // training CTAs per replica
+    if ((long long)cta * G > n0->d->max_inflight) cta = n0->d->max_inflight / G;
+    if (n0->max_ctas > 0 && cta > n0->max_ctas) cta = n0->max_ctas;
+    if (cta < 1) return fail(CHAOS_E_INVALID, "no training CTA per replica");
+    std::vector<KArgs> ka((size_t)R);
+    for (int r = 0; r < R; ++r) {
+        chaos_net* net = nets[r];
+        if (!net || net->d != n0->d || net->dev != n0->dev || net->group != G)
+            return fail(CHAOS_E_INVALID, "replica %d: NULL, another arch / device or another G", r);
+        if (n[r] < 1 || !d_images[r] || !d_labels[r]) return fail(CHAOS_E_INVALID, "replica %d: empty shard", r);
+        if (net->debug_trace) return fail(CHAOS_E_UNSUPPORTED, "replica emulation is not traced");
+        for (int q = 0; q < r; ++q)
+            if (nets[q] == net) return fail(CHAOS_E_INVALID, "replica %d repeats replica %d", r, q);
+        KArgs k = base_args(net);
+        k.images = d_images[r];
+        k.labels = d_labels[r];
+        k.n = n[r];
+        k.neg_lr = -lr;
+        k.loss_sum = net->loss_sum;
+        k.progress = net->progress;
+        if (net->px_arm > 0) {
+            if (!net->px || net->px_host.R != R || net->px_host.rank != r)
+                return fail(CHAOS_E_INVALID, "replica %d: fused averaging set up for rank %d of %d", r,
+                            net->px ? net->px_host.rank : -1, net->px ? net->px_host.R : 0);
+            if (net->px_arm != n0->px_arm || net->px_round0 != n0->px_round0 || net->px_comm != n0->px_comm)
+                return fail(CHAOS_E_INVALID, "replica %d: armed rounds / comm CTAs differ from replica 0", r);
+        }
+        ka[(size_t)r] = k;
+    }
+    for (int r = 0; r < R; ++r) {  // after validation: consumes the armed rounds
+        chaos_net* net = nets[r];
+        if (net != n0) CUDA_TRY(cudaStreamSynchronize(net->stream));  // its earlier work precedes the launch
+        CUDA_TRY(cudaMemsetAsync(net->counter, 0, sizeof(unsigned long long), n0->stream));
+        CUDA_TRY(cudaMemsetAsync(net->loss_sum, 0, sizeof(double), n0->stream));
+        net->last_train_n = n[r];
+        net->progress_enqueued += (unsigned long long)n[r];
+        if (net->px_arm > 0) {
+            chaos_status st = pavg_args(net, ka[(size_t)r]);
+            if (st) return st;
+            if (net != n0) CUDA_TRY(cudaStreamSynchronize(net->stream));  // its table copy
+        }
+    }
+    if (!n0->rep_dev) CUDA_TRY(cudaMalloc(&n0->rep_dev, sizeof(KArgs) * kPavgMaxR));
+    CUDA_TRY(cudaMemcpyAsync(n0->rep_dev, ka.data(), sizeof(KArgs) * (size_t)R, cudaMemcpyHostToDevice, n0->stream));
+    KArgs k0 = ka[0];
+    k0.reps = n0->rep_dev;
+    k0.rep_ctas = cta + comm;
+    void* args[] = {&k0};
+    // cooperative: all R * cta CTAs are co-resident (the replicas' CTAs wait on one another)
+    CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(n0->d->fn_rep), dim3((unsigned)(R * (cta + comm))),
+                                         dim3((unsigned)n0->d->nt), args, (size_t)n0->d->smem[gidx(n0)], n0->stream));
+    for (int r = 1; r < R; ++r) {  // the replicas' own streams wait for the launch
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventRecord(e, n0->stream));
+        CUDA_TRY(cudaStreamWaitEvent(nets[r]->stream, e, 0));
+        CUDA_TRY(cudaEventDestroy(e));
+    }
+    return CHAOS_OK;
 }
 
 chaos_status chaos_net_sync(chaos_net* net) {

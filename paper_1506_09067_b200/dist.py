@@ -269,6 +269,58 @@ class DistTrainer:
         if cuda:
             ts.wait_stream(cs)
 
+    def setup_fused(self, comm_ctas: int | None = None):
+        """Fused in-kernel averaging (fused variant; chaos_pavg_*):
+        the persistent hogwild kernel itself averages the replicas through peer memory -- no
+        collective launch beside it.  ``comm_ctas`` (default 1 for up to 2 ranks, else 2) extra CTAs
+        of the launch run the rounds (8 slices each) while the training CTAs never stall; 0 = the
+        training CTAs run them between image groups (148 slices).  Each rank allocates its exchange
+        buffer (snapshot ring + flags) and the ranks trade its CUDA IPC handle (an all-gather of 64
+        bytes); every rank maps every other rank's buffer (NVLink peer access)."""
+        import torch
+        import torch.distributed as dist
+        if comm_ctas is None:
+            comm_ctas = 1 if self.world <= 2 else 2
+        if hasattr(self.net, "set_option"):
+            from .chaos import OPT_PAVG_COMM_CTAS
+            self.net.set_option(OPT_PAVG_COMM_CTAS, comm_ctas)
+        self.comm_ctas = comm_ctas
+        self.net.pavg_setup(self.rank, self.world, self.k, 8 * comm_ctas if comm_ctas else 0)
+        if self.world > 1:
+            h = torch.tensor(list(self.net.pavg_ipc_handle()), dtype=torch.uint8)
+            if dist.get_backend(self.group) == "nccl":
+                h = h.cuda()
+            hs = [torch.zeros_like(h) for _ in range(self.world)]
+            dist.all_gather(hs, h, group=self.group)
+            for q, hq in enumerate(hs):
+                if q != self.rank:
+                    self.net.pavg_open_peer(q, bytes(hq.cpu().tolist()))
+        self.n_fused_rounds = 0
+        self._fused = True
+
+    def epoch_fused(self, images, labels, lr: float, lo: int = 0, hi: int | None = None, host=None,
+                    chunks: int = 8):
+        """One Training phase with the fused averaging (after ``setup_fused``): ONE hogwild launch
+        over the shard with ``len(async_targets(shortest shard, K))`` in-kernel averaging rounds
+        armed -- the same count on every rank (a round's CTAs wait for every replica's snapshot of
+        their slices) -- then one exact average of the parameters on the net's stream, after which
+        the replicas are identical.  ``host``/``chunks``: see ``_launch`` (the host entry is one
+        gated launch, so the armed rounds cover the whole shard)."""
+        hi = int(labels.shape[0]) if hi is None else hi
+        if not (self.world > 1 or self.force):
+            self._launch(images, labels, lr, lo, hi, host, chunks)
+            return
+        if not getattr(self, "_fused", False):
+            raise RuntimeError("epoch_fused needs setup_fused() first")
+        rounds = len(async_targets(self._agreed(hi - lo, "min"), self.k))
+        self.net.pavg_arm(rounds)
+        self._launch(images, labels, lr, lo, hi, host, chunks)
+        self.n_fused_rounds += rounds
+        params = self.net.device_params()
+        with self._on_net_stream(params):
+            self._average(params)
+        self.n_collectives += 1
+
     def sync_epoch(self, images, labels, lr: float, batch: int, grad=None):
         """Deterministic multi-GPU sync SGD: for every consecutive global
         batch of ``batch`` images, rank r computes the fixed-order gradient sum of its contiguous

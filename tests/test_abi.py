@@ -75,3 +75,19 @@ def test_oracle_shares_nothing_with_product():
     for f in os.listdir(os.path.join(ROOT, "oracle")):
         if f.endswith((".c", ".h", ".py")):
             assert not pat_orc.search(open(os.path.join(ROOT, "oracle", f)).read()), f
+
+
+def test_bench_kernels_do_not_spill():
+    # the large-net workers (the bench kernel and its fused-averaging / replica variants) at 640
+    # threads x 96 registers: no local-memory stack (a spill in the hot loop cost 25% once)
+    import shutil
+    import subprocess
+    from paper_1506_09067_b200.chaos import LIB_PATH
+    if not shutil.which("cuobjdump") or not os.path.exists(LIB_PATH):
+        pytest.skip("cuobjdump or libchaos.so missing")
+    out = subprocess.run(["cuobjdump", "--dump-resource-usage", LIB_PATH], capture_output=True, text=True).stdout
+    fns = re.findall(r"Function (\S+):\s*\n\s*(REG:\d+ STACK:\d+)", out)
+    large = [(f, r) for f, r in fns if "chaos_worker" in f and "LargeNetELi4ELi640" in f and "PaperLarge" not in f]
+    assert len(large) >= 7, len(large)
+    for f, r in large:
+        assert r.endswith("STACK:0"), (f, r)

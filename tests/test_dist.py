@@ -341,3 +341,76 @@ def test_gloo_world2_uneven_shards_agree_on_collective_count():
             assert (n0, n1) == (1025, 1021)
             np.testing.assert_array_equal(g0[0], g0[1])
     assert [o[1] for o in res[0][1]] == [2, 1]
+
+
+class FakeFusedNet(FakeNet):
+    """FakeNet plus the chaos_pavg_* host surface: the exchange buffer's 'IPC handle' names the rank
+    that made it; opened peers and armed rounds are recorded (the in-kernel rounds themselves are
+    GPU-tested: tests/test_gpu_pavg.py)."""
+
+    def pavg_setup(self, rank, world, k, nslice=0):
+        self.setup = (rank, world, k)
+        self.opened = {}
+        self.armed = []
+
+    def pavg_ipc_handle(self):
+        return bytes([self.rank]) + b"h" * 63
+
+    def pavg_open_peer(self, peer, handle):
+        assert len(handle) == 64 and peer not in self.opened
+        self.opened[peer] = handle[0]
+
+    def pavg_arm(self, rounds):
+        self.armed.append(rounds)
+
+
+def _fused_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # uneven shards (1029 / 1021 / 1000 images at K = 256): every rank arms the rounds of the
+        # shortest shard, launches once per epoch and ends with one exact average
+        edges = [(0, 1029), (1029, 2050), (2050, 3050)]
+        lo, hi = edges[rank]
+        X = torch.ones(3050, 3)
+        Y = torch.zeros(3050, dtype=torch.int32)
+        net = FakeFusedNet(8, rank)
+        net.w = net.w.double()
+        tr = DistTrainer(net, rank, world, 256)
+        with pytest.raises(RuntimeError):
+            tr.epoch_fused(X, Y, 0.01, lo, hi)  # setup_fused first
+        tr.setup_fused()
+        for _ in range(2):
+            tr.epoch_fused(X, Y, 0.01, lo, hi)
+        gathered = [torch.zeros_like(net.w) for _ in range(world)]
+        dist.all_gather(gathered, net.w)
+        q.put((rank, net.setup, net.opened, net.armed, net.calls, tr.n_collectives, tr.n_fused_rounds,
+               [g.numpy() for g in gathered]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world3_fused_averaging_host_logic():
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fused_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rounds = len(async_targets(1000, 256))
+    assert rounds == 3
+    sizes = [1029, 1021, 1000]
+    for rank, setup, opened, armed, calls, ncoll, nfused, gathered in res:
+        assert setup == (rank, world, 256)
+        assert opened == {q: q for q in range(world) if q != rank}  # every peer's handle, at its index
+        assert armed == [rounds, rounds]
+        assert calls == [sizes[rank], sizes[rank]]  # one launch per epoch
+        assert ncoll == 2 and nfused == 2 * rounds
+        for g in gathered[1:]:
+            np.testing.assert_array_equal(g, gathered[0])  # identical after the exact average
