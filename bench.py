@@ -199,7 +199,7 @@ def main():
     ap.add_argument("--force-dist", action="store_true",
                     help="run the multi-GPU leg (NCCL process group, configs[4] shards, averaging every K) "
                          "even with one rank -- exercises the N>1 code path on one GPU")
-    ap.add_argument("--avg", default="async", choices=["interval", "async", "fused"],
+    ap.add_argument("--avg", default="fused", choices=["interval", "async", "fused"],
                     help="multi-GPU hogwild averaging: 'interval' = one launch per K images, then a blocking "
                          "NCCL average; 'async' = one launch per shard with in-flight averages every K images on "
                          "a second stream (SURVEY NEXT-2); 'fused' = the persistent kernel averages the replicas "
