@@ -556,7 +556,11 @@ __device__ __forceinline__ float warp_sum(float v) {
 // MGF: map groups fastest over the lanes (a warp's lanes read a few windows' patches -- broadcasts,
 // distinct banks -- and the map groups' weight vectors) instead of windows fastest (neighbouring
 // windows 2 columns apart share banks)
-template <class L, int NT, bool MGF = false>
+// PL > 0 (image pairs): a warp's lanes = PL windows x 2 images x 32 / (2 PL) map groups, so its patch
+// loads come from two images whose offsets differ by an odd-bank-shifting stride -- 2 x PL distinct
+// addresses in distinct banks (the windows-fastest order puts 16 windows of one image, 2 columns
+// apart, on 16 of the 32 banks: 2-way conflicts, profiles/r4)
+template <class L, int NT, bool MGF = false, int PL = 0>
 __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const float* __restrict__ wsm,
                                          float* __restrict__ out, uint8_t* __restrict__ am, int cnt) {
     constexpr int MT = L::MT, KP = L::KP, K = L::K, PW = L::PW, P = L::P, MG = L::M / MT;
@@ -565,13 +569,27 @@ __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const flo
     constexpr bool A2 = (MT % 2 == 0);  // row pitch MP is a multiple of 4, so mg*MT is even
     constexpr int NSPL = L::NSPL, CH = L::C / NSPL;
     static_assert(NT % 32 == 0, "lane pairs never straddle warps");
-    const int total = MG * cnt * P * NSPL;
+    static_assert(PL == 0 || (!MGF && NSPL == 1 && 32 % (2 * (PL > 0 ? PL : 1)) == 0), "image-pair lane map");
+    constexpr int MGL = PL > 0 ? 32 / (2 * PL) : 1;            // map groups per warp
+    constexpr int NPB = PL > 0 ? (P + PL - 1) / PL : 1;         // window blocks
+    constexpr int NMB = (MG + MGL - 1) / MGL;                   // map-group blocks
+    const int total = PL > 0 ? NMB * ((cnt + 1) / 2) * NPB * 32 : MG * cnt * P * NSPL;
     for (int it = threadIdx.x; it < total; it += NT) {
-        const int half = it % NSPL;
-        const int p = MGF ? ((it / NSPL) / MG) % P : (it / NSPL) % P;
-        const int t = MGF ? 0 : (it / NSPL) / P;
-        const int g = MGF ? ((it / NSPL) / MG) / P : t % cnt;
-        const int mg = MGF ? (it / NSPL) % MG : t / cnt;
+        int half, p, g, mg;
+        if constexpr (PL > 0) {
+            const int l = it & 31, r = it >> 5;
+            half = 0;
+            p = (r % NPB) * PL + l % PL;
+            g = ((r / NPB) % ((cnt + 1) / 2)) * 2 + (l / PL) % 2;
+            mg = (r / NPB / ((cnt + 1) / 2)) * MGL + l / (2 * PL);
+            if (p >= P || g >= cnt || mg >= MG) continue;
+        } else {
+            half = it % NSPL;
+            p = MGF ? ((it / NSPL) / MG) % P : (it / NSPL) % P;
+            const int t = MGF ? 0 : (it / NSPL) / P;
+            g = MGF ? ((it / NSPL) / MG) / P : t % cnt;
+            mg = MGF ? (it / NSPL) % MG : t / cnt;
+        }
         const int pr = p / PW, pc = p - (p / PW) * PW;
         float acc[MT][KP * KP];
         {
@@ -1952,7 +1970,10 @@ __device__ __forceinline__ void conv_din_winp(const float* __restrict__ wsm, con
 //            sum is fixed (g, w, then m or the task's own order): deterministic, whichever warp runs
 //            a task.  out must not alias in / dp.  ctr: one int of shared memory, 0 on entry.
 // ------------------------------------------------------------------------------------
-template <class L, int NT, int MODE>
+// MS = 2: each (image, 32 input maps) delta_in task is split over two warps by output-map halves
+// (the δ_in warps' serial chains are the phase's critical path); the first half's sums go through
+// `out` to its partner (named barrier per pair), which adds its own in a fixed order.
+template <class L, int NT, int MODE, int MS = 1>
 __device__ __forceinline__ void conv_bwd_sparse(const KArgs& a, int slot, const float* __restrict__ wsm,
                                                 const float* __restrict__ dp, const uint8_t* __restrict__ am,
                                                 const float* __restrict__ in, float* __restrict__ out, int woff,
@@ -1961,10 +1982,16 @@ __device__ __forceinline__ void conv_bwd_sparse(const KArgs& a, int slot, const 
     constexpr int H = L::H, W = L::W, HW = H * W, HR = L::HR, WR = L::WR, BS = KP + K - 1;
     constexpr int NCW = (C + 31) / 32, NMG = M / 4, NTASK = NMG * NCW;
     static_assert(KP == 2 && M % 4 == 0 && L::MP == M, "2x2 pooling, 4 maps per vector");
+    static_assert(MS == 1 || MS == 2, "delta_in split over 1 or 2 warps");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#ifdef CHAOS_TIMING
+    const long long t_in = clock64();
+#endif
     // ---- delta_in
-    if (warp < cnt * NCW) {
-        const int cw = warp % NCW, g = warp / NCW;
+    if (warp < cnt * NCW * MS) {
+        const int sp = warp % MS, cw = (warp / MS) % NCW, g = warp / (MS * NCW);
+        constexpr int M4H = (NMG + 1) / 2 * 4;  // MS = 2: maps [0, M4H) and [M4H, M)
+        const int mlo = (MS == 2 && sp == 1) ? M4H : 0, mhi = (MS == 2 && sp == 0) ? M4H : M;
         const int n = cw * 32 + lane;
         const bool act = n < C;
         const float* wn = wsm + (act ? n : 0) * KK * L::MP;
@@ -1976,7 +2003,7 @@ __device__ __forceinline__ void conv_bwd_sparse(const KArgs& a, int slot, const 
 #pragma unroll
             for (int x = 0; x < WR; ++x) acc[y][x] = 0.f;
 #pragma unroll 1
-        for (int m4 = 0; m4 < M; m4 += 4) {
+        for (int m4 = mlo; m4 < mhi; m4 += 4) {
             float4 w4[KK];
 #pragma unroll
             for (int tp = 0; tp < KK; ++tp) w4[tp] = *reinterpret_cast<const float4*>(wn + tp * L::MP + m4);
@@ -2033,9 +2060,25 @@ __device__ __forceinline__ void conv_bwd_sparse(const KArgs& a, int slot, const 
                 }
             }
         }
-        if (act) {
+        float* ob = out + g * L::IN_SZ + (act ? n : 0) * HW;
+        if constexpr (MS == 2) {  // first half -> out (raw sums), pair barrier, second half adds
+            const int pair = 1 + g * NCW + cw;
+            if (sp == 0 && act) {
+#pragma unroll
+                for (int y = 0; y < HR; ++y)
+#pragma unroll
+                    for (int x = 0; x < WR; ++x) ob[y * W + x] = acc[y][x];
+            }
+            asm volatile("bar.sync %0, 64;" ::"r"(pair) : "memory");
+            if (sp == 1 && act) {
+#pragma unroll
+                for (int y = 0; y < HR; ++y)
+#pragma unroll
+                    for (int x = 0; x < WR; ++x) acc[y][x] = ob[y * W + x] + acc[y][x];
+            }
+        }
+        if (act && (MS == 1 || sp == 1)) {
             const float* ib = in + g * L::IN_SZ + n * HW;
-            float* ob = out + g * L::IN_SZ + n * HW;
 #pragma unroll
             for (int y = 0; y < H; ++y)
 #pragma unroll
@@ -2044,6 +2087,9 @@ __device__ __forceinline__ void conv_bwd_sparse(const KArgs& a, int slot, const 
                     ob[y * W + x] = (y < HR && x < WR ? acc[y < HR ? y : 0][x < WR ? x : 0] : 0.f) * (1.f - v * v);
                 }
         }
+#ifdef CHAOS_TIMING
+        if (threadIdx.x == 0 && a.ptime) a.ptime[blockIdx.x * kPhases + 17] += clock64() - t_in;
+#endif
     }
     // ---- weight gradient: tasks (4 output maps, 32 input maps) from the shared counter
     for (;;) {
@@ -2132,6 +2178,9 @@ __device__ __forceinline__ void conv_bwd_sparse(const KArgs& a, int slot, const 
                                    make_float4(sc * accb[0], sc * accb[1], sc * accb[2], sc * accb[3]));
         }
     }
+#ifdef CHAOS_TIMING
+    if (threadIdx.x == NT - 32 && a.ptime) a.ptime[blockIdx.x * kPhases + 18] += clock64() - t_in;
+#endif
 }
 
 // ------------------------------------------------------------------------------------
@@ -3023,7 +3072,14 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a0) {
         PTIME(1);
 
         // ---------------- a2: conv -> tanh -> pool, layer by layer
-        conv_fwd<C1, NT, CHAOS_MGF_C1>(sS, wb, a1, am1, cnt);
+#ifndef CHAOS_PL_C1  // conv1 / conv3 forward: image-pair lane map with this many windows per warp (0: off)
+#define CHAOS_PL_C1 0
+#endif
+#ifndef CHAOS_PL_C3
+#define CHAOS_PL_C3 4
+#endif
+        constexpr int PL1 = (NCONV >= 3 && !BIG && !CHAOS_MGF_C1 && C1::NSPL == 1 && (C1::IN_SZ & 1)) ? CHAOS_PL_C1 : 0;
+        conv_fwd<C1, NT, CHAOS_MGF_C1, PL1>(sS, wb, a1, am1, cnt);
         float* alast = a1;
         if constexpr (NCONV >= 2) {
             fence_async_smem();
@@ -3066,7 +3122,8 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a0) {
             L3.wait();
             TR_RE(2, 0);
             TR_DUMP(0, O::c3w, wb, C3::BLK);
-            conv_fwd<C3, NT, CHAOS_MGF_C3>(a2, wb, a3, am3, cnt);
+            constexpr int PL3 = (!CHAOS_MGF_C3 && C3::NSPL == 1 && C3::P <= 16) ? CHAOS_PL_C3 : 0;
+            conv_fwd<C3, NT, CHAOS_MGF_C3, PL3>(a2, wb, a3, am3, cnt);
             alast = a3;
         }
         fence_async_smem();  // WB (read by the conv forward) is refilled by the async proxy next
@@ -3282,7 +3339,11 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a0) {
                     int* ctr = reinterpret_cast<int*>(smem + 72);  // header word (kHdrBytes), reset here
                     if (threadIdx.x == 0) *ctr = 0;
                     __syncthreads();
-                    conv_bwd_sparse<C3, NT, MODE>(a, slot, wb, a3, am3, a2, sS, O::c3w, cnt, sc, ctr);
+#ifndef CHAOS_C3_MS  // conv3 delta_in: warps per (image, 32 input maps) task
+#define CHAOS_C3_MS 1
+#endif
+                    constexpr int C3MS = (G * ((C3::C + 31) / 32) * CHAOS_C3_MS <= NT / 32) ? CHAOS_C3_MS : 1;
+                    conv_bwd_sparse<C3, NT, MODE, C3MS>(a, slot, wb, a3, am3, a2, sS, O::c3w, cnt, sc, ctr);
                     __syncthreads();
                     PTIME(9);
                 } else if constexpr (C3::GWIN > 0) {

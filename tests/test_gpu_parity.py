@@ -592,7 +592,7 @@ def test_two_rank_sync_emulated_matches_oracle(torch_cuda):
     assert_parity(runs[0], ref, o.blocks())
 
 
-@pytest.mark.parametrize("mode", ["hogwild", "sync", "hogwild_dist", "hogwild_dist_chaoscomm"])
+@pytest.mark.parametrize("mode", ["hogwild", "sync", "hogwild_dist", "hogwild_dist_async", "hogwild_dist_chaoscomm"])
 def test_bench_line_contract(mode, torch_cuda):
     # bench.py's JSON line on one GPU: contract keys, roofline + cpu_baseline objects, e2e with host bytes
     import subprocess
@@ -602,8 +602,10 @@ def test_bench_line_contract(mode, torch_cuda):
            "--mode", mode.split("_")[0]]
     if mode != "hogwild":
         cmd.append("--no-cpu-baseline")
-    if mode.startswith("hogwild_dist"):  # the N>1 code path on one GPU: one-rank NCCL group, async averaging
+    if mode.startswith("hogwild_dist"):  # the N>1 code path on one GPU: one-rank NCCL group, fused averaging
         cmd.append("--force-dist")
+    if mode == "hogwild_dist_async":  # ... or the in-flight NCCL averaging on reserved SMs
+        cmd += ["--avg", "async"]
     if mode == "hogwild_dist_chaoscomm":  # ... with the library's own communicator
         cmd += ["--comm", "chaos"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
@@ -619,7 +621,10 @@ def test_bench_line_contract(mode, torch_cuda):
     if mode == "hogwild":
         assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
     if mode.startswith("hogwild_dist"):
-        assert d["config"]["averaging"] == "async" and d["collectives"] >= 2
+        avg = "async" if mode == "hogwild_dist_async" else "fused"
+        assert d["config"]["averaging"] == avg and d["collectives"] >= (2 if avg == "async" else 1)
+        if avg == "fused":  # in-kernel rounds every K = 1,024 claimed images of the 60,000
+            assert d["fused_rounds"] == 58 and d["config"]["pavg_comm_ctas"] == 1  # 1 timed step
         assert d["eval"]["test_errors"] < 0.05 * d["eval"]["images"]
 
 
