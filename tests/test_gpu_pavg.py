@@ -65,7 +65,8 @@ def fixed_order_rounds(ws, T):
     return ws
 
 
-@pytest.mark.parametrize("R,nslice,T,comm", [(2, 0, 3, 0), (4, 0, 2, 0), (3, 37, 5, 0), (2, 16, 3, 1), (4, 9, 4, 2)])
+@pytest.mark.parametrize("R,nslice,T,comm", [(2, 0, 3, 0), (4, 0, 2, 0), (3, 37, 5, 0), (2, 16, 3, 1), (4, 9, 4, 2),
+                                             (8, 0, 3, 0), (8, 16, 3, 1)])
 def test_rounds_without_training_are_the_fixed_order_iteration(R, nslice, T, comm, torch_cuda):
     # lr = 0: the replicas start from different weights and only the averaging changes them; every
     # slice of every replica runs T sequential rounds, so the result is exactly fixed_order_rounds
