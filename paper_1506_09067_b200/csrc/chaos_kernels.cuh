@@ -964,6 +964,9 @@ __device__ __forceinline__ void conv_fwd_slab(const float* __restrict__ in, cons
 // layout (splits reduced in a fixed order) and published with one bulk op; otherwise
 // each element is published directly.
 // ------------------------------------------------------------------------------------
+#ifndef CHAOS_GW_UNROLL  // conv_gw: unroll of the (image, window) loop (code size vs. the 32 KB L1.5 I-cache)
+#define CHAOS_GW_UNROLL 4
+#endif
 template <class L, int NT, int MODE, bool SCRATCH>
 __device__ __forceinline__ void conv_gw(const KArgs& a, int slot, const float* __restrict__ in,
                                         const float* __restrict__ dp, const uint8_t* __restrict__ am,
@@ -996,7 +999,8 @@ __device__ __forceinline__ void conv_gw(const KArgs& a, int slot, const float* _
         const float* ing = in + g * L::IN_SZ + n * HW;
         const float* dpg = dp + g * L::OUT_SZ + m * P;
         const uint8_t* amg = am + g * L::OUT_SZ + m * P;
-#pragma unroll 4
+        constexpr int GWU = CHAOS_GW_UNROLL;
+#pragma unroll GWU
         for (int q = q0; q < q1; ++q) {
             const float d = dpg[pp];
             int arg = 0;
@@ -2834,6 +2838,10 @@ __device__ __forceinline__ void pavg_comm_loop(const KArgs& a, int ccta, int* ct
     }
 }
 
+// ------------------------------------------------------------------------------------
+// PHASE(worker) The worker kernel: hogwild training, sync-batch gradients, evaluation, forward.
+// ------------------------------------------------------------------------------------
+// GATED (hogwild from host buffers only): claims wait for the copy stream's landed-images counter.
 // REP (one-GPU emulation of replicas, hogwild only): CTA b runs replica b / a0.rep_ctas with that
 // replica's arguments a0.reps[b / a0.rep_ctas].
 template <bool REP>
