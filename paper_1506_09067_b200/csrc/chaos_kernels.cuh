@@ -64,6 +64,16 @@ struct DinPair<N, std::void_t<decltype(N::DINSPLIT)>> {
     static constexpr int value = N::DINSPLIT;
 };
 
+// 2-conv nets whose conv2 delta_in runs window row by window row (conv_din_rows) declare DINROWS = true
+template <class N, class = void>
+struct DinRows {
+    static constexpr bool value = false;
+};
+template <class N>
+struct DinRows<N, std::void_t<decltype(N::DINROWS)>> {
+    static constexpr bool value = N::DINROWS;
+};
+
 // Nets whose conv3 / FC1 weights are too large to stage in shared memory (Table I large net,
 // SURVEY NEXT-1) declare BIGW = true: W1 + W2 are staged once per iteration and kept; conv3
 // and FC1 weights are read from L2 on demand.
@@ -196,8 +206,8 @@ struct SLayout {
     static constexpr int BS = Z + G * kZStride;
     static constexpr int WB = BS + kBiasScratch;
     static constexpr int DPB = (Net::NCONV == 2 && DinPair<Net>::value > 1)
-                                   ? (Net::NT / 32 / DinPair<Net>::value) * (DinPair<Net>::value - 1) * C2::RB * C2::W *
-                                         (C2::C < 32 ? C2::C : 32)
+                                   ? (Net::NT / 32 / DinPair<Net>::value) * (DinPair<Net>::value - 1) *
+                                         cmax(C2::RB * C2::W, C2::KP * C2::WR) * (C2::C < 32 ? C2::C : 32)
                                    : 0;
     // FWB: the 1-conv nets' (tiny) FC weights + bias, TMA-staged per iteration (read twice, by
     // the forward and by delta_in, instead of twice from L2)
@@ -1362,42 +1372,108 @@ __device__ __forceinline__ void conv_din(const float* __restrict__ wsm, const fl
         const float* dpg = dp + g * L::OUT_SZ;
         const uint8_t* amg = am + g * L::OUT_SZ;
         const int pr0 = b * R2;
+#ifndef CHAOS_DIN_V2  // conv_din: weights of two maps per 8-B load (lanes over input maps hit 4 banks
+#define CHAOS_DIN_V2 0   // with scalar loads: 5-way conflicts on the medium net) and a switch on the phase
+#endif
+        constexpr bool V2 = CHAOS_DIN_V2 && (L::MP % 2 == 0) && (M % (2 * MSPLIT) == 0);
+        float w2n[V2 ? KK : 1];  // the second map's weights of the pair (V2)
+        (void)w2n;
 #pragma unroll 1
         for (int m = m_lo; m < m_hi; ++m) {
             float w[KK];
+            if constexpr (V2) {
+                if (((m - m_lo) & 1) == 0) {
 #pragma unroll
-            for (int tp = 0; tp < KK; ++tp) w[tp] = wn[tp * L::MP + m];
-            float dv[NWR][PW];
-            int av[NWR][PW];
+                    for (int tp = 0; tp < KK; ++tp) {
+                        const float2 t2 = *reinterpret_cast<const float2*>(wn + tp * L::MP + m);
+                        w[tp] = t2.x;
+                        w2n[tp] = t2.y;
+                    }
+                } else {
 #pragma unroll
-            for (int dr = 0; dr < NWR; ++dr) {
-                const int pr = pr0 + DLO + dr;
-                const bool ok = pr >= 0 && pr < PH;
+                    for (int tp = 0; tp < KK; ++tp) w[tp] = w2n[tp];
+                }
+            } else {
 #pragma unroll
-                for (int pc = 0; pc < PW; ++pc) {
-                    const int o = m * P + (ok ? pr : 0) * PW + pc;
-                    dv[dr][pc] = ok ? dpg[o] : 0.f;
-                    av[dr][pc] = ok ? static_cast<int>(amg[o]) : -1;
+                for (int tp = 0; tp < KK; ++tp) w[tp] = wn[tp * L::MP + m];
+            }
+#ifndef CHAOS_DIN_LATE_D  // conv_din: load each window's (delta, phase) right before its use (fewer registers)
+#define CHAOS_DIN_LATE_D 1
+#endif
+            constexpr bool LATE = CHAOS_DIN_LATE_D;
+            float dv[LATE ? 1 : NWR][PW];
+            int av[LATE ? 1 : NWR][PW];
+            if constexpr (!LATE) {
+#pragma unroll
+                for (int dr = 0; dr < NWR; ++dr) {
+                    const int pr = pr0 + DLO + dr;
+                    const bool ok = pr >= 0 && pr < PH;
+#pragma unroll
+                    for (int pc = 0; pc < PW; ++pc) {
+                        const int o = m * P + (ok ? pr : 0) * PW + pc;
+                        dv[dr][pc] = ok ? dpg[o] : 0.f;
+                        av[dr][pc] = ok ? static_cast<int>(amg[o]) : -1;
+                    }
                 }
             }
 #pragma unroll
             for (int dr = 0; dr < NWR; ++dr) {
                 const int dlt = DLO + dr;
+                if constexpr (LATE) {
+                    const int pr = pr0 + DLO + dr;
+                    if (pr < 0 || pr >= PH) continue;  // warp-uniform
+#pragma unroll
+                    for (int pc = 0; pc < PW; ++pc) {
+                        dv[0][pc] = dpg[m * P + pr * PW + pc];
+                        av[0][pc] = static_cast<int>(amg[m * P + pr * PW + pc]);
+                    }
+                }
 #pragma unroll
                 for (int pc = 0; pc < PW; ++pc) {
-                    const int arg = av[dr][pc];
-                    const float d = dv[dr][pc];
+                    const int arg = av[LATE ? 0 : dr][pc];
+                    const float d = dv[LATE ? 0 : dr][pc];
+                    auto add_phase = [&](auto phc) {
+                        constexpr int ph = decltype(phc)::value;
 #pragma unroll
-                    for (int ph = 0; ph < KP * KP; ++ph) {
-                        if (arg == ph) {  // warp-uniform branch on the argmax phase
+                        for (int i = 0; i < K; ++i) {
+                            const int rr = dlt * KP + ph / KP + i;
+                            if (rr < 0 || rr >= RB) continue;  // compile-time after unrolling
 #pragma unroll
-                            for (int i = 0; i < K; ++i) {
-                                const int rr = dlt * KP + ph / KP + i;
-                                if (rr < 0 || rr >= RB) continue;  // compile-time after unrolling
+                            for (int j = 0; j < K; ++j) {
+                                const int cc = pc * KP + ph % KP + j;
+                                acc[rr][cc] = fmaf(w[i * K + j], d, acc[rr][cc]);
+                            }
+                        }
+                    };
+#ifndef CHAOS_DIN_SW
+#define CHAOS_DIN_SW 0
+#endif
+                    if constexpr (CHAOS_DIN_SW && KP == 3) {
+                        switch (arg) {  // warp-uniform: one indirect branch instead of a 9-way chain
+                            case 0: add_phase(std::integral_constant<int, 0>{}); break;
+                            case 1: add_phase(std::integral_constant<int, 1>{}); break;
+                            case 2: add_phase(std::integral_constant<int, 2>{}); break;
+                            case 3: add_phase(std::integral_constant<int, 3>{}); break;
+                            case 4: add_phase(std::integral_constant<int, 4>{}); break;
+                            case 5: add_phase(std::integral_constant<int, 5>{}); break;
+                            case 6: add_phase(std::integral_constant<int, 6>{}); break;
+                            case 7: add_phase(std::integral_constant<int, 7>{}); break;
+                            case 8: add_phase(std::integral_constant<int, 8>{}); break;
+                            default: break;
+                        }
+                    } else {
 #pragma unroll
-                                for (int j = 0; j < K; ++j) {
-                                    const int cc = pc * KP + ph % KP + j;
-                                    acc[rr][cc] = fmaf(w[i * K + j], d, acc[rr][cc]);
+                        for (int ph = 0; ph < KP * KP; ++ph) {
+                            if (arg == ph) {  // warp-uniform branch on the argmax phase
+#pragma unroll
+                                for (int i = 0; i < K; ++i) {
+                                    const int rr = dlt * KP + ph / KP + i;
+                                    if (rr < 0 || rr >= RB) continue;  // compile-time after unrolling
+#pragma unroll
+                                    for (int j = 0; j < K; ++j) {
+                                        const int cc = pc * KP + ph % KP + j;
+                                        acc[rr][cc] = fmaf(w[i * K + j], d, acc[rr][cc]);
+                                    }
                                 }
                             }
                         }
@@ -1439,6 +1515,122 @@ __device__ __forceinline__ void conv_din(const float* __restrict__ wsm, const fl
                 }
             }
         }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// PHASE(conv_din_rows) partial derivatives of the previous layer, window row by window row (any KP):
+//   dout[g][n][y][x] = (1 - in^2) * sum_m sum_w W[n][y-oy][x-ox][m] dp[g][m][w],  (oy, ox) = the
+//   argmax position of (g, m, w).
+// One group of MSPLIT warps per (image, 32 input maps), lanes over n; warp k of the group takes
+// output maps [k*M/MSPLIT, (k+1)*M/MSPLIT).  The accumulator holds the KP + K - 1 input rows one
+// window row reaches; each (map, window) is dispatched ONCE (warp-uniform branch on its phase) into
+// compile-time registers, so every argmax-sparse MAC is done with no band revisits (conv_din
+// dispatches a window once per band it reaches: 2.7x on the medium net, with ~8 MACs each).  After
+// window row pr the first KP rows are final: the group's partial rows meet in pbuf, warp 0 adds
+// them in a fixed order (deterministic) and writes them; the block then shifts up by KP rows.
+// pbuf: [NT/32/MSPLIT][MSPLIT-1][KP][WR][min(C,32)] floats.  dout may alias in.
+// ------------------------------------------------------------------------------------
+template <class L, int NT, int MSPLIT>
+__device__ __forceinline__ void conv_din_rows(const float* __restrict__ wsm, const float* __restrict__ dp,
+                                              const uint8_t* __restrict__ am, const float* in, float* dout, int cnt,
+                                              float* __restrict__ pbuf) {
+    constexpr int K = L::K, KP = L::KP, KK = L::KK, PW = L::PW, PH = L::PH, P = L::P, M = L::M, C = L::C;
+    constexpr int H = L::H, W = L::W, HW = H * W, R1 = KP + K - 1, WR = L::WR;
+    constexpr int NCW = (C + 31) / 32, NW = NT / 32, NG = NW / MSPLIT;
+    constexpr int CL = C < 32 ? C : 32;
+    constexpr int SL = KP * WR * CL;  // one partial block of KP rows
+    static_assert(NW % MSPLIT == 0 && NG <= 15, "warp groups, named barriers 1..15");
+    static_assert(WR <= W && L::HR <= H, "the windows' reach stays inside the input");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int half = warp % MSPLIT, grp = warp / MSPLIT;
+    const int m_lo = half * M / MSPLIT, m_hi = (half + 1) * M / MSPLIT;
+    for (int vw = grp; vw < cnt * NCW; vw += NG) {
+        const int cw = vw % NCW, g = vw / NCW;
+        const int n0 = cw * 32 + lane;
+        const bool act = n0 < C;
+        const int n = act ? n0 : 0;
+        const float* wn = wsm + n * KK * L::MP;
+        const int dgo = g * L::OUT_SZ;  // (offsets, not pointers: fewer live registers)
+        float acc[R1][WR];
+#pragma unroll
+        for (int r = 0; r < R1; ++r)
+#pragma unroll
+            for (int c = 0; c < WR; ++c) acc[r][c] = 0.f;
+        // rows [y0, y0 + nr) of the input are final in acc[0 .. nr): combine the group's partials, write
+        auto emit = [&](int y0, int nr) {
+            const float* ib = in + g * L::IN_SZ + n * HW;
+            float* ob = dout + g * L::IN_SZ + n * HW;
+            float* pb = pbuf + grp * (MSPLIT - 1) * SL + (lane < CL ? lane : 0);
+            if (MSPLIT > 1 && half > 0 && lane < CL) {
+#pragma unroll
+                for (int r = 0; r < KP; ++r)
+                    if (r < nr)
+#pragma unroll
+                        for (int c = 0; c < WR; ++c) pb[(half - 1) * SL + (r * WR + c) * CL] = acc[r][c];
+            }
+            if constexpr (MSPLIT > 1) asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(32 * MSPLIT) : "memory");
+            if (half == 0 && act) {
+#pragma unroll
+                for (int r = 0; r < KP; ++r) {
+                    if (r < nr) {
+#pragma unroll
+                        for (int c = 0; c < W; ++c) {
+                            float v = c < WR ? acc[r][c < WR ? c : 0] : 0.f;
+#pragma unroll
+                            for (int k = 0; k < MSPLIT - 1; ++k)
+                                if (c < WR) v += pb[k * SL + (r * WR + (c < WR ? c : 0)) * CL];
+                            const float x = ib[(y0 + r) * W + c];
+                            ob[(y0 + r) * W + c] = v * (1.f - x * x);
+                        }
+                    }
+                }
+            }
+            if constexpr (MSPLIT > 1) asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(32 * MSPLIT) : "memory");
+        };
+#pragma unroll 1
+        for (int pr = 0; pr < PH; ++pr) {
+#pragma unroll 1
+            for (int m = m_lo; m < m_hi; ++m) {
+                float w[KK];
+#pragma unroll
+                for (int tp = 0; tp < KK; ++tp) w[tp] = wn[tp * L::MP + m];
+#pragma unroll
+                for (int pc = 0; pc < PW; ++pc) {
+                    const float d = dp[dgo + m * P + pr * PW + pc];
+                    const int arg = static_cast<int>(am[dgo + m * P + pr * PW + pc]);
+#pragma unroll
+                    for (int ph = 0; ph < KP * KP; ++ph) {
+                        if (arg == ph) {  // warp-uniform
+#pragma unroll
+                            for (int i = 0; i < K; ++i)
+#pragma unroll
+                                for (int j = 0; j < K; ++j)
+                                    acc[ph / KP + i][pc * KP + ph % KP + j] =
+                                        fmaf(w[i * K + j], d, acc[ph / KP + i][pc * KP + ph % KP + j]);
+                        }
+                    }
+                }
+            }
+            emit(pr * KP, KP);
+#pragma unroll
+            for (int r = 0; r < R1; ++r)
+#pragma unroll
+                for (int c = 0; c < WR; ++c) acc[r][c] = (r + KP < R1) ? acc[r + KP < R1 ? r + KP : 0][c] : 0.f;
+        }
+        // the last K - 1 reached rows, in pieces of at most KP, then the floor-dropped rows (zero)
+#pragma unroll
+        for (int r0 = 0; r0 < R1 - KP; r0 += KP) {
+            emit(PH * KP + r0, (R1 - KP - r0) < KP ? (R1 - KP - r0) : KP);
+#pragma unroll
+            for (int r = 0; r < R1; ++r)
+#pragma unroll
+                for (int c = 0; c < WR; ++c) acc[r][c] = (r + KP < R1) ? acc[r + KP < R1 ? r + KP : 0][c] : 0.f;
+        }
+        if (half == 0 && act)
+            for (int y = L::HR; y < H; ++y)
+#pragma unroll
+                for (int c = 0; c < W; ++c) dout[g * L::IN_SZ + n * HW + y * W + c] = 0.f;
     }
 }
 
@@ -3500,7 +3692,9 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a0) {
                 conv_gw<C2, NT, MODE, false>(a, slot, a1, a2, am2, nullptr, O::c2w, cnt, sc);
                 __syncthreads();
                 PTIME(12);
-                if constexpr (DinPair<Net>::value > 1)
+                if constexpr (DinRows<Net>::value && DinPair<Net>::value > 1)
+                    conv_din_rows<C2, NT, DinPair<Net>::value>(wb + W2OFF, a2, am2, a1, a1, cnt, wb + S::WBUF);
+                else if constexpr (DinPair<Net>::value > 1)
                     conv_din<C2, NT, DinPair<Net>::value>(wb + W2OFF, a2, am2, a1, a1, cnt, wb + S::WBUF);
                 else
                     conv_din<C2, NT>(wb + W2OFF, a2, am2, a1, a1, cnt);

@@ -56,7 +56,10 @@ struct MediumNet {  // configs[2] = Table I medium
 #ifndef MEDIUM_DINSPLIT
 #define MEDIUM_DINSPLIT 4
 #endif
-    static constexpr int DINSPLIT = MEDIUM_DINSPLIT;  // conv2 delta_in: warps per (image, band) task
+    static constexpr int DINSPLIT = MEDIUM_DINSPLIT;  // conv2 delta_in: warps per (image, 32 maps) task
+    // conv2 delta_in window row by window row, each (map, window) dispatched once (conv_din_rows):
+    // 4.38 M vs 3.84 M samples/s (banded conv_din); the Table I small net (G = 1: one task) keeps conv_din
+    static constexpr bool DINROWS = true;
     using C1 = Conv<1, 29, 29, 20, 4, 2, 10, 16, 16, 2>;
 #ifndef MEDIUM_C2_MT
 #define MEDIUM_C2_MT 4
@@ -64,7 +67,10 @@ struct MediumNet {  // configs[2] = Table I medium
 #ifndef MEDIUM_C2_NSPL
 #define MEDIUM_C2_NSPL 1
 #endif
-    using C2 = Conv<20, 13, 13, 40, 5, 3, MEDIUM_C2_MT, 25, 1, 3, 0, 0, false, false, 0, false, MEDIUM_C2_NSPL>;
+#ifndef MEDIUM_C2_RB  // conv2 delta_in: input rows per band task
+#define MEDIUM_C2_RB 3
+#endif
+    using C2 = Conv<20, 13, 13, 40, 5, 3, MEDIUM_C2_MT, 25, 1, MEDIUM_C2_RB, 0, 0, false, false, 0, false, MEDIUM_C2_NSPL>;
     using C3 = C2;
     using F1 = Full<360, 150, true>;
     using F2 = Full<150, 10, false>;
