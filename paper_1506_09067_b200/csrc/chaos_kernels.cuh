@@ -109,16 +109,22 @@ __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 // Convolution block: conv (valid, stride 1, C->M maps, KxK) -> tanh -> KPxKP max-pool (floor).
 // Tuning knobs: MT maps per thread in the forward; TT taps per thread and GS split of the
 // (image, window) sum in the weight gradient; RB input rows per band in delta_in.
+// MPO > 0: the internal row pitch of W (default round4(M), 16-B rows).  An odd pitch puts the rows of
+// consecutive input maps in distinct banks (lanes over input maps reading one map's weights:
+// conflict-free, where a pitch of 40 hits 4 banks -- the medium net's conv2 delta_in); its forward
+// then reads weights with scalar (broadcast) loads.
 template <int C_, int H_, int W_, int M_, int K_, int KP_, int MT_, int TT_, int GS_, int RB_, int PB_ = 0,
-          int MS_ = 0, bool UNUSED_ = false, bool DIN3_ = false, int GWIN_ = 0, bool DWIN_ = false, int NSPL_ = 1>
+          int MS_ = 0, bool UNUSED_ = false, bool DIN3_ = false, int GWIN_ = 0, bool DWIN_ = false, int NSPL_ = 1,
+          int MPO_ = 0>
 struct Conv {
     static constexpr int C = C_, H = H_, W = W_, M = M_, K = K_, KP = KP_;
     static constexpr int OH = H - K + 1, OW = W - K + 1;
     static constexpr int PH = OH / KP, PW = OW / KP, P = PH * PW;
-    static constexpr int MP = round4(M);  // internal row pitch (maps padded to 16 B)
+    static constexpr int MP = MPO_ > 0 ? MPO_ : round4(M);  // internal row pitch
+    static_assert(MP >= M, "row pitch below the map count");
     static constexpr int KK = K * K;
-    static constexpr int ROWS = C * KK;   // internal W is [C*K*K][MP], bias [MP]
-    static constexpr int WFL = ROWS * MP, BFL = MP, BLK = WFL + BFL;
+    static constexpr int ROWS = C * KK;   // internal W is [C*K*K][MP], bias [round4(MP)]
+    static constexpr int WFL = round4(ROWS * MP), BFL = round4(MP), BLK = WFL + BFL;
     static constexpr int IN_SZ = C * H * W, OUT_SZ = M * P;
     static constexpr int MT = MT_, TT = TT_, GS = GS_, RB = RB_;
     static constexpr int NB = (H + RB - 1) / RB;
@@ -575,8 +581,8 @@ __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const flo
                                          float* __restrict__ out, uint8_t* __restrict__ am, int cnt) {
     constexpr int MT = L::MT, KP = L::KP, K = L::K, PW = L::PW, P = L::P, MG = L::M / MT;
     constexpr int PS = KP + K - 1;
-    constexpr bool A4 = (MT % 4 == 0) || (MG == 1);
-    constexpr bool A2 = (MT % 2 == 0);  // row pitch MP is a multiple of 4, so mg*MT is even
+    constexpr bool A4 = ((MT % 4 == 0) || (MG == 1)) && (L::MP % 4 == 0);
+    constexpr bool A2 = (MT % 2 == 0) && (L::MP % 2 == 0);  // 16-B rows: mg*MT is even
     constexpr int NSPL = L::NSPL, CH = L::C / NSPL;
     static_assert(NT % 32 == 0, "lane pairs never straddle warps");
     static_assert(PL == 0 || (!MGF && NSPL == 1 && 32 % (2 * (PL > 0 ? PL : 1)) == 0), "image-pair lane map");

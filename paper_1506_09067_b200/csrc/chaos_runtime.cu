@@ -70,7 +70,11 @@ struct MediumNet {  // configs[2] = Table I medium
 #ifndef MEDIUM_C2_RB  // conv2 delta_in: input rows per band task
 #define MEDIUM_C2_RB 3
 #endif
-    using C2 = Conv<20, 13, 13, 40, 5, 3, MEDIUM_C2_MT, 25, 1, MEDIUM_C2_RB, 0, 0, false, false, 0, false, MEDIUM_C2_NSPL>;
+#ifndef MEDIUM_C2_MP  // conv2 W row pitch: 41 (odd) -> conflict-free delta_in weight loads
+#define MEDIUM_C2_MP 41
+#endif
+    using C2 = Conv<20, 13, 13, 40, 5, 3, MEDIUM_C2_MT, 25, 1, MEDIUM_C2_RB, 0, 0, false, false, 0, false, MEDIUM_C2_NSPL,
+                    MEDIUM_C2_MP>;
     using C3 = C2;
     using F1 = Full<360, 150, true>;
     using F2 = Full<150, 10, false>;
