@@ -3345,7 +3345,10 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a0) {
             else if constexpr (FCSTAGE)
                 fc_fwd3<F1, G, NT, FRCH>(P + O::f1w, P + O::f1b, alast, hh, F1::OUT, cnt, wb, L4, L5, sS);
             else if constexpr (F1::IN % 4 == 0)
-                fc_fwd2<F1, G, NT, (NT > 512 || BIG ? 2 : 4)>(P + O::f1w, P + O::f1b, alast, hh, F1::OUT, cnt);
+#ifndef CHAOS_FC2_NR  // fc_fwd2 rows per warp task for NT <= 512 (medium: 150 rows)
+#define CHAOS_FC2_NR 5
+#endif
+                fc_fwd2<F1, G, NT, (NT > 512 || BIG ? 2 : CHAOS_FC2_NR)>(P + O::f1w, P + O::f1b, alast, hh, F1::OUT, cnt);
             else
                 fc_fwd<F1, G, NT>(P + O::f1w, P + O::f1b, alast, hh, F1::OUT, cnt);
             __syncthreads();

@@ -70,8 +70,8 @@ struct MediumNet {  // configs[2] = Table I medium
 #ifndef MEDIUM_C2_RB  // conv2 delta_in: input rows per band task
 #define MEDIUM_C2_RB 3
 #endif
-#ifndef MEDIUM_C2_MP  // conv2 W row pitch: 41 (odd) -> conflict-free delta_in weight loads
-#define MEDIUM_C2_MP 41
+#ifndef MEDIUM_C2_MP  // conv2 W row pitch: 42 (8-B rows, lanes over input maps 2-way; 41: conflict-free but scalar forward loads, -1.6%)
+#define MEDIUM_C2_MP 42
 #endif
     using C2 = Conv<20, 13, 13, 40, 5, 3, MEDIUM_C2_MT, 25, 1, MEDIUM_C2_RB, 0, 0, false, false, 0, false, MEDIUM_C2_NSPL,
                     MEDIUM_C2_MP>;
