@@ -37,7 +37,7 @@ namespace chaos {
 constexpr int kClasses = 10;
 constexpr int kZStride = 16;  // logits / output-delta row stride in shared memory
 constexpr int kHdrBytes = 512;  // mbarriers, claim word, labels, losses; [256, 512): tensor-core mbarriers
-constexpr int kBiasScratch = 256;  // floats: FC bias-gradient scratch
+constexpr int kBiasScratch = 160;  // floats: FC bias-gradient scratch (>= every FC layer's BFL, asserted)
 
 // kTrace: hogwild (kHogwild semantics) that also records, per claimed group and weighted layer,
 // when its weight reads and its publishes happened on two global event counters, and stores each
@@ -115,7 +115,7 @@ __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 // then reads weights with scalar (broadcast) loads.
 template <int C_, int H_, int W_, int M_, int K_, int KP_, int MT_, int TT_, int GS_, int RB_, int PB_ = 0,
           int MS_ = 0, bool UNUSED_ = false, bool DIN3_ = false, int GWIN_ = 0, bool DWIN_ = false, int NSPL_ = 1,
-          int MPO_ = 0>
+          int MPO_ = 0, int NPAD_ = 0>
 struct Conv {
     static constexpr int C = C_, H = H_, W = W_, M = M_, K = K_, KP = KP_;
     static constexpr int OH = H - K + 1, OW = W - K + 1;
@@ -123,8 +123,13 @@ struct Conv {
     static constexpr int MP = MPO_ > 0 ? MPO_ : round4(M);  // internal row pitch
     static_assert(MP >= M, "row pitch below the map count");
     static constexpr int KK = K * K;
-    static constexpr int ROWS = C * KK;   // internal W is [C*K*K][MP], bias [round4(MP)]
-    static constexpr int WFL = round4(ROWS * MP), BFL = round4(MP), BLK = WFL + BFL;
+    static constexpr int ROWS = C * KK;   // internal W is [C][K*K][MP] (input map n at n * NS), bias [round4(MP)]
+    // NPAD: floats of padding after each input map's K*K rows.  NS / 4 odd puts the 16-B weight vectors
+    // of consecutive input maps in distinct bank groups (lanes over input maps, LDS.128: the large
+    // net's conv3 delta_in, where NS = 400 hit 2 of 8 groups)
+    static constexpr int NPAD = NPAD_, NS = KK * MP + NPAD;
+    static_assert(NPAD % 4 == 0, "16-B aligned input-map blocks");
+    static constexpr int WFL = round4(C * NS), BFL = round4(MP), BLK = WFL + BFL;
     static constexpr int IN_SZ = C * H * W, OUT_SZ = M * P;
     static constexpr int MT = MT_, TT = TT_, GS = GS_, RB = RB_;
     static constexpr int NB = (H + RB - 1) / RB;
@@ -630,7 +635,7 @@ __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const flo
 #pragma unroll
                 for (int j = 0; j < K; ++j) {
                     float wv[MT];
-                    load_vec<MT, A4, A2>(wv, wb + ((n * K + i) * K + j) * L::MP);
+                    load_vec<MT, A4, A2>(wv, wb + n * L::NS + (i * K + j) * L::MP);
 #pragma unroll
                     for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -785,6 +790,7 @@ __device__ __forceinline__ void conv_fwd_tc2(const float* __restrict__ in, const
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const int k = sl * 8 + c * 4 + q;
+                        static_assert(L::NPAD == 0, "tensor-core B operand from [C*K*K][MP] rows");
                         const float v = (mB < M && k < KD) ? wsm[k * L::MP + mB] : 0.f;
                         hi[q] = tf32_rna(v);
                         lo[q] = tf32_rna(v - __uint_as_float(hi[q]));
@@ -899,6 +905,7 @@ __device__ __forceinline__ void conv_fwd_slab(const float* __restrict__ in, cons
                                               float* __restrict__ out, uint8_t* __restrict__ am, float* ring,
                                               Loader& R0, Loader& R1, Loader& R2) {
     constexpr int MT = L::MT, KP = L::KP, K = L::K, KK = L::KK, PW = L::PW, P = L::P, MG = L::M / MT;
+    static_assert(L::NPAD == 0, "conv_fwd_slab streams [K*K][MP] slabs");
     constexpr int PS = KP + K - 1, SLAB = KK * L::MP, ITEMS = MG * P;
     static_assert(ITEMS <= NT, "one item per thread");
     static_assert((SLAB * 4) % 16 == 0 && MT % 4 == 0, "16-B slabs, vector weight loads");
@@ -991,6 +998,7 @@ __device__ __forceinline__ void conv_gw(const KArgs& a, int slot, const float* _
     constexpr int TT = L::TT, TG = KK / TT, GS = L::GS;
     constexpr int HW = L::H * L::W;
     static_assert(GS == 1 || SCRATCH, "split sums need the scratch");
+    static_assert(!SCRATCH || L::NPAD == 0, "the scratch block is assembled without input-map padding");
     float* fin = scr + (GS > 1 ? GS * L::WFL : 0);  // final [WFL][BFL] block
     const int span = cnt * P;
     const int total = C * M * TG * GS;
@@ -1039,7 +1047,7 @@ __device__ __forceinline__ void conv_gw(const KArgs& a, int slot, const float* _
         }
 #pragma unroll
         for (int t = 0; t < TT; ++t) {
-            const int widx = (n * KK + tg * TT + t) * L::MP + m;
+            const int widx = n * L::NS + (tg * TT + t) * L::MP + m;
             if constexpr (!SCRATCH)
                 publish_elem<MODE>(a, slot, woff + widx, sc * acc[t]);
             else if constexpr (GS == 1)
@@ -1064,7 +1072,7 @@ __device__ __forceinline__ void conv_gw(const KArgs& a, int slot, const float* _
             for (int e = threadIdx.x; e < L::ROWS * M; e += NT) {
                 const int m = e % M;
                 const int row = e / M;
-                const int widx = row * L::MP + m;
+                const int widx = (row / KK) * L::NS + (row % KK) * L::MP + m;
                 float s = 0.f;
 #pragma unroll
                 for (int k = 0; k < GS; ++k) s += scr[k * L::WFL + widx];
@@ -1146,7 +1154,7 @@ __device__ __forceinline__ void conv_gw_m(const KArgs& a, int slot, const float*
 #pragma unroll
         for (int k = 0; k < NPT; ++k)
 #pragma unroll
-            for (int t = 0; t < KK; ++t) publish_elem<MODE>(a, slot, woff + ((n0 + k) * KK + t) * L::MP + m, sc * acc[k][t]);
+            for (int t = 0; t < KK; ++t) publish_elem<MODE>(a, slot, woff + (n0 + k) * L::NS + t * L::MP + m, sc * acc[k][t]);
         if (n0 == 0) publish_elem<MODE>(a, slot, woff + L::WFL + m, sc * accb);
     }
 }
@@ -1238,7 +1246,7 @@ __device__ __forceinline__ void conv_gw_win(const KArgs& a, int slot, const floa
 #pragma unroll
             for (int q4 = 0; q4 < NM; q4 += 4)
                 if ((NG * NM == M) || m0 + q4 < M)
-                    publish_vec4<MODE>(a, slot, woff + (n * KK + t) * L::MP + m0 + q4,
+                    publish_vec4<MODE>(a, slot, woff + n * L::NS + t * L::MP + m0 + q4,
                                        make_float4(sc * acc[q4][t], sc * acc[q4 + 1][t], sc * acc[q4 + 2][t],
                                                    sc * acc[q4 + 3][t]));
         if (n == 0)
@@ -1316,7 +1324,7 @@ __device__ __forceinline__ void conv_gw_wt(const KArgs& a, int slot, const float
         for (int t = 0; t < KR * K; ++t)
 #pragma unroll
             for (int q4 = 0; q4 < NM; q4 += 4)
-                publish_vec4<MODE>(a, slot, woff + (n * KK + tr * KR * K + t) * L::MP + m0 + q4,
+                publish_vec4<MODE>(a, slot, woff + n * L::NS + (tr * KR * K + t) * L::MP + m0 + q4,
                                    make_float4(sc * acc[q4][t], sc * acc[q4 + 1][t], sc * acc[q4 + 2][t],
                                                sc * acc[q4 + 3][t]));
         if (n == 0 && tr == 0)
@@ -1374,7 +1382,7 @@ __device__ __forceinline__ void conv_din(const float* __restrict__ wsm, const fl
         for (int r = 0; r < RB; ++r)
 #pragma unroll
             for (int c = 0; c < L::W; ++c) acc[r][c] = 0.f;
-        const float* wn = wsm + n * KK * L::MP;
+        const float* wn = wsm + n * L::NS;
         const float* dpg = dp + g * L::OUT_SZ;
         const uint8_t* amg = am + g * L::OUT_SZ;
         const int pr0 = b * R2;
@@ -1556,7 +1564,7 @@ __device__ __forceinline__ void conv_din_rows(const float* __restrict__ wsm, con
         const int n0 = cw * 32 + lane;
         const bool act = n0 < C;
         const int n = act ? n0 : 0;
-        const float* wn = wsm + n * KK * L::MP;
+        const float* wn = wsm + n * L::NS;
         const int dgo = g * L::OUT_SZ;  // (offsets, not pointers: fewer live registers)
         float acc[R1][WR];
 #pragma unroll
@@ -1675,7 +1683,7 @@ __device__ __forceinline__ void conv_din_gm(const float* __restrict__ wg, const 
         for (int r = 0; r < RB; ++r)
 #pragma unroll
             for (int c = 0; c < W; ++c) acc[r][c] = 0.f;
-        const float* wn = wg + static_cast<long long>(n) * KK * L::MP;
+        const float* wn = wg + static_cast<long long>(n) * L::NS;
         const float* dpg = dp + g * L::OUT_SZ;
         const uint8_t* amg = am + g * L::OUT_SZ;
         const int pr0 = b * R2;
@@ -1823,7 +1831,7 @@ __device__ __forceinline__ void conv_din3(const float* __restrict__ wsm, const f
     if (has) {
         const float* dpg = dp + g * L::OUT_SZ;
         const uint8_t* amg = am + g * L::OUT_SZ;
-        const float* wn = wsm + (act ? n : 0) * (WTP > 0 ? KK : KK * L::MP);
+        const float* wn = wsm + (act ? n : 0) * (WTP > 0 ? KK : L::NS);
         constexpr bool W4 = KK <= 4 && WTP == 0;
 #pragma unroll 1
         for (int wr = 0; wr < PB; ++wr) {
@@ -2015,7 +2023,7 @@ __device__ __forceinline__ void conv_din_win(const float* __restrict__ wsm, cons
     const int cw = warp % NCW, g = has ? warp / NCW : 0;
     const int n = cw * 32 + lane;
     const bool act = has && n < C;
-    const float* wn = wsm + (act ? n : 0) * KK * L::MP;
+    const float* wn = wsm + (act ? n : 0) * L::NS;
     const float* dpg = dp + g * L::OUT_SZ;
     const uint8_t* amg = am + g * L::OUT_SZ;
     float acc[HR][WR];
@@ -2097,7 +2105,7 @@ __device__ __forceinline__ void conv_din_winp(const float* __restrict__ wsm, con
     const int cw = warp % NCW, g = has ? warp / NCW : 0;
     const int n = cw * 32 + lane;
     const bool act = has && n < C;
-    const float* wn = wsm + (act ? n : 0) * KK * L::MP;
+    const float* wn = wsm + (act ? n : 0) * L::NS;
     const float4* dqg = dq4 + g * L::OUT_SZ;
     float acc[HR][WR];
 #pragma unroll
@@ -2196,7 +2204,7 @@ __device__ __forceinline__ void conv_bwd_sparse(const KArgs& a, int slot, const 
         const int mlo = (MS == 2 && sp == 1) ? M4H : 0, mhi = (MS == 2 && sp == 0) ? M4H : M;
         const int n = cw * 32 + lane;
         const bool act = n < C;
-        const float* wn = wsm + (act ? n : 0) * KK * L::MP;
+        const float* wn = wsm + (act ? n : 0) * L::NS;
         const float* dpg = dp + g * L::OUT_SZ;
         const uint8_t* amg = am + g * L::OUT_SZ;
         float acc[HR][WR];
@@ -2373,7 +2381,7 @@ __device__ __forceinline__ void conv_bwd_sparse(const KArgs& a, int slot, const 
         if (act) {
 #pragma unroll
             for (int t = 0; t < KK; ++t)
-                publish_vec4<MODE>(a, slot, woff + (n * KK + t) * L::MP + m0,
+                publish_vec4<MODE>(a, slot, woff + n * L::NS + t * L::MP + m0,
                                    make_float4(sc * acc[0][t], sc * acc[1][t], sc * acc[2][t], sc * acc[3][t]));
             if (n == 0)
                 publish_vec4<MODE>(a, slot, woff + L::WFL + m0,
@@ -3078,7 +3086,8 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a0) {
     // and kept (W2 serves the conv2 forward and delta_in); conv3 and FC1 read from L2
     constexpr bool BIG = S::BIG;
     constexpr int W2OFF = (NCONV >= 2) ? (BIG ? round4(C1::BLK) : S::WBUF - C2::BLK) : 0;
-    constexpr int W3A = (NCONV >= 3 && !BIG) ? (C3::C / 2) * C3::KK * C3::MP : 0;
+    constexpr int W3A = (NCONV >= 3 && !BIG) ? (C3::C / 2) * C3::NS : 0;
+    static_assert(F1::BFL <= kBiasScratch && F2::BFL <= kBiasScratch, "FC bias-gradient scratch");
     static_assert(NCONV < 3 || BIG || W3A <= W2OFF, "W3 first half must not overlap W2");
     static_assert(!BIG || NCONV == 3, "BIGW nets have three conv layers");
     // FC1 weights staged through WB in two chunks of FRCH rows (large net: WB is free between
@@ -3625,6 +3634,7 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a0) {
                     static_assert(C2_WTP == 0 || round4(C2::BLK) + C2::M * C2_WTP <= S::WBUF,
                                   "transposed W2 must fit in WB");
                     float* wbt = wb + round4(C2::BLK);
+                    static_assert(C2::NPAD == 0, "W2 transpose from [C*K*K][MP] rows");
                     for (int e = static_cast<int>(threadIdx.x) - t0; e < C2::ROWS * C2::M; e += nthr)
                         wbt[(e % C2::M) * C2_WTP + e / C2::M] = wb[(e / C2::M) * C2::MP + e % C2::M];
                 };

@@ -123,7 +123,10 @@ struct LargeNet {  // configs[3], configs[4]
 #define LARGE_C3_MT 4
 #endif
     using C2 = Conv<20, 13, 13, 60, 3, 2, LARGE_C2_MT, 9, 1, 4, LARGE_C2_PB, -1, false, true, 0, false, 1>;
-    using C3 = Conv<60, 5, 5, 100, 2, 2, LARGE_C3_MT, 4, 1, 5, 2, 0, false, false, 4, true, 1>;
+#ifndef LARGE_C3_NPAD  // conv3 W: floats of padding per input map (NS = 404: NS / 4 odd)
+#define LARGE_C3_NPAD 4
+#endif
+    using C3 = Conv<60, 5, 5, 100, 2, 2, LARGE_C3_MT, 4, 1, 5, 2, 0, false, false, 4, true, 1, 0, LARGE_C3_NPAD>;
     using F1 = Full<400, 150, true>;
     using F2 = Full<150, 10, false>;
 };
@@ -161,7 +164,7 @@ struct Repl<N, std::void_t<decltype(N::REPL)>> {
 
 struct Block {  // one weighted layer, host view
     bool conv;
-    int C, K, M, MP;  // conv
+    int C, K, M, MP, NS;  // conv (NS: floats per input map, K*K*MP + padding)
     int IN, OUT;      // full
     long long int_w, int_b;    // internal offsets (floats)
     long long norm_w, norm_b;  // normative offsets
@@ -197,6 +200,7 @@ void add_conv(NetDesc& d, long long w, long long b, long long& norm) {
     k.K = L::K;
     k.M = L::M;
     k.MP = L::MP;
+    k.NS = L::NS;
     k.int_w = w;
     k.int_b = b;
     k.nw = (long long)L::M * L::C * L::K * L::K;
@@ -478,7 +482,7 @@ void to_internal(const NetDesc& d, const float* norm, std::vector<float>& out) {
             for (int m = 0; m < b.M; ++m)
                 for (int n = 0; n < b.C; ++n)
                     for (int t = 0; t < b.K * b.K; ++t)
-                        out[b.int_w + ((long long)n * b.K * b.K + t) * b.MP + m] =
+                        out[b.int_w + (long long)n * b.NS + (long long)t * b.MP + m] =
                             norm[b.norm_w + ((long long)m * b.C + n) * b.K * b.K + t];
         } else {
             std::memcpy(&out[b.int_w], norm + b.norm_w, sizeof(float) * b.nw);
@@ -494,7 +498,7 @@ void to_normative(const NetDesc& d, const float* in, float* norm) {
                 for (int n = 0; n < b.C; ++n)
                     for (int t = 0; t < b.K * b.K; ++t)
                         norm[b.norm_w + ((long long)m * b.C + n) * b.K * b.K + t] =
-                            in[b.int_w + ((long long)n * b.K * b.K + t) * b.MP + m];
+                            in[b.int_w + (long long)n * b.NS + (long long)t * b.MP + m];
         } else {
             std::memcpy(norm + b.norm_w, &in[b.int_w], sizeof(float) * b.nw);
         }
