@@ -2204,7 +2204,7 @@ __device__ __forceinline__ void conv_bwd_sparse(const KArgs& a, int slot, const 
         const int mlo = (MS == 2 && sp == 1) ? M4H : 0, mhi = (MS == 2 && sp == 0) ? M4H : M;
         const int n = cw * 32 + lane;
         const bool act = n < C;
-        const float* wn = wsm + (act ? n : 0) * L::NS;
+        const float* wn = wsm + (act ? n : C - 1) * L::NS;
         const float* dpg = dp + g * L::OUT_SZ;
         const uint8_t* amg = am + g * L::OUT_SZ;
         float acc[HR][WR];
@@ -2270,7 +2270,7 @@ __device__ __forceinline__ void conv_bwd_sparse(const KArgs& a, int slot, const 
                 }
             }
         }
-        float* ob = out + g * L::IN_SZ + (act ? n : 0) * HW;
+        float* ob = out + g * L::IN_SZ + (act ? n : C - 1) * HW;
         if constexpr (MS == 2) {  // first half -> out (raw sums), pair barrier, second half adds
             const int pair = 1 + g * NCW + cw;
             if (sp == 0 && act) {
@@ -2320,7 +2320,7 @@ __device__ __forceinline__ void conv_bwd_sparse(const KArgs& a, int slot, const 
         }
 #pragma unroll 1
         for (int g = 0; g < cnt; ++g) {
-            const float* ing = in + g * L::IN_SZ + (act ? n : 0) * HW;
+            const float* ing = in + g * L::IN_SZ + (act ? n : C - 1) * HW;
             const float* dpg = dp + g * L::OUT_SZ + m0 * P;
             const uint8_t* amg = am + g * L::OUT_SZ + m0 * P;
             float dvs[4 * P];
