@@ -227,7 +227,7 @@ def main():
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
     distributed = world > 1 or args.force_dist
-    if distributed and args.mode == "hogwild" and args.avg == "async":
+    if distributed and args.mode == "hogwild" and args.avg in ("async", "fused"):  # fused: for its fallback
         # the averaging collectives run beside a persistent kernel that holds every other SM:
         # NCCL's blocks must all be co-resident on the reserved SMs (a channel block waiting for
         # a peer whose matching block cannot be scheduled would never finish), so cap them, and
@@ -268,8 +268,12 @@ def main():
     trainer = DistTrainer(net, rank, world, args.k, force_collective=args.force_dist,
                           comm=args.comm if args.mode == "hogwild" else "torch")
     grad_buf = torch.zeros_like(net.device_params()) if args.mode == "sync" else None
-    if use_fused:
-        trainer.setup_fused(args.pavg_comm)
+    if use_fused and not trainer.setup_fused(args.pavg_comm):
+        # a rank could not map a peer's exchange buffer (no peer access): every rank falls back to
+        # the in-flight NCCL averaging -- caps set before any collective runs on the communicator
+        use_fused, use_async = False, True
+        net.set_option(OPT_RESERVE_SMS, args.reserve_sms)
+        args.avg = "async (fused unavailable: " + getattr(trainer, "fused_error", "a peer rank") + ")"
 
     def step(Xs, Ys, lr_s):
         if args.mode == "sync":

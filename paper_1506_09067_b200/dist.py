@@ -276,7 +276,8 @@ class DistTrainer:
         of the launch run the rounds (8 slices each) while the training CTAs never stall; 0 = the
         training CTAs run them between image groups (148 slices).  Each rank allocates its exchange
         buffer (snapshot ring + flags) and the ranks trade its CUDA IPC handle (an all-gather of 64
-        bytes); every rank maps every other rank's buffer (NVLink peer access)."""
+        bytes); every rank maps every other rank's buffer (NVLink peer access).  Returns False -- on
+        every rank -- if any rank could not map a peer's buffer (then use epoch_async / epoch)."""
         import torch
         import torch.distributed as dist
         if comm_ctas is None:
@@ -286,17 +287,28 @@ class DistTrainer:
             self.net.set_option(OPT_PAVG_COMM_CTAS, comm_ctas)
         self.comm_ctas = comm_ctas
         self.net.pavg_setup(self.rank, self.world, self.k, 8 * comm_ctas if comm_ctas else 0)
+        ok = True
         if self.world > 1:
+            on_gpu = dist.get_backend(self.group) == "nccl"
             h = torch.tensor(list(self.net.pavg_ipc_handle()), dtype=torch.uint8)
-            if dist.get_backend(self.group) == "nccl":
+            if on_gpu:
                 h = h.cuda()
             hs = [torch.zeros_like(h) for _ in range(self.world)]
             dist.all_gather(hs, h, group=self.group)
-            for q, hq in enumerate(hs):
-                if q != self.rank:
-                    self.net.pavg_open_peer(q, bytes(hq.cpu().tolist()))
+            try:
+                for q, hq in enumerate(hs):
+                    if q != self.rank:
+                        self.net.pavg_open_peer(q, bytes(hq.cpu().tolist()))
+            except Exception as e:  # e.g. no peer access between the devices
+                ok = False
+                self.fused_error = f"{type(e).__name__}: {e}"
+            # every rank must agree: a kernel waiting for a peer that never averages would hang
+            t = torch.tensor([1 if ok else 0], dtype=torch.int64, device="cuda" if on_gpu else "cpu")
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+            ok = bool(t.item())
         self.n_fused_rounds = 0
-        self._fused = True
+        self._fused = ok
+        return ok
 
     def epoch_fused(self, images, labels, lr: float, lo: int = 0, hi: int | None = None, host=None,
                     chunks: int = 8):

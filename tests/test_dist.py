@@ -414,3 +414,42 @@ def test_gloo_world3_fused_averaging_host_logic():
         assert ncoll == 2 and nfused == 2 * rounds
         for g in gathered[1:]:
             np.testing.assert_array_equal(g, gathered[0])  # identical after the exact average
+
+
+class FakeFusedNetNoPeer(FakeFusedNet):
+    """Rank 1 cannot map its peers' buffers (no peer access)."""
+
+    def pavg_open_peer(self, peer, handle):
+        if self.rank == 1:
+            raise RuntimeError("peer access unsupported")
+        super().pavg_open_peer(peer, handle)
+
+
+def _fused_fallback_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        net = FakeFusedNetNoPeer(8, rank)
+        tr = DistTrainer(net, rank, world, 256)
+        q.put((rank, tr.setup_fused(), getattr(tr, "fused_error", None)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world3_fused_setup_agrees_on_failure():
+    # one rank failing to map a peer's exchange buffer makes setup_fused return False on EVERY rank
+    # (bench.py then falls back to the NCCL averaging everywhere: no rank waits for a missing peer)
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fused_fallback_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [ok for _, ok, _ in res] == [False, False, False]
+    assert res[1][2] is not None and "peer access" in res[1][2]
