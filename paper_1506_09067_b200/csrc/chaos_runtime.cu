@@ -8,6 +8,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -1002,7 +1003,14 @@ chaos_status host_epoch(chaos_net* net, const float* h_images, const int32_t* h_
         long long chunk = (n + 15) / 16;
         chunk = (chunk + 15) / 16 * 16;  // 16-image multiples keep the 16-B image alignment
         if (chunk < 2048) chunk = 2048;
-        const long long nch = (n + chunk - 1) / chunk;
+        // chunk edges: a ramp 512, 1024, ... up to `chunk`, so the copy exposed before the first
+        // claims is ~0.1 ms of PCIe time instead of a whole n/16 chunk (the rest overlaps training)
+        std::vector<long long> edge{0};
+        for (long long sz = 512; edge.back() < (long long)n;) {
+            edge.push_back(std::min<long long>(n, edge.back() + sz));
+            sz = std::min<long long>(chunk, sz * 2);
+        }
+        const long long nch = (long long)edge.size() - 1;
         if (!net->ready) CUDA_TRY(cudaMalloc(&net->ready, sizeof(unsigned long long)));
         if (!net->ready_copied) CUDA_TRY(cudaEventCreateWithFlags(&net->ready_copied, cudaEventDisableTiming));
         // the previous host epoch's copies (async entry) may still be queued to read ready_host:
@@ -1025,8 +1033,8 @@ chaos_status host_epoch(chaos_net* net, const float* h_images, const int32_t* h_
         CUDA_TRY(cudaMemsetAsync(net->loss_sum, 0, sizeof(double), net->stream));
         net->last_train_n = n;
         for (long long c = 0; c < nch; ++c) {
-            const long long off = c * chunk;
-            const long long len = (n - off) < chunk ? (n - off) : chunk;
+            const long long off = edge[(size_t)c];
+            const long long len = edge[(size_t)c + 1] - off;
             CUDA_TRY(cudaMemcpyAsync(net->st_x + off * 841, h_images + off * 841, sizeof(float) * 841 * len,
                                      cudaMemcpyHostToDevice, net->copy_stream));
             CUDA_TRY(cudaMemcpyAsync(net->st_y + off, h_labels + off, sizeof(int) * len, cudaMemcpyHostToDevice,
