@@ -1496,6 +1496,11 @@ chaos_status chaos_train_epoch_replicas(chaos_net* const* nets, int32_t R, const
                             net->px ? net->px_host.rank : -1, net->px ? net->px_host.R : 0);
             if (net->px_arm != n0->px_arm || net->px_round0 != n0->px_round0 || net->px_comm != n0->px_comm)
                 return fail(CHAOS_E_INVALID, "replica %d: armed rounds / comm CTAs differ from replica 0", r);
+            if (net->px_peers_set != (1 << R) - 1)  // (checked here so no replica's rounds are consumed)
+                return fail(CHAOS_E_INVALID, "replica %d: exchange buffers of %d replicas expected, peer mask 0x%x",
+                            r, R, net->px_peers_set);
+        } else if (n0->px_arm > 0) {
+            return fail(CHAOS_E_INVALID, "replica %d is not armed like replica 0", r);
         }
         ka[(size_t)r] = k;
     }
