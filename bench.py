@@ -261,6 +261,8 @@ def main():
     if use_async:
         net.set_option(OPT_RESERVE_SMS, args.reserve_sms)
     info = net.launch_info()
+    if args.mode == "sync" and args.sync_batch < info["group"] * N_SM:
+        info["group"] = 1  # G unset: batches smaller than G x #SMs run one image per CTA (chaos.h)
     X = torch.from_numpy(xs).cuda()
     Y = torch.from_numpy(ys).cuda()
     Xt = torch.from_numpy(xt).cuda()

@@ -81,6 +81,9 @@ typedef enum {
     CHAOS_OPT_STREAM = 0,        /* value = (int64_t)cudaStream_t */
     CHAOS_OPT_SYNC_BATCH = 1,    /* B >= 1, default 64 */
     CHAOS_OPT_GROUP = 2,         /* G, images per CTA per claim: compiled values 1 and the net's default.
+                                    Never set: hogwild runs at the net's default G, and a sync / gradient
+                                    batch of fewer than G x #SMs images at G = 1 (it then fills G times more
+                                    SMs; the fixed summation order is that of G = 1).
                                     A worker publishes each layer's G-image gradient sum once (G_pub = G,
                                     the paper's delayed updates); SURVEY's separate
                                     CHAOS_OPT_PUBLISH_GROUP is not exposed: publishing per image inside a

@@ -386,6 +386,7 @@ struct chaos_net {
     long long st_cap = 0;
     int sync_batch = 64;
     int group = 1;
+    bool group_set = false;              // CHAOS_OPT_GROUP given explicitly (else sync batches may use G = 1)
     int max_ctas = 0;
     int debug_claims = 0;
     int reserve_sms = 0;                   // hogwild: SMs left free of training CTAs
@@ -603,7 +604,10 @@ KArgs base_args(chaos_net* net) {
 // (out == nullptr) params -= lr * fixed-order sum, or out = sum.
 chaos_status sync_batch(chaos_net* net, const float* X, const int32_t* Y, long long nb, float lr, float* out,
                         double* loss_sum) {
-    const int G = net->group;
+    // G never set: a batch with fewer than G * SMs images runs one image per CTA (G = 1) so it
+    // spreads over G times more SMs (B = 64: 1.7x on the large and medium nets, scripts/sync_group_sweep.py)
+    const int G = (!net->group_set && nb < (long long)net->d->gdef * net->sms) ? 1 : net->group;
+    const int gi = G == 1 ? 0 : 1;
     const long long slots = (nb + G - 1) / G;
     chaos_status s = ensure_partial(net, slots);
     if (s) return s;
@@ -613,7 +617,9 @@ chaos_status sync_batch(chaos_net* net, const float* X, const int32_t* Y, long l
     k.labels = Y;
     k.n = nb;
     k.loss_sum = loss_sum;
-    const int grid = grid_for(net, kSync, slots);
+    long long gsz = (long long)net->sms * net->occ[gi][kSync];
+    if (net->max_ctas > 0 && gsz > net->max_ctas) gsz = net->max_ctas;
+    const int grid = (int)std::max<long long>(1, std::min<long long>(gsz, slots));
 #ifdef CHAOS_TIMING
     if (net->ptime_grid < grid) {
         if (net->ptime) cudaFree(net->ptime);
@@ -624,7 +630,7 @@ chaos_status sync_batch(chaos_net* net, const float* X, const int32_t* Y, long l
     }
     k.ptime = net->ptime;  // accumulates over the epoch's batches (reset by a hogwild epoch)
 #endif
-    net->d->fn[gidx(net)][kSync]<<<grid, net->d->nt, net->d->smem[gidx(net)], net->stream>>>(k);
+    net->d->fn[gi][kSync]<<<grid, net->d->nt, net->d->smem[gi], net->stream>>>(k);
     CUDA_TRY(cudaGetLastError());
     const long long np = net->d->pint;
     chaos_reduce_update<<<(unsigned)((np + 255) / 256), 256, 0, net->stream>>>(net->params, net->partial, np,
@@ -742,6 +748,7 @@ chaos_status chaos_net_set_option(chaos_net* net, chaos_option opt, int64_t valu
             if (value != 1 && value != net->d->gdef)
                 return fail(CHAOS_E_INVALID, "group G must be 1 or %d for net %s", net->d->gdef, net->d->name);
             net->group = (int)value;
+            net->group_set = true;
             return CHAOS_OK;
         case CHAOS_OPT_MAX_CTAS:
             if (value < 0) return fail(CHAOS_E_INVALID, "max_ctas must be >= 0 (0 = all SMs)");

@@ -84,7 +84,7 @@ def test_forward_logits(name, group, torch_cuda):
 
 @pytest.mark.parametrize("name", NETS)
 @pytest.mark.parametrize("n", [1, 13])
-@pytest.mark.parametrize("group", [None, 4])
+@pytest.mark.parametrize("group", [None, 4])  # None: G unset, small batches run at G = 1
 def test_gradients(name, n, group, torch_cuda):
     # default G and G = 4 (the tiny / Table I small nets default to G = 1), each against the oracle
     o, net, p = make(name, 5, torch_cuda, group)
@@ -165,7 +165,7 @@ def test_sync_steps(name, torch_cuda):
 
 
 @pytest.mark.parametrize("name", NETS)
-@pytest.mark.parametrize("group", [None, 1])
+@pytest.mark.parametrize("group", [4, 1])  # explicit: an unset G runs these small batches at G = 1
 def test_exact_pool_ties(name, group, torch_cuda):
     # every pool window ties exactly (SURVEY C-14, first maximum in row-major order):
     # (a) all-zero weights -- every activation is 0; closed form: the output bias gradient is
