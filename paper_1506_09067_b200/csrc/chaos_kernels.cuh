@@ -74,6 +74,16 @@ struct DinRows<N, std::void_t<decltype(N::DINROWS)>> {
     static constexpr bool value = N::DINROWS;
 };
 
+// Nets whose conv1 forward splits its last partial pass into single-map sub-items declare TAIL1 = true
+template <class N, class = void>
+struct Tail1 {
+    static constexpr bool value = false;
+};
+template <class N>
+struct Tail1<N, std::void_t<decltype(N::TAIL1)>> {
+    static constexpr bool value = N::TAIL1;
+};
+
 // Nets whose conv3 / FC1 weights are too large to stage in shared memory (Table I large net,
 // SURVEY NEXT-1) declare BIGW = true: W1 + W2 are staged once per iteration and kept; conv3
 // and FC1 weights are read from L2 on demand.
@@ -581,7 +591,10 @@ __device__ __forceinline__ float warp_sum(float v) {
 // loads come from two images whose offsets differ by an odd-bank-shifting stride -- 2 x PL distinct
 // addresses in distinct banks (the windows-fastest order puts 16 windows of one image, 2 columns
 // apart, on 16 of the 32 banks: 2-way conflicts, profiles/r4)
-template <class L, int NT, bool MGF = false, int PL = 0>
+// TAIL: the items of the last, partial pass of NT threads are split into single-map sub-items spread
+// over all threads (the large net's conv1: 1,352 items on 640 threads left a third pass of 72 items,
+// 11% of the threads busy for a whole pass)
+template <class L, int NT, bool MGF = false, int PL = 0, bool TAIL = false>
 __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const float* __restrict__ wsm,
                                          float* __restrict__ out, uint8_t* __restrict__ am, int cnt) {
     constexpr int MT = L::MT, KP = L::KP, K = L::K, PW = L::PW, P = L::P, MG = L::M / MT;
@@ -595,7 +608,9 @@ __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const flo
     constexpr int NPB = PL > 0 ? (P + PL - 1) / PL : 1;         // window blocks
     constexpr int NMB = (MG + MGL - 1) / MGL;                   // map-group blocks
     const int total = PL > 0 ? NMB * ((cnt + 1) / 2) * NPB * 32 : MG * cnt * P * NSPL;
-    for (int it = threadIdx.x; it < total; it += NT) {
+    static_assert(!TAIL || (PL == 0 && !MGF && NSPL == 1), "tail split: the windows-fastest item map");
+    const int full = TAIL ? total / NT * NT : total;
+    for (int it = threadIdx.x; it < full; it += NT) {
         int half, p, g, mg;
         if constexpr (PL > 0) {
             const int l = it & 31, r = it >> 5;
@@ -664,6 +679,47 @@ __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const flo
                     arg = q;
                 }
             const int o = g * L::OUT_SZ + (mg * MT + mt) * P + p;
+            out[o] = tanhf(best);
+            if constexpr (KP > 1) am[o] = static_cast<uint8_t>(arg);
+        }
+    }
+    if constexpr (TAIL) {
+        for (int st = threadIdx.x; st < (total - full) * MT; st += NT) {
+            const int it = full + st / MT, mt = st % MT;
+            const int p = it % P, t = it / P, g = t % cnt, m = (t / cnt) * MT + mt;
+            const int pr = p / PW, pc = p - (p / PW) * PW;
+            float acc[KP * KP];
+#pragma unroll
+            for (int q = 0; q < KP * KP; ++q) acc[q] = wsm[L::WFL + m];
+            const float* ib = in + g * L::IN_SZ + (pr * KP) * L::W + pc * KP;
+#pragma unroll 1
+            for (int n = 0; n < L::C; ++n) {
+                float patch[PS][PS];
+#pragma unroll
+                for (int u = 0; u < PS; ++u)
+#pragma unroll
+                    for (int v = 0; v < PS; ++v) patch[u][v] = ib[n * (L::H * L::W) + u * L::W + v];
+#pragma unroll
+                for (int i = 0; i < K; ++i)
+#pragma unroll
+                    for (int j = 0; j < K; ++j) {
+                        const float w = wsm[n * L::NS + (i * K + j) * L::MP + m];
+#pragma unroll
+                        for (int u = 0; u < KP; ++u)
+#pragma unroll
+                            for (int v = 0; v < KP; ++v)
+                                acc[u * KP + v] = fmaf(w, patch[u + i][v + j], acc[u * KP + v]);
+                    }
+            }
+            float best = acc[0];
+            int arg = 0;
+#pragma unroll
+            for (int q = 1; q < KP * KP; ++q)
+                if (acc[q] > best) {  // first strict maximum wins (R4)
+                    best = acc[q];
+                    arg = q;
+                }
+            const int o = g * L::OUT_SZ + m * P + p;
             out[o] = tanhf(best);
             if constexpr (KP > 1) am[o] = static_cast<uint8_t>(arg);
         }
@@ -3294,7 +3350,11 @@ __global__ void __launch_bounds__(NT, 1) chaos_worker(KArgs a0) {
 #define CHAOS_PL_C3 4
 #endif
         constexpr int PL1 = (NCONV >= 3 && !BIG && !CHAOS_MGF_C1 && C1::NSPL == 1 && (C1::IN_SZ & 1)) ? CHAOS_PL_C1 : 0;
-        conv_fwd<C1, NT, CHAOS_MGF_C1, PL1>(sS, wb, a1, am1, cnt);
+#ifndef CHAOS_TAIL_C1  // conv1 forward: split the last partial pass into single-map sub-items (1: every
+#define CHAOS_TAIL_C1 0  // net, for sweeps; else the nets that declare TAIL1 -- measured per net)
+#endif
+        constexpr bool TAIL1 = (CHAOS_TAIL_C1 || Tail1<Net>::value) && PL1 == 0 && !CHAOS_MGF_C1 && C1::NSPL == 1;
+        conv_fwd<C1, NT, CHAOS_MGF_C1, PL1, TAIL1>(sS, wb, a1, am1, cnt);
         float* alast = a1;
         if constexpr (NCONV >= 2) {
             fence_async_smem();

@@ -61,6 +61,7 @@ struct MediumNet {  // configs[2] = Table I medium
     // conv2 delta_in window row by window row, each (map, window) dispatched once (conv_din_rows):
     // 4.38 M vs 3.84 M samples/s (banded conv_din); the Table I small net (G = 1: one task) keeps conv_din
     static constexpr bool DINROWS = true;
+    static constexpr bool TAIL1 = true;  // conv1 forward tail split: 5.06 -> 5.13 M (large net: -0.5%, off)
     using C1 = Conv<1, 29, 29, 20, 4, 2, 10, 16, 16, 2>;
 #ifndef MEDIUM_C2_MT
 #define MEDIUM_C2_MT 4
