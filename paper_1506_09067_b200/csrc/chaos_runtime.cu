@@ -1011,13 +1011,13 @@ chaos_status host_epoch(chaos_net* net, const float* h_images, const int32_t* h_
         long long chunk = (n + 15) / 16;
         chunk = (chunk + 15) / 16 * 16;  // 16-image multiples keep the 16-B image alignment
         if (chunk < 2048) chunk = 2048;
-        // chunk edges: a ramp 512, 1024, ... up to `chunk`, so the copy exposed before the first
-        // claims is ~0.1 ms of PCIe time instead of a whole n/16 chunk (the rest overlaps training)
+        // chunk edges: a doubling ramp 512, 1024, 2048, ... so the copy exposed before the first claims
+        // is ~0.03 ms of PCIe time, and the copies (~50 GB/s) stay ahead of the training (~14 GB/s of
+        // images at 4 M samples/s) with few host calls (7 chunks for 60,000 images)
+        (void)chunk;
         std::vector<long long> edge{0};
-        for (long long sz = 512; edge.back() < (long long)n;) {
+        for (long long sz = 512; edge.back() < (long long)n; sz *= 2)
             edge.push_back(std::min<long long>(n, edge.back() + sz));
-            sz = std::min<long long>(chunk, sz * 2);
-        }
         const long long nch = (long long)edge.size() - 1;
         if (!net->ready) CUDA_TRY(cudaMalloc(&net->ready, sizeof(unsigned long long)));
         if (!net->ready_copied) CUDA_TRY(cudaEventCreateWithFlags(&net->ready_copied, cudaEventDisableTiming));
