@@ -218,6 +218,8 @@ chaos_status chaos_dist_average_buffer(chaos_net* net, float* d_buf, int64_t n, 
  * after all its rounds are applied on every replica; every replica must run the same launches
  * with the same armed rounds (collective), so the caller agrees the count (e.g. from the shortest
  * shard).  The final exact average after a launch is the caller's (chaos_dist_average / NCCL).
+ * A launch whose peers stop publishing (a dead rank) does not hang: after ~10 s of waiting it gives
+ * its remaining rounds up and the next synchronizing call returns CHAOS_E_CUDA ("waited").
  * chaos_pavg_setup: allocates this replica's exchange buffer (cudaMalloc, zeroed: snapshot ring +
  *   flags + checksums) for rank in [0, world), world <= 8, interval k >= 1 images, nslice slices
  *   (0 = the SM count; every replica must use the same value and the same arch).  Once per net.

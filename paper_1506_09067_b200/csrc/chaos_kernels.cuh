@@ -49,7 +49,7 @@ __host__ __device__ constexpr bool is_hog(int mode) { return mode == kHogwild ||
 // read (done count at its start / started count at its end), 4/5 the delta_in read (-1: the
 // forward read's values serve); [30] = worker (CTA), [31] = the worker's iteration.
 constexpr int kTraceRec = 32;
-enum Latch : int { kLatchLabel = 1, kLatchNonfinite = 2, kLatchPavg = 4 };
+enum Latch : int { kLatchLabel = 1, kLatchNonfinite = 2, kLatchPavg = 4, kLatchPavgTimeout = 8 };
 
 __host__ __device__ constexpr int round4(int x) { return (x + 3) / 4 * 4; }
 
@@ -2963,6 +2963,7 @@ __device__ __noinline__ void pavg_service(float* params, const PavgArgs* pp, uns
     const PavgArgs& p = *pp;
     const int R = p.R, me = p.rank, nslice = p.nslice, sfl = p.slice_fl;
     unsigned long long* sums = reinterpret_cast<unsigned long long*>(ctl + 4);
+    unsigned waits = 0;  // thread 0: consecutive waits
     for (;;) {
         if (threadIdx.x < 32) {
             const int ts = ctl[0], tap = ctl[1];
@@ -2991,7 +2992,15 @@ __device__ __noinline__ void pavg_service(float* params, const PavgArgs* pp, uns
         const int act = ctl[2];
         if (act == 0) break;
         if (act == 3) {
-            if (threadIdx.x == 0) __nanosleep(500);
+            // a peer that never publishes (a dead rank) would hang the launch: after ~10 s of waiting
+            // give the launch's remaining rounds up and latch the error (reported by the next sync)
+            if (threadIdx.x == 0) {
+                __nanosleep(500);
+                if (++waits > (1u << 24)) {
+                    atomicOr(p.latch, kLatchPavgTimeout);
+                    ctl[0] = ctl[1] = rounds;
+                }
+            }
         } else if (act == 1) {
             const unsigned t = r0 + static_cast<unsigned>(ctl[0]) + 1u;
             const int b = static_cast<int>(t % kPavgBufs);

@@ -471,6 +471,8 @@ chaos_status check_latch(chaos_net* net) {
         CUDA_TRY(cudaMemsetAsync(net->latch, 0, sizeof(int), net->stream));
         CUDA_TRY(cudaStreamSynchronize(net->stream));
         if (h & kLatchLabel) return fail(CHAOS_E_LABEL, "device: a label outside [0, %d)", kClasses);
+        if (h & kLatchPavgTimeout)
+            return fail(CHAOS_E_CUDA, "device: fused averaging waited > 10 s for a peer replica (rounds abandoned)");
         if (h & kLatchPavg)
             return fail(CHAOS_E_CUDA, "device: fused averaging read a peer snapshot whose checksum does not match");
         return fail(CHAOS_E_NONFINITE, "device: non-finite loss");

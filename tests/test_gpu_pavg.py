@@ -285,3 +285,27 @@ def test_ipc_exchange_buffers_between_processes(tmp_path, torch_cuda):
     outs = [p.communicate(timeout=240)[0] for p in procs]
     for r, (p, out) in enumerate(zip(procs, outs)):
         assert p.returncode == 0 and f"ipc ok {r}" in out, out[-2000:]
+
+
+def test_dead_peer_times_out_instead_of_hanging(torch_cuda):
+    # rank 0 of 2 whose peer never launches (a dead rank): the launch's rounds wait ~10 s, are given
+    # up, and the next synchronizing call reports the latched error -- no hang
+    import time
+
+    import torch
+    from paper_1506_09067_b200 import ChaosError, Net
+    a, b = Net(sd.ARCHS["large"], init_seed=1), Net(sd.ARCHS["large"], init_seed=2)
+    a.pavg_setup(0, 2, 256)
+    b.pavg_setup(1, 2, 256)
+    a.pavg_set_peer(1, b)
+    d = sd.prototype_dataset(1, 2000, 0)
+    X, Y = torch.from_numpy(d.x_train).cuda(), torch.from_numpy(d.y_train).cuda()
+    a.pavg_arm(3)
+    t = time.time()
+    a.train_epoch(X, Y, 0.001)
+    with pytest.raises(ChaosError, match="waited"):
+        a.sync()
+    assert time.time() - t < 120
+    assert np.isfinite(a.get_params()).all()
+    for net in (a, b):
+        net.close()
