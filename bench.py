@@ -39,8 +39,12 @@ FP32_PEAK_TFLOPS = N_SM * 128 * 2 * 1.965e9 / 1e12
 # the pools use, argmax-only backward (gW and delta_in), 2 FLOP per parameter for the update
 ALGO_FLOP = {"tiny": 202_990, "medium": 4_985_880, "large": 5_495_720,
              # Table I large (NEXT-1): 34,286,140 MAC (fwd 22,648,820; bwd 11,637,320) + 2 x 383,160
-             "paper_large": 69_338_600}
-KERNEL_NET = {"tiny": "TinyNet", "medium": "MediumNet", "large": "LargeNet", "paper_large": "PaperLargeNet"}
+             "paper_large": 69_338_600,
+             # Table I small (NEXT-1): fwd 160,330 MAC (conv 54,080 + 101,250, FC 4,500 + 500), argmax-only
+             # bwd 46,020 MAC (conv2 gW + delta_in 2 x 11,250, conv1 gW 13,520, FC 2 x 5,000) + 2 x 6,405
+             "paper_small": 425_510}
+KERNEL_NET = {"tiny": "TinyNet", "medium": "MediumNet", "large": "LargeNet", "paper_large": "PaperLargeNet",
+              "paper_small": "PaperSmallNet"}
 
 
 def env_rank():
@@ -187,7 +191,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--arch", default="large", choices=["tiny", "medium", "large", "paper_large"])
+    ap.add_argument("--arch", default="large", choices=["tiny", "medium", "large", "paper_small", "paper_large"])
     ap.add_argument("--k", type=int, default=K_AVG)
     ap.add_argument("--ref-images", type=int, default=400)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -6,7 +6,7 @@
 TAG=${1:-ev}
 O=gpurun_out/${TAG}
 bash scripts/gpu_round.sh $TAG
-for a in tiny medium paper_large; do
+for a in tiny medium paper_small paper_large; do
   timeout 600 python bench.py --arch $a --no-cpu-baseline > ${O}_bench_$a.json 2> ${O}_bench_$a.err; echo "bench $a rc=$?"
 done
 for v in "fused strong" "async strong" "fused weak" "interval weak"; do

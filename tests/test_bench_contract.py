@@ -42,3 +42,44 @@ def test_bench_flags_documented():
     for flag in ("--gpus", "--steps", "--warmup", "--impl", "--arch", "--mode", "--avg", "--comm", "--force-dist",
                  "--reserve-sms", "--k"):
         assert flag in out.stdout, flag
+
+
+def algorithmic_flop(layers, h=29, w=29, c=1):
+    """SURVEY §8(d) D-3, recomputed from the layer list alone: 2 FLOP per MAC of the forward conv
+    outputs the pools use and of the FC layers, of the argmax-only backward (conv weight gradients;
+    conv delta_in except the first conv layer; FC weight gradients and delta_in), plus 2 FLOP per
+    parameter for the update."""
+    fwd = bwd = params = 0
+    first_conv = True
+    i = 0
+    n_in = c * h * w
+    while i < len(layers):
+        kind, units, k, _ = layers[i]
+        if kind == 1:  # conv, then its pool
+            kp = layers[i + 1][2]
+            oh, ow = h - k + 1, w - k + 1
+            ph, pw = oh // kp, ow // kp
+            taps = c * k * k
+            fwd += ph * kp * pw * kp * units * taps
+            bwd += ph * pw * units * taps * (1 if first_conv else 2)
+            params += units * (taps + 1)
+            first_conv = False
+            c, h, w = units, ph, pw
+            n_in = c * h * w
+            i += 2
+        else:
+            fwd += n_in * units
+            bwd += 2 * n_in * units
+            params += units * (n_in + 1)
+            n_in = units
+            i += 1
+    return 2 * (fwd + bwd) + 2 * params
+
+
+def test_algorithmic_flop_table_matches_the_layer_lists():
+    # the roofline numerators in bench.py (ALGO_FLOP) against an independent recount from the archs
+    sys.path.insert(0, ROOT)
+    import bench
+    import synthdata as sd
+    for name, flop in bench.ALGO_FLOP.items():
+        assert algorithmic_flop(sd.ARCHS[name]) == flop, (name, algorithmic_flop(sd.ARCHS[name]), flop)
