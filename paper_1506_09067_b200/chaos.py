@@ -368,7 +368,9 @@ class Net:
         maps it (default: its own)."""
         p, b = C.c_void_p(), C.c_int64()
         if peer is None:
-            peer = self._pavg_rank
+            peer = getattr(self, "_pavg_rank", None)
+            if peer is None:
+                raise ValueError("pavg_setup has not been called on this net")
         _check(lib().chaos_pavg_exchange(self._h, int(peer), C.byref(p), C.byref(b)))
         return int(p.value), int(b.value)
 
