@@ -182,7 +182,7 @@ def run_reference(args):
                              "sample": f"{per_step} images of configs[3] per step, oracle float64, 1 thread",
                              **host_identity()},
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def main():
@@ -476,10 +476,30 @@ def main():
         line["fused_rounds"] = fused_rounds  # in-kernel averaging rounds inside the timed region
         line["config"]["pavg_comm_ctas"] = trainer.comm_ctas
         line["roofline"]["kernel"] = line["roofline"]["kernel"][:-1] + ",PAVG>"
-    print(json.dumps(line), flush=True)
+    emit(line)
     if distributed:
         dist.destroy_process_group()
 
 
+def _json_stdout():
+    """The JSON line is the only thing this script writes to stdout: file descriptor 1 is pointed at
+    stderr for the run (NCCL prints its version banner to the C-level stdout under NCCL_DEBUG=WARN /
+    VERSION), and the line goes to a duplicate of the original stdout."""
+    global _OUT
+    if "-h" in sys.argv or "--help" in sys.argv:
+        return
+    sys.stdout.flush()
+    _OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
+
+_OUT = None
+
+
+def emit(line):
+    print(json.dumps(line), file=_OUT or sys.stdout, flush=True)
+
+
 if __name__ == "__main__":
+    _json_stdout()
     main()
