@@ -297,6 +297,27 @@ def main():
             dist.barrier(device_ids=[local])
 
     lr = w.lr0
+    if distributed and (use_fused or use_async):
+        # the in-kernel / in-flight averaging has only ever run on one GPU (replica emulations): if
+        # its first step fails on ANY rank (a peer's rounds timing out is latched and raised by
+        # sync), every rank drops to the blocking K-interval NCCL averaging -- agreed collectively,
+        # before anything is timed -- and the line says so
+        bad = 0
+        try:
+            step(X, Y, lr)
+            net.sync()
+            if os.environ.get("CHAOS_BENCH_FAIL_WARMUP"):  # test hook: exercise the fallback
+                raise RuntimeError("CHAOS_BENCH_FAIL_WARMUP is set")
+        except Exception as e:  # noqa: BLE001
+            bad = 1
+            print(f"[bench] rank {rank}: {args.avg} averaging failed in warm-up: {e}", file=sys.stderr)
+        tb = torch.tensor([bad], dtype=torch.int64, device="cuda")
+        dist.all_reduce(tb, op=dist.ReduceOp.MAX)
+        if int(tb.item()):
+            args.avg = f"interval ({args.avg} failed in warm-up on some rank)"
+            use_fused = use_async = False
+            net.set_option(OPT_RESERVE_SMS, 0)
+            trainer._average(net.device_params())  # the same weights on every rank again
     for s in range(args.warmup):
         step(X, Y, lr * 0.9 ** s)
     net.sync()

@@ -558,6 +558,19 @@ __device__ __forceinline__ void load_vec(float (&v)[N], const float* p) {
     }
 }
 
+// Packed FP32 FMA (PTX fma.rn.f32x2, SASS FFMA2, sm_100+): (a0, a1) += (x0, x1) * s, each half the IEEE
+// fma of the scalar form (bitwise the same results), one issue slot for both.  Measured
+// (scripts/microbench/ffma2_rate.cu): the same 125 FMA/clk/SM peak as FFMA; a conv2-forward-shaped loop
+// on 640 threads 88.7 -> 105.9 FMA/clk/SM.
+#ifndef CHAOS_FFMA2
+#define CHAOS_FFMA2 1
+#endif
+__device__ __forceinline__ void fma_pair(float& a0, float& a1, float x0, float x1, float s) {
+    const float2 r = __ffma2_rn(make_float2(x0, x1), make_float2(s, s), make_float2(a0, a1));
+    a0 = r.x;
+    a1 = r.y;
+}
+
 // Sums 32 values across the warp's lanes at once (v[k] of every lane -> lane k): 16+8+4+2+1
 // shuffles; at each step a lane keeps the half of its values its lane bit selects.
 __device__ __forceinline__ float warp_transpose_sum(float (&v)[32], int lane) {
@@ -651,13 +664,26 @@ __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const flo
                 for (int j = 0; j < K; ++j) {
                     float wv[MT];
                     load_vec<MT, A4, A2>(wv, wb + n * L::NS + (i * K + j) * L::MP);
+                    if constexpr (CHAOS_FFMA2 && MT % 2 == 0) {
+                        // two maps per packed FMA (SASS FFMA2: the weight pair as loaded, the patch value
+                        // as its broadcast scalar operand): each half is the same IEEE fma, half the issue slots
 #pragma unroll
-                    for (int mt = 0; mt < MT; ++mt)
+                        for (int mt = 0; mt < MT; mt += 2)
 #pragma unroll
-                        for (int u = 0; u < KP; ++u)
+                            for (int u = 0; u < KP; ++u)
 #pragma unroll
-                            for (int v = 0; v < KP; ++v)
-                                acc[mt][u * KP + v] = fmaf(wv[mt], patch[u + i][v + j], acc[mt][u * KP + v]);
+                                for (int v = 0; v < KP; ++v)
+                                    fma_pair(acc[mt][u * KP + v], acc[mt + 1][u * KP + v], wv[mt], wv[mt + 1],
+                                             patch[u + i][v + j]);
+                    } else {
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                            for (int u = 0; u < KP; ++u)
+#pragma unroll
+                                for (int v = 0; v < KP; ++v)
+                                    acc[mt][u * KP + v] = fmaf(wv[mt], patch[u + i][v + j], acc[mt][u * KP + v]);
+                    }
                 }
         }
         if constexpr (NSPL == 2) {  // the two halves of an item sit in adjacent lanes

@@ -592,7 +592,8 @@ def test_two_rank_sync_emulated_matches_oracle(torch_cuda):
     assert_parity(runs[0], ref, o.blocks())
 
 
-@pytest.mark.parametrize("mode", ["hogwild", "sync", "hogwild_dist", "hogwild_dist_async", "hogwild_dist_chaoscomm"])
+@pytest.mark.parametrize("mode", ["hogwild", "sync", "hogwild_dist", "hogwild_dist_async", "hogwild_dist_chaoscomm",
+                                  "hogwild_dist_fallback"])
 def test_bench_line_contract(mode, torch_cuda):
     # bench.py's JSON line on one GPU: contract keys, roofline + cpu_baseline objects, e2e with host bytes
     import subprocess
@@ -608,7 +609,10 @@ def test_bench_line_contract(mode, torch_cuda):
         cmd += ["--avg", "async"]
     if mode == "hogwild_dist_chaoscomm":  # ... with the library's own communicator
         cmd += ["--comm", "chaos"]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root)
+    env = dict(os.environ)
+    if mode == "hogwild_dist_fallback":  # a failed first fused step: every rank drops to blocking intervals
+        env["CHAOS_BENCH_FAIL_WARMUP"] = "1"
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=root, env=env)
     assert out.returncode == 0, out.stderr[-3000:]
     d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
@@ -620,7 +624,10 @@ def test_bench_line_contract(mode, torch_cuda):
     assert d["e2e"]["h2d_bytes_per_step"] == 60000 * (841 + 1) * 4
     if mode == "hogwild":
         assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
-    if mode.startswith("hogwild_dist"):
+    if mode == "hogwild_dist_fallback":
+        assert d["config"]["averaging"].startswith("interval (fused failed") and d["collectives"] >= 58
+        assert d["eval"]["test_errors"] < 0.05 * d["eval"]["images"]
+    elif mode.startswith("hogwild_dist"):
         avg = "async" if mode == "hogwild_dist_async" else "fused"
         assert d["config"]["averaging"] == avg and d["collectives"] >= (2 if avg == "async" else 1)
         if avg == "fused":  # in-kernel rounds every K = 1,024 claimed images of the 60,000
