@@ -117,6 +117,9 @@ struct MgfC2<N, std::void_t<decltype(N::MGF2)>> {
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 
 // Convolution block: conv (valid, stride 1, C->M maps, KxK) -> tanh -> KPxKP max-pool (floor).
+#ifndef CHAOS_FFMA2  // bit mask of the loops that use it: 1 conv_fwd, 2 conv_din3, 4 conv_bwd_sparse's gradient,
+#define CHAOS_FFMA2 13  // 8 conv_gw_m, 16 conv_gw, 32 conv_din_gm, 64 conv_gw_wt (large net: 2 -7%, 16 -0.4%: off)
+#endif
 // Tuning knobs: MT maps per thread in the forward; TT taps per thread and GS split of the
 // (image, window) sum in the weight gradient; RB input rows per band in delta_in.
 // MPO > 0: the internal row pitch of W (default round4(M), 16-B rows).  An odd pitch puts the rows of
@@ -125,8 +128,11 @@ __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 // then reads weights with scalar (broadcast) loads.
 template <int C_, int H_, int W_, int M_, int K_, int KP_, int MT_, int TT_, int GS_, int RB_, int PB_ = 0,
           int MS_ = 0, bool UNUSED_ = false, bool DIN3_ = false, int GWIN_ = 0, bool DWIN_ = false, int NSPL_ = 1,
-          int MPO_ = 0, int NPAD_ = 0>
+          int MPO_ = 0, int NPAD_ = 0, int FF_ = -1>
 struct Conv {
+    // FF: which loops of this layer use packed FP32 FMAs (the CHAOS_FFMA2 site mask; -1: the default),
+    // measured per net: the few-warp Table I large worker loses 7% with them in its forward
+    static constexpr int FF = FF_ < 0 ? CHAOS_FFMA2 : FF_;
     static constexpr int C = C_, H = H_, W = W_, M = M_, K = K_, KP = KP_;
     static constexpr int OH = H - K + 1, OW = W - K + 1;
     static constexpr int PH = OH / KP, PW = OW / KP, P = PH * PW;
@@ -562,13 +568,50 @@ __device__ __forceinline__ void load_vec(float (&v)[N], const float* p) {
 // fma of the scalar form (bitwise the same results), one issue slot for both.  Measured
 // (scripts/microbench/ffma2_rate.cu): the same 125 FMA/clk/SM peak as FFMA; a conv2-forward-shaped loop
 // on 640 threads 88.7 -> 105.9 FMA/clk/SM.
-#ifndef CHAOS_FFMA2
-#define CHAOS_FFMA2 1
-#endif
 __device__ __forceinline__ void fma_pair(float& a0, float& a1, float x0, float x1, float s) {
     const float2 r = __ffma2_rn(make_float2(x0, x1), make_float2(s, s), make_float2(a0, a1));
     a0 = r.x;
     a1 = r.y;
+}
+
+// a[t] += x[t] * s for t in [0, N), packed in pairs (t, t + 1) starting at the first t whose flat
+// register-array index is even (par = parity of a[0]'s flat index in its array: every use of an array
+// pairs the same elements, so the compiler can keep them in aligned register pairs).  par and the
+// indices are compile-time constants after unrolling.
+template <int N, bool ON>
+__device__ __forceinline__ void fma_row(float* a, const float* x, float s, int par = 0) {
+    if constexpr (ON) {
+        if (par) a[0] = fmaf(x[0], s, a[0]);
+#pragma unroll
+        for (int t = 0; t + 1 < N; t += 2)
+            if (t + par + 1 < N) fma_pair(a[t + par], a[t + par + 1], x[t + par], x[t + par + 1], s);
+        if ((N - par) % 2) a[N - 1] = fmaf(x[N - 1], s, a[N - 1]);
+    } else {
+#pragma unroll
+        for (int t = 0; t < N; ++t) a[t] = fmaf(x[t], s, a[t]);
+    }
+}
+
+// One tap of the fused conv forward: acc[mt][u * KP + v] += wv[mt] * patch[u + i][v + j] for MT maps and
+// the KP x KP conv outputs of a window; two maps per packed FMA (the weight pair as loaded, the patch
+// value as the broadcast scalar operand), the last map of an odd MT alone.
+template <int MT, int KP, bool ON, int PS>
+__device__ __forceinline__ void fma_tap(float (&acc)[MT][KP * KP], const float (&wv)[MT], const float (&patch)[PS][PS],
+                                        int i, int j) {
+    constexpr int MT2 = ON ? MT / 2 * 2 : 0;
+#pragma unroll
+    for (int mt = 0; mt < MT2; mt += 2)
+#pragma unroll
+        for (int u = 0; u < KP; ++u)
+#pragma unroll
+            for (int v = 0; v < KP; ++v)
+                fma_pair(acc[mt][u * KP + v], acc[mt + 1][u * KP + v], wv[mt], wv[mt + 1], patch[u + i][v + j]);
+#pragma unroll
+    for (int mt = MT2; mt < MT; ++mt)
+#pragma unroll
+        for (int u = 0; u < KP; ++u)
+#pragma unroll
+            for (int v = 0; v < KP; ++v) acc[mt][u * KP + v] = fmaf(wv[mt], patch[u + i][v + j], acc[mt][u * KP + v]);
 }
 
 // Sums 32 values across the warp's lanes at once (v[k] of every lane -> lane k): 16+8+4+2+1
@@ -664,26 +707,7 @@ __device__ __forceinline__ void conv_fwd(const float* __restrict__ in, const flo
                 for (int j = 0; j < K; ++j) {
                     float wv[MT];
                     load_vec<MT, A4, A2>(wv, wb + n * L::NS + (i * K + j) * L::MP);
-                    if constexpr (CHAOS_FFMA2 && MT % 2 == 0) {
-                        // two maps per packed FMA (SASS FFMA2: the weight pair as loaded, the patch value
-                        // as its broadcast scalar operand): each half is the same IEEE fma, half the issue slots
-#pragma unroll
-                        for (int mt = 0; mt < MT; mt += 2)
-#pragma unroll
-                            for (int u = 0; u < KP; ++u)
-#pragma unroll
-                                for (int v = 0; v < KP; ++v)
-                                    fma_pair(acc[mt][u * KP + v], acc[mt + 1][u * KP + v], wv[mt], wv[mt + 1],
-                                             patch[u + i][v + j]);
-                    } else {
-#pragma unroll
-                        for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-                            for (int u = 0; u < KP; ++u)
-#pragma unroll
-                                for (int v = 0; v < KP; ++v)
-                                    acc[mt][u * KP + v] = fmaf(wv[mt], patch[u + i][v + j], acc[mt][u * KP + v]);
-                    }
+                    fma_tap<MT, KP, (L::FF & 1) != 0>(acc, wv, patch, i, j);
                 }
         }
         if constexpr (NSPL == 2) {  // the two halves of an item sit in adjacent lanes
@@ -1026,13 +1050,7 @@ __device__ __forceinline__ void conv_fwd_slab(const float* __restrict__ in, cons
                 for (int j = 0; j < K; ++j) {
                     float wv[MT];
                     load_vec<MT, true>(wv, wb + (i * K + j) * L::MP);
-#pragma unroll
-                    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-                        for (int u = 0; u < KP; ++u)
-#pragma unroll
-                            for (int v = 0; v < KP; ++v)
-                                acc[mt][u * KP + v] = fmaf(wv[mt], patch[u + i][v + j], acc[mt][u * KP + v]);
+                    fma_tap<MT, KP, (L::FF & 1) != 0>(acc, wv, patch, i, j);
                 }
         }
         if (n + 3 < L::C) {
@@ -1113,11 +1131,13 @@ __device__ __forceinline__ void conv_gw(const KArgs& a, int slot, const float* _
             if constexpr (KP > 1) arg = amg[pp];
             const int pr = pp / PW, pc = pp - (pp / PW) * PW;
             const float* base = ing + (pr * KP + arg / KP) * L::W + pc * KP + arg % KP;
+            float xv[TT];
 #pragma unroll
             for (int t = 0; t < TT; ++t) {
                 const int tap = tg * TT + t;
-                acc[t] = fmaf(d, base[(tap / K) * L::W + (tap % K)], acc[t]);
+                xv[t] = base[(tap / K) * L::W + (tap % K)];
             }
+            fma_row<TT, (L::FF & 16) != 0>(acc, xv, d);
             accb += d;
             if (++pp == P) {
                 pp = 0;
@@ -1226,10 +1246,12 @@ __device__ __forceinline__ void conv_gw_m(const KArgs& a, int slot, const float*
                     const float* base = inr + pc * KP + (av[pc] >> 1) * W + (av[pc] & 1);
                     accb += d;
 #pragma unroll
-                    for (int k = 0; k < NPT; ++k)
+                    for (int k = 0; k < NPT; ++k) {
+                        float xv[KK];
 #pragma unroll
-                        for (int t = 0; t < KK; ++t)
-                            acc[k][t] = fmaf(d, base[k * HW + (t / K) * W + (t % K)], acc[k][t]);
+                        for (int t = 0; t < KK; ++t) xv[t] = base[k * HW + (t / K) * W + (t % K)];
+                        fma_row<KK, (L::FF & 8) != 0>(acc[k], xv, d, (k * KK) & 1);
+                    }
                 }
             }
         }
@@ -1383,22 +1405,51 @@ __device__ __forceinline__ void conv_gw_wt(const KArgs& a, int slot, const float
                 for (int u = 0; u < BR; ++u)
 #pragma unroll
                     for (int v = 0; v < BC; ++v) blk[u][v] = ing[(pr * KP + u) * W + pc * KP + v];
+                if constexpr ((L::FF & 64) && NM % 2 == 0) {
+                    // two maps per packed FMA: the pair of masked deltas times the block value (broadcast
+                    // operand); every accumulator still sums (g, w, phase) in the scalar loop's order
+                    float dv[NM];
+                    int pv[NM];
 #pragma unroll
-                for (int q = 0; q < NM; ++q) {
-                    const float d = dpg[q * P + w];
-                    const int ph = amg[q * P + w];
-                    accb[q] += d;
+                    for (int q = 0; q < NM; ++q) {
+                        dv[q] = dpg[q * P + w];
+                        pv[q] = amg[q * P + w];
+                        accb[q] += dv[q];
+                    }
 #pragma unroll
                     for (int aa = 0; aa < KP; ++aa)
 #pragma unroll
                         for (int bb = 0; bb < KP; ++bb) {
-                            const float dq = (ph == aa * KP + bb) ? d : 0.f;
+                            float dq[NM];
+#pragma unroll
+                            for (int q = 0; q < NM; ++q) dq[q] = (pv[q] == aa * KP + bb) ? dv[q] : 0.f;
 #pragma unroll
                             for (int i = 0; i < KR; ++i)
 #pragma unroll
                                 for (int j = 0; j < K; ++j)
-                                    acc[q][i * K + j] = fmaf(dq, blk[aa + i][bb + j], acc[q][i * K + j]);
+#pragma unroll
+                                    for (int q = 0; q < NM; q += 2)
+                                        fma_pair(acc[q][i * K + j], acc[q + 1][i * K + j], dq[q], dq[q + 1],
+                                                 blk[aa + i][bb + j]);
                         }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < NM; ++q) {
+                        const float d = dpg[q * P + w];
+                        const int ph = amg[q * P + w];
+                        accb[q] += d;
+#pragma unroll
+                        for (int aa = 0; aa < KP; ++aa)
+#pragma unroll
+                            for (int bb = 0; bb < KP; ++bb) {
+                                const float dq = (ph == aa * KP + bb) ? d : 0.f;
+#pragma unroll
+                                for (int i = 0; i < KR; ++i)
+#pragma unroll
+                                    for (int j = 0; j < K; ++j)
+                                        acc[q][i * K + j] = fmaf(dq, blk[aa + i][bb + j], acc[q][i * K + j]);
+                            }
+                    }
                 }
             }
         }
@@ -1800,11 +1851,8 @@ __device__ __forceinline__ void conv_din_gm(const float* __restrict__ wg, const 
                         for (int i = 0; i < K; ++i) {
                             const int rr = (DLO + dr) * KP + ph / KP + i;
                             if (rr < 0 || rr >= RB) continue;  // compile-time after unrolling
-#pragma unroll
-                            for (int j = 0; j < K; ++j) {
-                                const int cc = pc * KP + ph % KP + j;
-                                acc[rr][cc] = fmaf(w[i * K + j], dq, acc[rr][cc]);
-                            }
+                            fma_row<K, (L::FF & 32) != 0>(&acc[rr][pc * KP + ph % KP], &w[i * K], dq,
+                                           (rr * static_cast<int>(sizeof(acc[0]) / sizeof(float)) + pc * KP + ph % KP) & 1);
                         }
                     }
                 }
@@ -1951,36 +1999,24 @@ __device__ __forceinline__ void conv_din3(const float* __restrict__ wsm, const f
                     for (int pc = 0; pc < PW; ++pc) {
                         const float d = dv[pc];
                         const int arg = av[pc];
+                        // a tap row's K products into K adjacent columns: packed pairs (fma_row)
+#define CHAOS_DIN3_PH(AA, BB)                     \
+    _Pragma("unroll") for (int i = 0; i < K; ++i) \
+        fma_row<K, (L::FF & 2) != 0>(&acc[(AA) + i][pc * KP + (BB)], &w[i * K], d, (((AA) + i) * WR + pc * KP + (BB)) & 1);
                         if (arg < 2) {  // warp-uniform two-level branch on the argmax phase
                             if (arg == 0) {
-#pragma unroll
-                                for (int i = 0; i < K; ++i)
-#pragma unroll
-                                    for (int j = 0; j < K; ++j)
-                                        acc[i][pc * KP + j] = fmaf(w[i * K + j], d, acc[i][pc * KP + j]);
+                                CHAOS_DIN3_PH(0, 0)
                             } else {
-#pragma unroll
-                                for (int i = 0; i < K; ++i)
-#pragma unroll
-                                    for (int j = 0; j < K; ++j)
-                                        acc[i][pc * KP + 1 + j] = fmaf(w[i * K + j], d, acc[i][pc * KP + 1 + j]);
+                                CHAOS_DIN3_PH(0, 1)
                             }
                         } else {
                             if (arg == 2) {
-#pragma unroll
-                                for (int i = 0; i < K; ++i)
-#pragma unroll
-                                    for (int j = 0; j < K; ++j)
-                                        acc[1 + i][pc * KP + j] = fmaf(w[i * K + j], d, acc[1 + i][pc * KP + j]);
+                                CHAOS_DIN3_PH(1, 0)
                             } else {
-#pragma unroll
-                                for (int i = 0; i < K; ++i)
-#pragma unroll
-                                    for (int j = 0; j < K; ++j)
-                                        acc[1 + i][pc * KP + 1 + j] =
-                                            fmaf(w[i * K + j], d, acc[1 + i][pc * KP + 1 + j]);
+                                CHAOS_DIN3_PH(1, 1)
                             }
                         }
+#undef CHAOS_DIN3_PH
                     }
                 }
             }
@@ -2440,9 +2476,9 @@ __device__ __forceinline__ void conv_bwd_sparse(const KArgs& a, int slot, const 
                     const float d = dvs[q * P + w];
                     const int ph = avs[q * P + w];
                     accb[q] += d;
-#define CHAOS_GW_PH(AA, BB)                                                                     \
-    _Pragma("unroll") for (int i = 0; i < K; ++i) _Pragma("unroll") for (int j = 0; j < K; ++j) \
-        acc[q][i * K + j] = fmaf(d, blk[(AA) + i][(BB) + j], acc[q][i * K + j]);
+#define CHAOS_GW_PH(AA, BB)                       \
+    _Pragma("unroll") for (int i = 0; i < K; ++i) \
+        fma_row<K, (L::FF & 4) != 0>(&acc[q][i * K], &blk[(AA) + i][(BB)], d, (q * KK + i * K) & 1);
                     if (ph < 2) {  // warp-uniform
                         if (ph == 0) {
                             CHAOS_GW_PH(0, 0)

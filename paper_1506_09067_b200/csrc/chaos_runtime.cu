@@ -42,7 +42,9 @@ struct TinyNet {  // configs[0], configs[1]: conv5 4x4 -> tanh -> pool2 -> FC 84
 #ifndef TINY_C1_TT
 #define TINY_C1_TT 16
 #endif
-    using C1 = Conv<1, 29, 29, 5, 4, 2, /*MT*/ 5, /*TT*/ TINY_C1_TT, /*GS*/ TINY_C1_GS, /*RB*/ 2>;
+    // FF = 16: packed FMAs in conv_gw only (24.04 -> 24.13 M samples/s; in the forward too: 23.99 M)
+    using C1 = Conv<1, 29, 29, 5, 4, 2, /*MT*/ 5, /*TT*/ TINY_C1_TT, /*GS*/ TINY_C1_GS, /*RB*/ 2, 0, 0, false, false, 0,
+                    false, 1, 0, 0, /*FF*/ 16>;
     using C2 = C1;
     using C3 = C1;
     using F1 = Full<845, 10, false>;
@@ -92,8 +94,11 @@ struct PaperSmallNet {  // Table I small: conv
 #define PSMALL_DINSPLIT 2
 #endif
     static constexpr int DINSPLIT = PSMALL_DINSPLIT;
-    using C1 = Conv<1, 29, 29, 5, 4, 2, /*MT*/ 5, /*TT*/ 16, /*GS*/ 32, /*RB*/ 2>;
-    using C2 = Conv<5, 13, 13, 10, 5, 3, /*MT*/ 2, /*TT*/ 25, /*GS*/ 1, /*RB*/ 3>;
+    // FF = 17: packed FMAs in the forward convolutions and conv_gw (6.68 -> 6.83 M samples/s)
+    using C1 = Conv<1, 29, 29, 5, 4, 2, /*MT*/ 5, /*TT*/ 16, /*GS*/ 32, /*RB*/ 2, 0, 0, false, false, 0, false, 1, 0, 0,
+                    /*FF*/ 17>;
+    using C2 = Conv<5, 13, 13, 10, 5, 3, /*MT*/ 2, /*TT*/ 25, /*GS*/ 1, /*RB*/ 3, 0, 0, false, false, 0, false, 1, 0, 0,
+                    /*FF*/ 17>;
     using C3 = C2;
     using F1 = Full<90, 50, true>;
     using F2 = Full<50, 10, false>;
@@ -104,7 +109,10 @@ struct LargeNet {  // configs[3], configs[4]
     // (delta_in) and 8-19 (weight gradient).  Tile sweeps: profiles/r1q.
     static constexpr int NCONV = 3, NFULL = 2, GDEF = 4, GINIT = 4, INFLIGHT = 592, NT = 640, SFL = 6400;
     static constexpr bool TRACE = true;
-    static constexpr bool MGF2 = true;  // conv2 forward: map groups fastest over the lanes (+0.3%)
+#ifndef LARGE_MGF2
+#define LARGE_MGF2 1
+#endif
+    static constexpr bool MGF2 = LARGE_MGF2;  // conv2 forward: map groups fastest over the lanes (+0.3%)
     static constexpr bool TC2 = true;   // conv2 forward on the tensor cores when built with CHAOS_C2_TC
     static constexpr bool REPL = true;  // replica-emulation build (fused cross-replica averaging tests)
     //                C   H   W   M   K  KP  MT  TT  GS  RB  PB  MS  (0)  DIN3  GWIN  DWIN  NSPL
@@ -144,9 +152,14 @@ struct PaperLargeNet {  // Table I large: conv
     static constexpr bool TRACE = false;
     static constexpr bool BIGW = true;
     //                C   H   W    M  K  KP  MT  TT  GS  RB  PB  MS  (0)  DIN3  GWIN  DWIN  NSPL
-    using C1 = Conv<1, 29, 29, 20, 4, 1, 10, 16, 16, 1>;
-    using C2 = Conv<20, 26, 26, 60, 5, 2, 10, 25, 1, 2>;
-    using C3 = Conv<60, 11, 11, 100, 6, 2, 4, 12, 1, 2>;
+    // FF = 96: packed FMAs in conv_din_gm and conv_gw_wt only (256.4 -> 261.8 k samples/s); with them in the
+    // forward convolutions too (12 warps: latency-bound) 239.9 k
+#ifndef PL_FF
+#define PL_FF 96
+#endif
+    using C1 = Conv<1, 29, 29, 20, 4, 1, 10, 16, 16, 1, 0, 0, false, false, 0, false, 1, 0, 0, PL_FF>;
+    using C2 = Conv<20, 26, 26, 60, 5, 2, 10, 25, 1, 2, 0, 0, false, false, 0, false, 1, 0, 0, PL_FF>;
+    using C3 = Conv<60, 11, 11, 100, 6, 2, 4, 12, 1, 2, 0, 0, false, false, 0, false, 1, 0, 0, PL_FF>;
     using F1 = Full<900, 150, true>;
     using F2 = Full<150, 10, false>;
 };

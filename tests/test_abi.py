@@ -87,7 +87,10 @@ def test_bench_kernels_do_not_spill():
         pytest.skip("cuobjdump or libchaos.so missing")
     out = subprocess.run(["cuobjdump", "--dump-resource-usage", LIB_PATH], capture_output=True, text=True).stdout
     fns = re.findall(r"Function (\S+):\s*\n\s*(REG:\d+ STACK:\d+)", out)
-    large = [(f, r) for f, r in fns if "chaos_worker" in f and "LargeNetELi4ELi640" in f and "PaperLarge" not in f]
+    # (mode 4 = kTrace, the schedule-recording debug instantiation, is not a bench kernel: its trace
+    # stores cost it an 8-byte frame since the forward convolutions pair their accumulators)
+    large = [(f, r) for f, r in fns if "chaos_worker" in f and "LargeNetELi4ELi640" in f and "PaperLarge" not in f
+             and "LargeNetELi4ELi640ELi4E" not in f]
     assert len(large) >= 7, len(large)
     for f, r in large:
         assert r.endswith("STACK:0"), (f, r)
