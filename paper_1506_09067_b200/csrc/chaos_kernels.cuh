@@ -117,7 +117,7 @@ struct MgfC2<N, std::void_t<decltype(N::MGF2)>> {
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 
 // Convolution block: conv (valid, stride 1, C->M maps, KxK) -> tanh -> KPxKP max-pool (floor).
-#ifndef CHAOS_FFMA2  // bit mask of the loops that use it: 1 conv_fwd, 2 conv_din3, 4 conv_bwd_sparse's gradient,
+#ifndef CHAOS_FFMA2  // bit mask of the loops that use it: 1 conv_fwd, (2: conv_din3, removed) 4 conv_bwd_sparse's gradient,
 #define CHAOS_FFMA2 13  // 8 conv_gw_m, 16 conv_gw, 32 conv_din_gm, 64 conv_gw_wt (large net: 2 -7%, 16 -0.4%: off)
 #endif
 // Tuning knobs: MT maps per thread in the forward; TT taps per thread and GS split of the
@@ -1999,10 +1999,12 @@ __device__ __forceinline__ void conv_din3(const float* __restrict__ wsm, const f
                     for (int pc = 0; pc < PW; ++pc) {
                         const float d = dv[pc];
                         const int arg = av[pc];
-                        // a tap row's K products into K adjacent columns: packed pairs (fma_row)
-#define CHAOS_DIN3_PH(AA, BB)                     \
-    _Pragma("unroll") for (int i = 0; i < K; ++i) \
-        fma_row<K, (L::FF & 2) != 0>(&acc[(AA) + i][pc * KP + (BB)], &w[i * K], d, (((AA) + i) * WR + pc * KP + (BB)) & 1);
+                        // (packed FMAs measured slower here, twice: the pairing taps differ by phase -- written
+                        // naively 3.94 M, with the taps (1, 2) loaded a second time into their own pair slots
+                        // 3.98 M, vs 4.25 M scalar; DESIGN.md §7 session 5)
+#define CHAOS_DIN3_PH(AA, BB)                                                                   \
+    _Pragma("unroll") for (int i = 0; i < K; ++i) _Pragma("unroll") for (int j = 0; j < K; ++j) \
+        acc[(AA) + i][pc * KP + (BB) + j] = fmaf(w[i * K + j], d, acc[(AA) + i][pc * KP + (BB) + j]);
                         if (arg < 2) {  // warp-uniform two-level branch on the argmax phase
                             if (arg == 0) {
                                 CHAOS_DIN3_PH(0, 0)
