@@ -94,3 +94,20 @@ def test_bench_kernels_do_not_spill():
     assert len(large) >= 7, len(large)
     for f, r in large:
         assert r.endswith("STACK:0"), (f, r)
+
+
+def test_bench_kernel_uses_packed_fp32_fma():
+    # DESIGN.md §7 session 5: the large net's forward convolutions and two of its gradients run on sm_100's
+    # packed FP32 FMA (SASS FFMA2, two fused multiply-adds per issue slot).  nvcc never forms it from
+    # scalar code, so a refactor that drops fma_pair would silently cost 3.5%: check the bench kernel's SASS
+    import shutil
+    import subprocess
+    from paper_1506_09067_b200.chaos import LIB_PATH
+    if not shutil.which("cuobjdump") or not os.path.exists(LIB_PATH):
+        pytest.skip("cuobjdump or libchaos.so missing")
+    out = subprocess.run(["cuobjdump", "--dump-resource-usage", LIB_PATH], capture_output=True, text=True).stdout
+    fn = [f for f in re.findall(r"Function (\S+):", out) if "chaos_worker" in f and "LargeNetELi4ELi640ELi0ELb0ELb0ELb0" in f]
+    assert len(fn) == 1, fn
+    sass = subprocess.run(["cuobjdump", "-sass", "-fun", fn[0], LIB_PATH], capture_output=True, text=True).stdout
+    n2, n1 = len(re.findall(r"\bFFMA2\b", sass)), len(re.findall(r"\bFFMA\b", sass))
+    assert n2 >= 500 and n1 >= 500, (n2, n1)  # packed forward / sparse gradients, scalar delta_in and FC
