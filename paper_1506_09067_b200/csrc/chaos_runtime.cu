@@ -65,11 +65,13 @@ struct MediumNet {  // configs[2] = Table I medium
     static constexpr bool DINROWS = true;
     static constexpr bool TAIL1 = true;  // conv1 forward tail split: 5.06 -> 5.13 M (large net: -0.5%, off)
     using C1 = Conv<1, 29, 29, 20, 4, 2, 10, 16, 16, 2>;
+    // conv2 forward: 8 maps per item with the input maps split over two adjacent lanes (session 5, packed
+    // FMAs: 5.181 -> 5.204 M samples/s; MT 8 / 10 / 5 unsplit 4.59 / 4.34 / 4.79 M, MT 4 split 4.96 M)
 #ifndef MEDIUM_C2_MT
-#define MEDIUM_C2_MT 4
+#define MEDIUM_C2_MT 8
 #endif
 #ifndef MEDIUM_C2_NSPL
-#define MEDIUM_C2_NSPL 1
+#define MEDIUM_C2_NSPL 2
 #endif
 #ifndef MEDIUM_C2_RB  // conv2 delta_in: input rows per band task
 #define MEDIUM_C2_RB 3
