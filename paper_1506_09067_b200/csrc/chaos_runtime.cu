@@ -131,14 +131,17 @@ struct LargeNet {  // configs[3], configs[4]
 #ifndef LARGE_C2_MT  // conv2 forward: output maps per thread item
 #define LARGE_C2_MT 10
 #endif
-#ifndef LARGE_C3_MT  // conv3 forward: output maps per thread item
-#define LARGE_C3_MT 4
-#endif
+#ifndef LARGE_C3_MT  // conv3 forward: output maps per thread item (session 5, packed FMAs: 10 maps with the input
+#define LARGE_C3_MT 10  // maps split over two adjacent lanes, 320 half-items: 25.6k -> 23.5k cycles, 4.252 -> 4.275 M;
+#endif               // MT 4 / 5 split 4.15 / 4.16 M, MT 10 unsplit 4.21 M, MT 10 split + map groups fastest 4.07 M)
     using C2 = Conv<20, 13, 13, 60, 3, 2, LARGE_C2_MT, 9, 1, 4, LARGE_C2_PB, -1, false, true, 0, false, 1>;
 #ifndef LARGE_C3_NPAD  // conv3 W: floats of padding per input map (NS = 404: NS / 4 odd)
 #define LARGE_C3_NPAD 4
 #endif
-    using C3 = Conv<60, 5, 5, 100, 2, 2, LARGE_C3_MT, 4, 1, 5, 2, 0, false, false, 4, true, 1, 0, LARGE_C3_NPAD>;
+#ifndef LARGE_C3_NSPL  // conv3 forward: input maps of an item split over this many adjacent lanes
+#define LARGE_C3_NSPL 2
+#endif
+    using C3 = Conv<60, 5, 5, 100, 2, 2, LARGE_C3_MT, 4, 1, 5, 2, 0, false, false, 4, true, LARGE_C3_NSPL, 0, LARGE_C3_NPAD>;
     using F1 = Full<400, 150, true>;
     using F2 = Full<150, 10, false>;
 };
